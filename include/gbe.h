@@ -1,0 +1,240 @@
+/* gbe.h — C ABI of the B200 bucket-elimination library (libgbe.so).
+ *
+ * The library computes the (mini-)bucket / UTIL-message tables of Bucket
+ * Elimination, Mini-Bucket Elimination and DPOP on an NVIDIA B200 (sm_100a)
+ * with hand-written CUDA kernels.  Citations: P:n = line n of PAPER.md
+ * (arXiv 1608.05288, Fioretto, Pontelli, Yeoh, Dechter), S:n = line n of
+ * SPEC.md.  Readings of ambiguous passages (A1..A17) are listed in DESIGN.md.
+ *
+ * Conventions (all calls):
+ *   - Every call returns a gbe_status; on failure gbe_last_error() returns a
+ *     thread-local message (e.g. "bucket x17: 3.49e9 rows > budget").  No
+ *     partial results are written on failure unless stated.
+ *   - The caller owns every host array passed in or out; outputs are
+ *     caller-allocated with the documented sizes.  The library copies what it
+ *     keeps.  Opaque handles are freed only by the matching *_destroy.
+ *   - `stream` is a cudaStream_t cast to void* (NULL = legacy default stream).
+ *   - Variables are 0..n-1.  An ordering lists the variables from the first
+ *     (root side, lowest priority) to the last; BE eliminates from
+ *     order[n-1] down to order[0] (Alg. 1).
+ *   - Tables are flat, lexicographic, first scope variable most significant
+ *     (bucket-table).  Original functions are given in their
+ *     declared scope order; every table the library produces has its scope
+ *     sorted by ascending order position (root side most significant, A2).
+ *   - Integer costs: int32 with infinity = GBE_INF_I32 = 2^30 ("R+ u {inf}",
+ *     P:118); every aggregation clamps at infinity (A9).  Float64 costs are
+ *     IEEE doubles (MPE stored as -log p, A10), +inf = forbidden.
+ *   - Infeasible instances are not errors: the optimum is returned with
+ *     is_inf = 1.
+ */
+#ifndef GBE_H
+#define GBE_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GBE_INF_I32 (1 << 30)
+#define GBE_MAX_SEP 40    /* output-scope variables of one bucket            */
+#define GBE_MAX_INPUTS 32 /* input tables of one (mini-)bucket               */
+#define GBE_MAX_DOMAIN 256 /* argmins are stored as uint8                    */
+
+typedef enum {
+  GBE_OK = 0,
+  GBE_E_INVALID = 1, /* bad argument, i-bound below a member arity */
+  GBE_E_PARSE = 2,   /* file parse error; message carries the line */
+  GBE_E_BUDGET = 3,  /* plan exceeds the memory budget; names the bucket */
+  GBE_E_CUDA = 4,    /* CUDA runtime / kernel failure, or no device */
+  GBE_E_COMM = 5,    /* collective hook failed */
+  GBE_E_INTERNAL = 6
+} gbe_status;
+
+/* Semiring of the aggregate/eliminate operators.
+ * MPE is solved as min-sum over -log p in float64 (A10). */
+typedef enum { GBE_MINSUM_I32 = 0, GBE_MINSUM_F64 = 1 } gbe_semiring;
+
+typedef enum {
+  GBE_ORDER_MINFILL = 0,      /* greedy min-fill, ties (fill, degree, id) (A3) */
+  GBE_ORDER_PAPER_DEGREE = 1, /* x_i < x_j iff |N(x_i)| < |N(x_j)|, ties by id */
+  GBE_ORDER_GIVEN = 2         /* `given` is validated and copied */
+} gbe_order_kind;
+
+/* A cost value: is_inf = 1 means infinity; i holds int32-semiring values,
+ * f holds float64 ones (the other field is 0). */
+typedef struct {
+  int32_t is_inf;
+  int64_t i;
+  double f;
+} gbe_value;
+
+typedef struct gbe_problem gbe_problem; /* immutable after creation     */
+typedef struct gbe_plan gbe_plan;       /* ordering, (mini-)buckets, layouts,
+                                           stride maps, shard plan            */
+typedef struct gbe_run gbe_run;         /* device-resident UTIL messages/argmins */
+
+/* ---------------------------------------------------------------------
+ * Problems: WCSP <X,D,C>, DCOP = WCSP + identity agent map
+ * (P:416-417), belief network CPTs for MPE.
+ * ------------------------------------------------------------------- */
+
+/* n variables with domain sizes dom[n] (1 <= dom <= GBE_MAX_DOMAIN); nf
+ * functions, function f has arity[f] variables listed consecutively in
+ * `scopes` (declared order) and prod(dom over its scope) consecutive costs in
+ * `costs` (int32 for GBE_MINSUM_I32, double for GBE_MINSUM_F64).
+ * Errors: GBE_E_INVALID (bad ids, duplicate scope variable, negative cost,
+ * sum of the largest finite entries >= 2^30 for int32). */
+gbe_status gbe_problem_create(int32_t n, const int32_t *dom, int32_t nf,
+                              const int32_t *arity, const int32_t *scopes,
+                              gbe_semiring sr, const void *costs, gbe_problem **out);
+
+/* WCSP text format: `name n maxdom nf ub`, n domain sizes, then per
+ * function `arity vars... default ntuples` and ntuples lines `vals... cost`;
+ * costs >= ub are infinity.  GBE_E_PARSE with the line number on error. */
+gbe_status gbe_problem_load_wcsp(const char *path, gbe_problem **out);
+
+/* UAI BAYES/MARKOV model; tables are probabilities, stored as
+ * -log p (p = 0 -> +inf).  `evid` (NULL ok): `count var val ...`; evidence
+ * variables are conditioned by slicing; out-of-domain evidence ->
+ * GBE_E_INVALID. */
+gbe_status gbe_problem_load_uai(const char *model, const char *evid, gbe_problem **out);
+
+/* Synthetic instances (§8.1) from a JSON
+ * object, e.g. {"topology":"scalefree","n":200,"d":3,"p2":0,"seed":5}.
+ * topology: "random" (n,d,edges,mode), "scalefree" (n,d), "grid"
+ * (rows,cols,d), "bn" (n,dmin,dmax,maxpar,window), "network" (n,dmin,dmax,
+ * nf,amin,amax,cmax).  Uses the shared seeded generator module gen/. */
+gbe_status gbe_generate(const char *json_cfg, gbe_problem **out);
+
+/* sizes of a problem */
+gbe_status gbe_problem_info(const gbe_problem *p, int32_t *n, int32_t *nf,
+                            gbe_semiring *sr);
+
+void gbe_problem_destroy(gbe_problem *p);
+
+/* Cost of a complete assignment assign[n] (Eq. 1); MPE: sum of -log p. */
+gbe_status gbe_evaluate(const gbe_problem *p, const int32_t *assign, gbe_value *out);
+
+/* ---------------------------------------------------------------------
+ * Structure: ordering / induced width, pseudo-tree
+ * ------------------------------------------------------------------- */
+
+/* order_out[n] receives the ordering; width_out (NULL ok) its induced width. */
+gbe_status gbe_order(const gbe_problem *p, gbe_order_kind kind, const int32_t *given,
+                     int32_t *order_out, int32_t *width_out);
+
+/* Pseudo-tree of `order` = its elimination tree (A14): parent_out[v] is the
+ * latest-ordered variable of v's UTIL-message scope (-1 for a root), and
+ * sep_size_out[v] (NULL ok) = |sep(v)|.  Every primal edge joins an ancestor
+ * and a descendant. */
+gbe_status gbe_pseudotree(const gbe_problem *p, const int32_t *order,
+                          int32_t *parent_out, int32_t *sep_size_out);
+
+/* ---------------------------------------------------------------------
+ * Plans and solves
+ * ------------------------------------------------------------------- */
+
+/* Plan BE (ibound < 0) or MBE(ibound) (Alg. 2; i-bound = maximum arity of a
+ * generated function, |mini-bucket scope union| <= ibound + 1, reading A5;
+ * greedy first-fit partition, reading A6).  json_exec (NULL ok):
+ *   {"device":0, "budget_bytes":N, "world_size":W, "rank":r,
+ *    "shard_min_rows":N, "retain":"none"|"args"|"all", "timing":true}
+ * "retain":"all" keeps every table on the device for gbe_run_table().
+ * Errors: GBE_E_INVALID (bad order, i-bound < member arity - 1),
+ * GBE_E_BUDGET (names the bucket and its rows). */
+gbe_status gbe_plan_create(const gbe_problem *p, const int32_t *order, int32_t ibound,
+                           const char *json_exec, gbe_plan **out);
+
+/* Plan description as JSON into buf[cap] (tables: var, mini-bucket, sep,
+ * rows, inputs, dest, shard range; totals: cells, algorithmic bytes). */
+gbe_status gbe_plan_info(const gbe_plan *plan, char *buf, size_t cap);
+
+void gbe_plan_destroy(gbe_plan *plan);
+
+/* Exact BE (Alg. 1 / Alg. 3 with no partition): uploads the original tables
+ * (one batched H2D), runs one bucket kernel per bucket with device-resident
+ * messages, then the value phase; blocks until done.  opt = optimum,
+ * assign_out[n] = the assignment (smallest-index tie-break, A8).  stats_json
+ * (NULL ok) receives per-bucket timings when the plan has "timing":true. */
+gbe_status gbe_solve_be(gbe_plan *plan, void *stream, gbe_value *opt, int32_t *assign_out,
+                        char *stats_json, size_t cap);
+
+/* MBE(i) (Alg. 2): lower = sum of constants; upper = evaluate(assignment);
+ * the value phase minimises the sum of all mini-bucket functions (A7). */
+gbe_status gbe_solve_mbe(gbe_plan *plan, void *stream, gbe_value *lower, gbe_value *upper,
+                         int32_t *assign_out, char *stats_json, size_t cap);
+
+/* DPOP UTIL phase on the plan's pseudo-tree: UTIL messages are the
+ * bucket functions (Thm 1); siblings run concurrently.  The run
+ * keeps the argmin tables for the VALUE phase.  root_util = optimum. */
+gbe_status gbe_dpop_util(gbe_plan *plan, void *stream, gbe_run **run_out,
+                         gbe_value *root_util);
+/* DPOP VALUE phase: assign_out[n]. */
+gbe_status gbe_dpop_value(gbe_run *run, int32_t *assign_out);
+/* statistics of a run as JSON (per-bucket kernel ms, cells, bytes) */
+gbe_status gbe_run_stats(const gbe_run *run, char *buf, size_t cap);
+/* copy table t (creation order, as in gbe_plan_info) to host; needs
+ * "retain":"all".  host_out: rows * (4 or 8) bytes; host_arg: rows bytes
+ * (either may be NULL).  Only rows owned by this rank are written. */
+gbe_status gbe_run_table(const gbe_run *run, int32_t t, void *host_out, uint8_t *host_arg);
+void gbe_run_destroy(gbe_run *run);
+
+/* ---------------------------------------------------------------------
+ * The hot primitive: one (mini-)bucket, Alg. 1 line 3 / Alg. 2 line 5.
+ * out[r - row_begin] = min_v ⊕_j T_j[off_j(r) + v],  arg = first minimiser,
+ * where off_j(r) = sum_p digit_p(r) * stride[j][p] - shift[j] and digit_p(r)
+ * is the mixed-radix decomposition of r over radix[0..nsep) (radix[0] most
+ * significant).  This restates the index map Eq. with strides
+ * precomputed per input (the "mul/div/mod" vectors) and fuses Gpu::
+ * Aggregate (Proc. 4) with Gpu::Eliminate (Proc. 5):
+ * the d^{|sep|+1} aggregated table is never materialised.
+ * ------------------------------------------------------------------- */
+typedef struct gbe_bucket_desc {
+  int32_t semiring;              /* gbe_semiring                                  */
+  int32_t nsep;                  /* output scope size m (0 = one output row)      */
+  int32_t d;                     /* domain size of the eliminated variable         */
+  int32_t ninputs;               /* k, 0 <= k <= GBE_MAX_INPUTS                    */
+  int64_t rows;                  /* prod(radix) = R                               */
+  int32_t radix[GBE_MAX_SEP];    /* output digit radices, [0] most significant     */
+  int64_t stride[GBE_MAX_INPUTS][GBE_MAX_SEP]; /* element stride of output digit p
+                                    in input j; 0 if the variable is absent.  The
+                                    eliminated variable has stride 1 in every input */
+  int64_t shift[GBE_MAX_INPUTS]; /* subtracted from every offset of input j (row-
+                                    sharded inputs: first local element)           */
+} gbe_bucket_desc;
+
+/* desc: HOST pointer; dev_inputs[k]: device pointers to int32 or double tables;
+ * dev_out: device array of (row_end - row_begin) int32/double; dev_arg: device
+ * uint8 array of the same length or NULL.  Asynchronous on `stream`.
+ * Errors: GBE_E_INVALID (sizes, d > 256, k > GBE_MAX_INPUTS), GBE_E_CUDA. */
+gbe_status gbe_bucket_kernel(const void *desc, const void *const *dev_inputs, void *dev_out,
+                             uint8_t *dev_arg, int64_t row_begin, int64_t row_end,
+                             void *stream);
+
+/* ---------------------------------------------------------------------
+ * Hooks
+ * ------------------------------------------------------------------- */
+/* Device memory: alloc(bytes, stream, u) / free(ptr, u).  Default:
+ * cudaMallocAsync / cudaFreeAsync on the solve stream. NULL restores it. */
+gbe_status gbe_set_allocator(void *(*alloc_fn)(size_t, void *stream, void *u),
+                             void (*free_fn)(void *, void *u), void *u);
+
+/* All-gather of a row-sharded message among the plan's world_size ranks:
+ * every rank contributes `bytes` from `send` and receives world_size * bytes
+ * into `recv` (rank-major).  Return 0 on success.  Needed only when a plan has
+ * world_size > 1.  NULL removes the hook. */
+gbe_status gbe_set_allgather(int (*ag)(const void *send, void *recv, size_t bytes,
+                                       void *stream, void *u),
+                             void *u);
+
+/* Thread-local message of the last failing call ("" if none). */
+const char *gbe_last_error(void);
+
+/* Library version string. */
+const char *gbe_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

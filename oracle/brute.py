@@ -1,0 +1,112 @@
+"""Pure-Python brute force for tiny instances (TEST INFRASTRUCTURE ONLY).
+
+Enumerates the whole state space Sigma of Eq. (1) (MPE Eq. (2),
+P:388-391, as min-sum over -log p) in lexicographic order of a given ordering
+(order[0] most significant) and returns the optimum together with the
+lexicographically smallest optimal assignment under that ordering.  No
+elimination, no tables: the plain definition of the optimum.
+"""
+from __future__ import annotations
+
+import itertools
+
+INF_I32 = 1 << 30
+
+
+def _cost(inst, assign):
+    if inst.is_f64:
+        s = 0.0
+        for f in range(inst.nf):
+            sc = inst.scope(f)
+            idx = 0
+            for v in sc:
+                idx = idx * int(inst.dom[v]) + assign[int(v)]
+            s = s + float(inst.costs[inst.table_off[f] + idx])
+        return s
+    s = 0
+    for f in range(inst.nf):
+        sc = inst.scope(f)
+        idx = 0
+        for v in sc:
+            idx = idx * int(inst.dom[v]) + assign[int(v)]
+        s = min(s + int(inst.costs[inst.table_off[f] + idx]), INF_I32)
+    return s
+
+
+def brute_force(inst, order=None, limit=2_000_000):
+    """Returns (optimum, assignment).  Ties: the first optimum met in
+    lexicographic order of `order` (default: identity)."""
+    n = inst.n
+    order = list(range(n)) if order is None else [int(v) for v in order]
+    space = 1
+    for v in order:
+        space *= int(inst.dom[v])
+    if space > limit:
+        raise ValueError(f"state space {space} exceeds brute-force limit {limit}")
+    best, best_a = None, None
+    assign = [0] * n
+    for vals in itertools.product(*[range(int(inst.dom[v])) for v in order]):
+        for v, val in zip(order, vals):
+            assign[v] = val
+        c = _cost(inst, assign)
+        if best is None or c < best:
+            best, best_a = c, list(assign)
+    if best is None:  # n == 0
+        best, best_a = (0.0 if inst.is_f64 else 0), []
+        best = _cost(inst, [])
+    return best, best_a
+
+
+def mpe_linear(inst, order=None, limit=2_000_000):
+    """MPE in the linear domain: max over Sigma of prod_f exp(-cost) (Eq. 2),
+    computed as a product of probabilities (not a log-sum)."""
+    import math
+    n = inst.n
+    order = list(range(n)) if order is None else [int(v) for v in order]
+    best = -1.0
+    assign = [0] * n
+    for vals in itertools.product(*[range(int(inst.dom[v])) for v in order]):
+        for v, val in zip(order, vals):
+            assign[v] = val
+        p = 1.0
+        for f in range(inst.nf):
+            idx = 0
+            for v in inst.scope(f):
+                idx = idx * int(inst.dom[v]) + assign[int(v)]
+            p *= math.exp(-float(inst.costs[inst.table_off[f] + idx]))
+        if p > best:
+            best = p
+    return best
+
+
+def brute_force_np(inst, order=None, limit=50_000_000):
+    """Vectorised brute force (same definition as brute_force): enumerates
+    every assignment in lexicographic order of `order`, sums every function
+    (int: clamp at 2^30; f64: in function-index order), returns the first
+    minimum."""
+    import numpy as np
+    n = inst.n
+    order = list(range(n)) if order is None else [int(v) for v in order]
+    dims = [int(inst.dom[v]) for v in order]
+    space = int(np.prod(dims, dtype=np.int64)) if dims else 1
+    if space > limit:
+        raise ValueError(f"state space {space} exceeds limit {limit}")
+    idx = np.arange(space, dtype=np.int64)
+    vals = np.zeros((n, space), dtype=np.int64)
+    rem = idx.copy()
+    for pos in range(n - 1, -1, -1):
+        vals[order[pos]] = rem % dims[pos]
+        rem //= dims[pos]
+    total = np.zeros(space, dtype=np.float64 if inst.is_f64 else np.int64)
+    for f in range(inst.nf):
+        sc = [int(v) for v in inst.scope(f)]
+        k = np.zeros(space, dtype=np.int64)
+        for v in sc:
+            k = k * int(inst.dom[v]) + vals[v]
+        t = inst.table(f)[k]
+        if inst.is_f64:
+            total = total + t
+        else:
+            total = np.minimum(total + t.astype(np.int64), INF_I32)
+    best = int(np.argmin(total))  # first occurrence = lexicographically smallest
+    return (float(total[best]) if inst.is_f64 else int(total[best])), [int(vals[v][best]) for v in range(n)]

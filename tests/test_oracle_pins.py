@@ -1,0 +1,399 @@
+"""Pins of the CPU oracle to things other than itself (-m "not gpu").
+
+Each test names the PAPER.md passage (P:n) or mathematical fact it checks.
+A plausible mistake in the oracle (dropped term, wrong sign / index,
+transposed operand, wrong bucket rule, wrong tie-break) fails at least one.
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from gen import configs
+from oracle.brute import brute_force, brute_force_np, mpe_linear
+
+INF = oracle.INF_I32
+
+
+def example1(costs=None):
+    """Example 1: 4 binary variables x1..x4 (ids 0..3), functions
+    f(x1,x2), f(x1,x4), f(x2,x3), f(x2,x4), f(x3,x4)."""
+    scopes = [(0, 1), (0, 3), (1, 2), (1, 3), (2, 3)]
+    rng = np.random.default_rng(7)
+    if costs is None:
+        costs = [rng.integers(0, 10, 4) for _ in scopes]
+    return gen.Instance.from_functions([2, 2, 2, 2], list(zip(scopes, costs)))
+
+
+# ---------------------------------------------------------------- structure
+
+def test_example1_induced_width_is_3():
+    """along <x1,x2,x3,x4> the induced width is 3."""
+    assert oracle.induced_width(example1(), [0, 1, 2, 3]) == 3
+
+
+def test_example1_primal_graph_has_5_edges():
+    """P:162-163 / S:141: 5 binary constraints -> 5 edges."""
+    assert int(oracle.primal_graph(example1()).sum()) == 2 * 5
+
+
+def test_degree_ordering_example():
+    """S:163 applying P:610 to Example 1 (degrees 2,3,2,3): <x1,x3,x2,x4>."""
+    assert list(oracle.degree_order(example1())) == [0, 2, 1, 3]
+
+
+def test_induced_width_closed_forms():
+    """Path graph -> 1, complete graph K4 -> 3, cycle -> 2 (any ordering)."""
+    path = gen.Instance.from_functions([2] * 3, [((0, 1), [0] * 4), ((1, 2), [0] * 4)])
+    assert oracle.induced_width(path, [0, 1, 2]) == 1
+    k4 = gen.Instance.from_functions([2] * 4, [((a, b), [0] * 4) for a in range(4) for b in range(a + 1, 4)])
+    for order in itertools.permutations(range(4)):
+        assert oracle.induced_width(k4, order) == 3
+    cyc = gen.Instance.from_functions([2] * 6, [((i, (i + 1) % 6), [0] * 4) for i in range(6)])
+    for order in [range(6), [3, 1, 5, 0, 2, 4]]:
+        assert oracle.induced_width(cyc, list(order)) == 2
+
+
+def test_minfill_on_trees_gives_width_1():
+    """A tree has treewidth 1 and min-fill never adds fill on a tree."""
+    for seed in range(5):
+        t = gen.random_graph(30, 2, 29, 1, 0.0, seed)
+        assert oracle.induced_width(t, oracle.minfill_order(t)) == 1
+
+
+def test_example2_pseudotree():
+    """Example 2: tree edges {12,23,34}; x4's pseudo-parents are x1
+    and x2 (backedges (1,4), (2,4))."""
+    par = oracle.elim_tree(example1(), [0, 1, 2, 3])
+    assert list(par) == [-1, 0, 1, 2]
+    tree = {(min(v, p), max(v, p)) for v, p in enumerate(par) if p >= 0}
+    assert tree == {(0, 1), (1, 2), (2, 3)}
+    back = set(example1().edges()) - tree
+    assert back == {(0, 3), (1, 3)}
+
+
+def test_example3_buckets():
+    """Example 3: B4 = {f14, f24, f34}, B3 = {f23, f^4},
+    B2 = {f12, f^3}, B1 = {f^2} (reading A1: latest-ordered variable)."""
+    r = oracle.solve_be(example1(), [0, 1, 2, 3])
+    by_var = {t.var: (i, t) for i, t in enumerate(r.tables)}
+    assert [t.var for t in r.tables] == [3, 2, 1, 0]
+    assert by_var[3][1].members == [(0, 1), (0, 3), (0, 4)]
+    assert by_var[2][1].members == [(0, 2), (1, by_var[3][0])]
+    assert by_var[1][1].members == [(0, 0), (1, by_var[2][0])]
+    assert by_var[0][1].members == [(1, by_var[1][0])]
+    assert list(by_var[3][1].sep) == [0, 1, 2]
+
+
+def test_example4_minibucket_partition():
+    """Example 4 with z=1 (reading A5: i bounds the generated
+    arity): B4 splits into the singletons {f14}, {f24}, {f34}; then
+    B3 = {f23, f^4_3}, B2 = {f12, f^4_2, f^3_1}, B1 = {f^4_1, f^2_1}."""
+    r = oracle.solve_mbe(example1(), [0, 1, 2, 3], 1)
+    assert r.status == 0
+    tabs = r.tables
+    b4 = [(i, t) for i, t in enumerate(tabs) if t.var == 3]
+    assert [t.members for _, t in b4] == [[(0, 1)], [(0, 3)], [(0, 4)]]
+    assert [list(t.sep) for _, t in b4] == [[0], [1], [2]]
+    f41, f42, f43 = (i for i, _ in b4)
+    t3 = [t for t in tabs if t.var == 2]
+    assert len(t3) == 1 and t3[0].members == [(0, 2), (1, f43)]
+    i31 = [i for i, t in enumerate(tabs) if t.var == 2][0]
+    t2 = [t for t in tabs if t.var == 1]
+    assert len(t2) == 1 and t2[0].members == [(0, 0), (1, f42), (1, i31)]
+    i21 = [i for i, t in enumerate(tabs) if t.var == 1][0]
+    t1 = [t for t in tabs if t.var == 0]
+    assert len(t1) == 1 and t1[0].members == [(1, f41), (1, i21)]
+
+
+def test_minibucket_ibound_below_arity_is_invalid():
+    """a member that cannot fit the bound is an error."""
+    assert oracle.solve_mbe(example1(), [0, 1, 2, 3], 0).status == 1
+
+
+# ---------------------------------------------------------------- index map
+
+def test_section63_index_map_example():
+    """§6.3 example: aggregating T_j = f23 (scope x2,x3) into the
+    output table over (x1,x2,x3) maps T_id 0..7 to r_j 0,1,2,3,0,1,2,3.  We
+    read it through the oracle's bucket function: a selector member g(x3)
+    forces the eliminated value v, so out(x1,x2) = f23[map(x1,x2,v)]."""
+    dom = [2, 2, 2]
+    f23 = ((1, 2), [0, 1, 2, 3])  # value = its own row index r_j
+    got = []
+    for v in range(2):
+        sel = ((2,), [0, INF] if v == 0 else [INF, 0])
+        out, arg = oracle.bucket_eval(dom, False, 2, [f23, sel], [0, 1])
+        assert list(arg) == [v] * 4
+        got.append(list(out))
+    tid_to_rj = [got[tid % 2][tid // 2] for tid in range(8)]  # T_id = x1 x2 x3
+    assert tid_to_rj == [0, 1, 2, 3, 0, 1, 2, 3]
+
+
+def test_eliminate_closed_form():
+    """S:279 (Proc. 5): scope (x1,x2), chi = [5,2,7,1], min over
+    the last variable -> [2,1] with argmins [1,1]."""
+    out, arg = oracle.bucket_eval([2, 2], False, 1, [((0, 1), [5, 2, 7, 1])], [0])
+    assert list(out) == [2, 1] and list(arg) == [1, 1]
+
+
+def test_transposed_scope_is_reranked():
+    """A member declared as (x2, x1) must be read transposed."""
+    out, _ = oracle.bucket_eval([2, 2], False, 1, [((1, 0), [5, 2, 7, 1])], [0])
+    # f(x2,x1): f(x1=0,x2=0)=5, f(x1=0,x2=1)=7, f(x1=1,x2=0)=2, f(x1=1,x2=1)=1
+    assert list(out) == [5, 1]
+
+
+def test_one_hot_pins_each_row_mapping():
+    """One-hot inputs: a single 1 in a zero table of a member over a random
+    sub-scope lights exactly the output rows whose tuple projects onto that
+    cell (naive tuple matching)."""
+    rng = np.random.default_rng(3)
+    for trial in range(40):
+        m = int(rng.integers(1, 5))
+        dom = [int(x) for x in rng.integers(1, 4, m + 1)]
+        x = m
+        sep = list(range(m))
+        sub = sorted(rng.choice(m, size=int(rng.integers(0, m + 1)), replace=False).tolist())
+        scope = [int(v) for v in rng.permutation(sub + [x])]
+        cells = int(np.prod([dom[v] for v in scope]))
+        hot = int(rng.integers(cells))
+        t = np.zeros(cells, np.int64)
+        t[hot] = 1
+        # second member pins v: cost 0 only at v = 0
+        selv = [0] + [INF] * (dom[x] - 1)
+        out, _ = oracle.bucket_eval(dom, False, x, [(scope, t), ((x,), selv)], sep)
+        hot_tuple = np.unravel_index(hot, [dom[v] for v in scope])
+        hv = dict(zip(scope, hot_tuple))
+        for r, tup in enumerate(itertools.product(*[range(dom[v]) for v in sep])):
+            a = dict(zip(sep, tup))
+            a[x] = 0
+            expect = 1 if all(a[v] == hv[v] for v in scope) else 0
+            assert out[r] == expect
+
+
+# ---------------------------------------------------------------- exactness
+
+@pytest.mark.parametrize("seed", range(200))
+def test_be_equals_brute_force_small(seed):
+    """Cor. 3 / S:586: BE optimum = brute-force optimum, and the
+    BE assignment (smallest-index forward pass) is the lexicographically
+    smallest optimum under the ordering."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(6, 10))
+    d = int(rng.integers(2, 5))
+    while d ** n > 70000:
+        n -= 1
+    p1 = float(rng.uniform(0.2, 0.9))
+    p2 = [0.0, 0.3, 0.5][seed % 3]
+    ne = max(n - 1, int(p1 * n * (n - 1) / 2))
+    inst = gen.random_graph(n, d, ne, 0, p2, seed)
+    order = oracle.minfill_order(inst) if seed % 2 else oracle.degree_order(inst)
+    r = oracle.solve_be(inst, order)
+    opt, a = brute_force_np(inst, order)
+    assert r.value == opt
+    assert oracle.evaluate(inst, r.assignment) == opt
+    if opt < INF:  # an infeasible optimum (INF) has no unique assignment
+        assert list(r.assignment) == a
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_c1_config_against_brute_force(seed):
+    """C1 (n=12, d=3, 19 or 39 edges, p2 in {0, 0.5}): exact BE vs 3^12
+    brute force."""
+    inst = configs.c1(seed, literal=bool(seed % 2), p2=0.5 if seed >= 3 else 0.0)
+    order = oracle.minfill_order(inst)
+    r = oracle.solve_be(inst, order)
+    opt, a = brute_force_np(inst, order)
+    assert r.value == opt and oracle.evaluate(inst, r.assignment) == opt
+    if opt < INF:
+        assert list(r.assignment) == a
+
+
+def test_pure_python_brute_force_agrees_with_vectorised():
+    inst = gen.random_graph(7, 3, 10, 0, 0.3, 11)
+    assert brute_force(inst, range(7)) == brute_force_np(inst, range(7))
+
+
+def _tree_dp(inst, root=0):
+    """Independent min-sum dynamic programme on a tree (w* = 1)."""
+    n = inst.n
+    nbr = {v: [] for v in range(n)}
+    fn = {}
+    for f in range(inst.nf):
+        u, v = (int(x) for x in inst.scope(f))
+        nbr[u].append(v)
+        nbr[v].append(u)
+        t = inst.table(f).reshape(int(inst.dom[u]), int(inst.dom[v]))
+        fn[(u, v)] = t
+        fn[(v, u)] = t.T
+
+    def msg(c, p):  # min over c of f(p, c) + sum of c's children messages
+        below = np.zeros(int(inst.dom[c]), np.int64)
+        for g in nbr[c]:
+            if g != p:
+                below = np.minimum(below + msg(g, c), INF)
+        tab = fn[(p, c)].astype(np.int64)
+        return np.minimum(tab + below[None, :], INF).min(axis=1)
+
+    tot = np.zeros(int(inst.dom[root]), np.int64)
+    for c in nbr[root]:
+        tot = np.minimum(tot + msg(c, root), INF)
+    return int(tot.min())
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_tree_instances_match_tree_dp(seed):
+    inst = gen.random_graph(40, 4, 39, 1, 0.2 if seed % 2 else 0.0, seed)
+    order = oracle.minfill_order(inst)
+    assert oracle.induced_width(inst, order) == 1
+    assert oracle.solve_be(inst, order).value == _tree_dp(inst)
+
+
+def test_special_cases():
+    """S:514-style closed forms: all-zero -> 0 and all-zero assignment;
+    unary-only -> sum of minima and argmins; all-INF -> INF; d = 1 copy."""
+    z = gen.Instance.from_functions([3, 3, 3], [((0, 1), [0] * 9), ((1, 2), [0] * 9)])
+    r = oracle.solve_be(z, [0, 1, 2])
+    assert r.value == 0 and list(r.assignment) == [0, 0, 0]
+    un = gen.Instance.from_functions([3, 2], [((0,), [4, 1, 9]), ((1,), [7, 3])])
+    r = oracle.solve_be(un, [0, 1])
+    assert r.value == 1 + 3 and list(r.assignment) == [1, 1]
+    inf = gen.Instance.from_functions([2, 2], [((0, 1), [INF] * 4)])
+    r = oracle.solve_be(inf, [0, 1])
+    assert r.value == INF and list(r.assignment) == [0, 0]
+    out, arg = oracle.bucket_eval([3, 1], False, 1, [((0, 1), [5, 6, 7])], [0])
+    assert list(out) == [5, 6, 7] and list(arg) == [0, 0, 0]
+
+
+def test_disconnected_components_sum():
+    """disconnected graphs are solved per component and the root
+    costs are summed."""
+    a = gen.random_graph(6, 3, 8, 0, 0.0, 1)
+    b = gen.random_graph(5, 3, 6, 0, 0.0, 2)
+    fns = [(list(a.scope(f)), a.table(f)) for f in range(a.nf)]
+    fns += [([int(v) + 6 for v in b.scope(f)], b.table(f)) for f in range(b.nf)]
+    ab = gen.Instance.from_functions([3] * 11, fns)
+    va = oracle.solve_be(a, oracle.minfill_order(a)).value
+    vb = oracle.solve_be(b, oracle.minfill_order(b)).value
+    assert oracle.solve_be(ab, oracle.minfill_order(ab)).value == va + vb
+
+
+# ---------------------------------------------------------------- MBE
+
+@pytest.mark.parametrize("seed", range(30))
+def test_mbe_bound_sandwich_and_exactness(seed):
+    """MBE lower <= BE <= evaluate(MBE assignment); with i >= w*
+    there is no partition and every table equals BE's (Thm 1)."""
+    inst = gen.random_graph(14, 3, 30, 0, 0.0 if seed % 2 else 0.3, seed)
+    order = oracle.minfill_order(inst)
+    w = oracle.induced_width(inst, order)
+    be = oracle.solve_be(inst, order)
+    for i in range(1, w + 1):
+        r = oracle.solve_mbe(inst, order, i)
+        assert r.status == 0
+        assert r.value <= be.value <= r.upper
+        assert r.upper == oracle.evaluate(inst, r.assignment)
+        assert max(len(t.sep) for t in r.tables) <= i  # Cor. 1: arity <= i
+    r = oracle.solve_mbe(inst, order, w)
+    assert r.value == be.value == r.upper
+    assert len(r.tables) == len(be.tables)
+    for t, u in zip(r.tables, be.tables):
+        assert np.array_equal(t.out, u.out) and np.array_equal(t.arg, u.arg)
+
+
+# ---------------------------------------------------------------- DPOP
+
+@pytest.mark.parametrize("seed", range(10))
+def test_elimination_tree_is_a_pseudotree(seed):
+    """every primal edge joins an ancestor and a descendant; Cor. 2
+    (P:876-883): n - #components UTIL messages."""
+    inst = gen.scalefree(25, 2, 0.0, seed)
+    order = oracle.minfill_order(inst)
+    par = oracle.elim_tree(inst, order)
+
+    def anc(v):
+        out = set()
+        while par[v] >= 0:
+            v = int(par[v])
+            out.add(v)
+        return out
+
+    for u, v in inst.edges():
+        assert u in anc(v) or v in anc(u)
+    assert sum(1 for p in par if p >= 0) == inst.n - 1
+    r = oracle.solve_be(inst, order)
+    # UTIL message of v goes to parent(v): the table's destination
+    for t in r.tables:
+        assert t.dest == par[t.var]
+
+
+# ---------------------------------------------------------------- MPE
+
+@pytest.mark.parametrize("seed", range(12))
+def test_mpe_matches_linear_domain_brute_force(seed):
+    """MPE Eq. (2): exp(-BE value) = max_sigma prod Pr within
+    1e-9 relative; the BE assignment attains it."""
+    inst = gen.belief_net(9, 2, 3, 2, 4, seed)
+    order = oracle.minfill_order(inst)
+    r = oracle.solve_be(inst, order)
+    best = mpe_linear(inst)
+    assert math.isclose(math.exp(-r.value), best, rel_tol=1e-9)
+    assert math.isclose(oracle.evaluate(inst, r.assignment), r.value, rel_tol=1e-12)
+
+
+def test_mpe_chain_viterbi():
+    """A chain BN (one parent each) has the closed-form Viterbi recursion."""
+    inst = gen.belief_net(30, 2, 4, 1, 1, 5)
+    # Viterbi in the linear domain with rescaling
+    dom = [int(d) for d in inst.dom]
+    p0 = np.exp(-inst.table(0))
+    best = p0.copy()
+    logscale = 0.0
+    for v in range(1, inst.n):
+        cpt = np.exp(-inst.table(v)).reshape(dom[v - 1], dom[v])
+        best = (best[:, None] * cpt).max(axis=0)
+        s = best.max()
+        best /= s
+        logscale += math.log(s)
+    viterbi_log = logscale + math.log(best.max())
+    r = oracle.solve_be(inst, oracle.minfill_order(inst))
+    assert math.isclose(-r.value, viterbi_log, rel_tol=1e-9)
+
+
+# ---------------------------------------------------------------- generators
+
+def test_generator_laws():
+    """2(n-2)+1 scale-free edges; grid degree profile 2/3/4;
+    P:922 (reading A4): exact edge count, connected."""
+    for n in (10, 57, 200):
+        assert len(gen.scalefree(n, 2, 0.0, 1).edges()) == 2 * (n - 2) + 1
+    g = gen.grid(4, 5, 2)
+    adj = oracle.primal_graph(g)
+    deg = adj.sum(1).reshape(4, 5)
+    assert deg[0, 0] == deg[0, 4] == deg[3, 0] == deg[3, 4] == 2
+    assert (deg[1:3, 1:4] == 4).all() and deg[0, 2] == 3 and deg[2, 0] == 3
+    r = gen.random_graph(12, 3, 19, 0, 0.0, 4)
+    assert len(r.edges()) == 19
+    assert oracle.induced_width(r, oracle.minfill_order(r)) >= 1
+
+
+def test_generator_tightness_exact_count():
+    """P:928 / S:564: exactly floor(p2 * cells) infinite cells per function."""
+    inst = gen.random_graph(10, 5, 20, 0, 0.5, 3)
+    for f in range(inst.nf):
+        assert int((inst.table(f) == INF).sum()) == 12
+
+
+def test_pinned_config_widths():
+    """BASELINE.md re-parameterisations: C2 w*=10, C4 w*=20, C5 w*=18 under
+    min-fill; C3 row-major w*=20."""
+    assert oracle.induced_width(configs.c2(), oracle.minfill_order(configs.c2())) == 10
+    c4 = configs.c4()
+    assert oracle.induced_width(c4, oracle.minfill_order(c4)) == 20
+    c5 = configs.c5()
+    assert oracle.induced_width(c5, oracle.minfill_order(c5)) == 18
+    assert oracle.induced_width(configs.c3(), configs.c3_order()) == 20
