@@ -1,0 +1,278 @@
+"""Benchmark: UTIL/bucket cells/s of an exact DPOP solve (UTIL + VALUE) on the
+BASELINE C4 workload (scale-free DCOP, n=200, d=3, w*=20; largest UTIL table
+3^20 = 3.49e9 rows) -- see DESIGN.md §7 for why C4 is the N=1 workload.
+
+  python bench.py --gpus N --steps K --warmup W [--impl reference]
+
+One step = one pass of the whole hot path: batched upload + relayout of the
+original tables, one fused aggregate+project kernel per bucket (device-
+resident messages), constants, value phase, optimum + assignment back to the
+host.  Prints ONE JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "UTIL/bucket table cells/sec (exact DPOP solve, UTIL+VALUE)"
+UNIT = "cells/s"
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+def workload(name):
+    from gen import configs
+    if name == "c4":
+        return configs.c4(), None, "C4 scale-free DCOP n=200 d=3 seed=5 (min-fill w*=20), DPOP"
+    if name == "c4alt":
+        return configs.c4(seed=configs.C4_ALT_SEED), None, "C4-alt scale-free DCOP n=200 d=3 seed=9 (w*=16), DPOP"
+    if name == "c2":
+        return configs.c2(), None, "C2 random DCOP n=100 d=5 (w*=10), DPOP"
+    raise SystemExit(f"unknown workload {name}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def cpu_sample(inst, order, seconds_target=12.0, steps=None):
+    """The oracle (as it stands) on a bounded sample: rows of the largest
+    bucket of this workload, with synthetic member tables of the same shapes."""
+    import numpy as np
+
+    import oracle
+    import paper_1608_05288_b200 as G
+    P = G.Problem.from_instance(inst)
+    info = G.Plan(P, order).info()
+    t = max(info["tables"], key=lambda t: t["rows"] * t["d"])
+    dom = [int(x) for x in inst.dom]
+    rng = np.random.default_rng(0)
+    pos = {int(v): i for i, v in enumerate(order)}
+    members = []
+    for kind, idx in t["members"]:
+        if kind == 0:
+            sc = sorted([int(v) for v in inst.scope(idx)], key=lambda v: pos[v])
+        else:
+            sc = info["tables"][idx]["sep"]
+        cells = int(np.prod([dom[v] for v in sc]))
+        members.append((sc, rng.integers(0, 100, cells).astype(np.int32)))
+    cores = os.cpu_count() or 1
+
+    def run(nrows):
+        t0 = time.perf_counter()
+        oracle.bucket_eval(dom, False, t["var"], members, t["sep"], 0, nrows, nthreads=cores)
+        return time.perf_counter() - t0
+
+    n0 = 20000
+    dt = run(n0)
+    nrows = int(min(t["rows"], max(n0, n0 * seconds_target / max(dt, 1e-6))))
+    dt = run(nrows)
+    return {"cells": nrows * t["d"], "seconds": dt, "cores": cores,
+            "sample": f"rows [0,{nrows}) of the largest bucket (x{t['var']}, {t['rows']} rows, "
+                      f"d={t['d']}, k={len(t['members'])}) with synthetic member tables"}, run, nrows, t["d"]
+
+
+def reference_arm(args, world, rank):
+    """--impl reference: the CPU oracle on the box's host cores."""
+    if rank != 0:
+        return
+    inst, order_none, desc = workload(args.workload)
+    import paper_1608_05288_b200 as G
+    order, w = G.Problem.from_instance(inst).order()
+    base, run, nrows, d = cpu_sample(inst, order, seconds_target=max(2.0, 60.0 / max(args.steps + args.warmup, 1)))
+    for _ in range(args.warmup):
+        run(nrows)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run(nrows)
+    dt = (time.perf_counter() - t0) / max(args.steps, 1)
+    val = nrows * d / dt
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic", "config": {"workload": desc, "sample": base["sample"]},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": base["cores"], "kind": "oracle",
+                         "sample": base["sample"]},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--workload", default="c4")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return reference_arm(args, world, rank)
+
+    import numpy as np
+    import torch
+
+    import paper_1608_05288_b200 as G
+    from paper_1608_05288_b200 import dist as gdist
+
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        pg = gdist.init(local)
+    inst, _, desc = workload(args.workload)
+    P = G.Problem.from_instance(inst)
+    order, w = P.order()
+    exe = dict(device=local, world_size=world, rank=rank)
+    plan = G.Plan(P, order, resident_inputs=True, timing=True, **exe)
+    plan_e2e = G.Plan(P, order, **exe)
+    info = plan.info()
+    ntasks = len(info["tables"])
+    total_cells = info["total_cells"]
+    stream = torch.cuda.current_stream()
+
+    def step(pl):
+        run, root = pl.dpop_util(stream)
+        a = run.value()
+        st = run.stats()
+        run.close()
+        return root, a, st
+
+    for _ in range(max(args.warmup, 3)):
+        root, assign, _ = step(plan)
+        step(plan_e2e)
+
+    def timed(pl, k):
+        gdist.barrier(pg)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        stats = []
+        e0.record(stream)
+        for _ in range(k):
+            r = step(pl)
+            stats.append(r[2])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / k
+        ms = gdist.max_over_ranks(ms, pg)
+        return ms, stats, r
+
+    with ClockSampler(local) as clk:
+        ms, stats, (root, assign, _) = timed(plan, args.steps)
+    ms_e2e, _, _ = timed(plan_e2e, args.steps)
+    clocks = clk.summary()
+
+    # roofline of the dominant kernel (BK), from the live per-launch events
+    bk_ms = sum(t["ms"] for s in stats for t in s["tasks"]) / len(stats)
+    bk_bytes = sum(t["bytes"] for t in stats[0]["tasks"])
+    big = max(stats[0]["tasks"], key=lambda t: t["cells"])
+    big_ms = sum(t["ms"] for s in stats for t in s["tasks"] if t["var"] == big["var"] and t["mb"] == big["mb"]) / len(stats)
+    peaks, peak_src = measured_peaks()
+    achieved = bk_bytes / (bk_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.workload)
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        base, _, _, _ = cpu_sample(inst, order)
+        cpu = {"value": base["cells"] / base["seconds"], "unit": UNIT, "cores": base["cores"],
+               "kind": "oracle", "sample": base["sample"]}
+
+    value = total_cells * world / (ms * 1e-3) if False else total_cells / (ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic",
+        "config": {"workload": desc, "n": inst.n, "induced_width": w, "buckets": ntasks,
+                   "total_cells": total_cells, "largest_table_rows": max(t["rows"] for t in info["tables"]),
+                   "parallelism": f"row-shard x{world}" if world > 1 else "1 GPU",
+                   "l2": "no flush: every step writes >= 14 GB of UTIL tables (> 126 MB L2)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                     "kernel": "bk (all bucket launches of one step)", "peak_source": peak_src,
+                     "largest_bucket": {"var": big["var"], "cells": big["cells"], "bytes": big["bytes"],
+                                        "ms": big_ms, "gbs": big["bytes"] / (big_ms * 1e-3) / 1e9,
+                                        "cells_per_s": big["cells"] / (big_ms * 1e-3)}},
+        "clocks": clocks,
+        "e2e": {"value": total_cells / (ms_e2e * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": int(inst.costs.nbytes),
+                "d2h_bytes_per_step": int(4 * inst.n + 8), "ms_per_step": ms_e2e},
+        "gpu_launches": args.steps * (ntasks + 3),
+        "optimum": root,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    gdist.finish(pg)
+
+
+if __name__ == "__main__":
+    main()

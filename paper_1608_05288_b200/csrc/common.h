@@ -1,0 +1,159 @@
+// common.h — internal types of libgbe (not part of the C ABI).
+//
+// Citations: P:n = PAPER.md line n (arXiv 1608.05288).  Readings A1..A17:
+// DESIGN.md §3.  This file and everything under csrc/ is product code: it
+// never includes or links anything from oracle/.
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "gbe.h"
+
+namespace gbe {
+
+constexpr int32_t kInfI32 = GBE_INF_I32;
+
+// ---------------------------------------------------------------------------
+// errors: thread-local last error + status propagation
+
+void set_error(const std::string &msg);
+const char *last_error();
+
+struct Error {
+  gbe_status status;
+  std::string msg;
+};
+
+#define GBE_FAIL(st, ...)                                   \
+  do {                                                      \
+    char _gbe_buf[512];                                     \
+    std::snprintf(_gbe_buf, sizeof(_gbe_buf), __VA_ARGS__); \
+    throw ::gbe::Error{st, _gbe_buf};                       \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// problem: <X, D, C>, functions in declared scope order
+
+struct Problem {
+  int32_t n = 0, nf = 0;
+  gbe_semiring sr = GBE_MINSUM_I32;
+  std::vector<int32_t> dom;       // [n]
+  std::vector<int32_t> arity;     // [nf]
+  std::vector<int64_t> scope_off; // [nf+1]
+  std::vector<int32_t> scopes;
+  std::vector<int64_t> table_off; // [nf+1]
+  std::vector<int32_t> icost;     // int32 semiring
+  std::vector<double> fcost;      // f64 semiring
+  bool is_f64() const { return sr == GBE_MINSUM_F64; }
+  size_t elem() const { return is_f64() ? 8 : 4; }
+  const int32_t *scope(int f) const { return scopes.data() + scope_off[f]; }
+};
+
+// ---------------------------------------------------------------------------
+// minimal JSON (flat objects of numbers / strings / bools)
+
+struct Json {
+  std::map<std::string, std::string> kv; // raw scalar text (strings unquoted)
+  static Json parse(const char *text);   // throws Error{GBE_E_INVALID}
+  bool has(const std::string &k) const { return kv.count(k) != 0; }
+  int64_t i(const std::string &k, int64_t def) const;
+  double f(const std::string &k, double def) const;
+  std::string s(const std::string &k, const std::string &def) const;
+  bool b(const std::string &k, bool def) const;
+};
+
+// ---------------------------------------------------------------------------
+// plan: ordering, (mini-)bucket tasks, layouts, stride maps, shard plan
+
+struct Member {
+  int32_t kind;  // 0 original function, 1 message (task index)
+  int32_t index;
+};
+
+// Row sharding of one task's output over the ranks: the rows
+// split into `blocks` blocks of `block_rows` rows (a block = one value of the
+// `key_digits` most significant output digits); rank r owns blocks
+// [r*per, min((r+1)*per, blocks)).
+struct Shard {
+  bool on = false;
+  int32_t key_digits = 0;
+  int64_t blocks = 1, block_rows = 0, per = 0;
+  int64_t lo = 0, hi = 0;   // this rank's row range
+  bool gather = false;      // the consumer needs the whole message
+};
+
+struct Task {                  // one (mini-)bucket: Alg. 1 line 3 / Alg. 2 line 5
+  int32_t var = -1, mb = 0;    // eliminated variable, mini-bucket index
+  int32_t dest = -1;           // bucket variable receiving the message (-1 const)
+  int32_t consumer = -1;       // task consuming the message (-1 = constant)
+  std::vector<Member> members; // canonical order (originals, then messages)
+  std::vector<int32_t> sep;    // output scope, ascending order position
+  int64_t rows = 1;
+  int32_t d = 1;
+  int32_t height = 0;          // longest chain of producers below (DPOP levels)
+  gbe_bucket_desc desc{};      // radices + per-input stride maps (shift = 0)
+  int64_t in_cells = 0;        // sum of input table sizes
+  Shard shard;
+};
+
+struct ExecOptions {
+  int device = 0;
+  int64_t budget_bytes = -1;   // <0: device memory at plan time
+  int world_size = 1, rank = 0;
+  int64_t shard_min_rows = 1ll << 24;
+  int retain = 1;              // 0 none, 1 args, 2 all
+  bool timing = false;
+  int kernel = -1;             // -1 auto, else force a kernel variant
+  bool resident_inputs = false; // keep the uploaded originals on the device between solves
+};
+
+struct Plan {
+  std::shared_ptr<const Problem> prob;
+  std::vector<int32_t> order, pos;
+  int32_t ibound = -1;
+  int32_t width = 0;
+  std::vector<Task> tasks;                     // creation order
+  std::vector<std::vector<Member>> bucket;     // canonical B_x per variable
+  std::vector<int32_t> var_task;               // BE: the task of each variable
+  std::vector<Member> constants;               // originals of arity 0, then root messages
+  std::vector<int32_t> perm_strides;           // relayout: per original, per sorted pos
+  std::vector<int64_t> sorted_off;             // relayout
+  int64_t total_cells = 0;                     // sum over tasks of rows*d
+  int64_t total_bytes = 0;                     // algorithmic bytes
+  int64_t peak_bytes = 0;                      // estimated device peak
+  ExecOptions ex;
+};
+
+// planner.cpp
+std::vector<std::vector<char>> primal_adjacency(const Problem &p);
+void order_minfill(const Problem &p, std::vector<int32_t> &order);
+void order_degree(const Problem &p, std::vector<int32_t> &order);
+int32_t induced_width(const Problem &p, const std::vector<int32_t> &order);
+std::unique_ptr<Plan> make_plan(std::shared_ptr<const Problem> p, const int32_t *order,
+                                int32_t ibound, const ExecOptions &ex);
+std::string plan_json(const Plan &plan);
+
+// problem.cpp
+std::shared_ptr<Problem> problem_create(int32_t n, const int32_t *dom, int32_t nf,
+                                        const int32_t *arity, const int32_t *scopes,
+                                        gbe_semiring sr, const void *costs);
+std::shared_ptr<Problem> problem_load_wcsp(const char *path);
+std::shared_ptr<Problem> problem_load_uai(const char *model, const char *evid);
+std::shared_ptr<Problem> problem_generate(const char *json);
+gbe_value problem_evaluate(const Problem &p, const int32_t *assign);
+
+}  // namespace gbe
+
+// opaque handles of the C ABI
+struct gbe_problem {
+  std::shared_ptr<gbe::Problem> p;
+};
+struct gbe_plan {
+  std::unique_ptr<gbe::Plan> plan;
+  void *dev = nullptr;  // executor state (executor.cpp)
+};

@@ -1,0 +1,548 @@
+// executor.cpp — device executor for BE / MBE / DPOP plans.
+//
+// Alg. 3 re-designed for one B200: the original tables go to the
+// device in ONE batched copy and are re-laid-out there;
+// every (mini-)bucket is one fused aggregate+project kernel (BK) whose
+// messages stay device-resident and are freed once consumed; the
+// value phase is a single-warp kernel walking the forward
+// order over the argmin tables.  Row-sharded buckets call the
+// all-gather hook only when a consumer needs a whole message.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <sstream>
+
+#include "common.h"
+#include "executor.h"
+#include "kernels.h"
+
+namespace gbe {
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t _e = (call);                                                            \
+    if (_e != cudaSuccess) GBE_FAIL(GBE_E_CUDA, "%s: %s", #call, cudaGetErrorString(_e)); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// hooks
+
+static void *(*g_alloc)(size_t, void *, void *) = nullptr;
+static void (*g_free)(void *, void *) = nullptr;
+static void *g_alloc_u = nullptr;
+static int (*g_ag)(const void *, void *, size_t, void *, void *) = nullptr;
+static void *g_ag_u = nullptr;
+
+void set_allocator(void *(*a)(size_t, void *, void *), void (*f)(void *, void *), void *u) {
+  g_alloc = a;
+  g_free = f;
+  g_alloc_u = u;
+}
+void set_allgather(int (*ag)(const void *, void *, size_t, void *, void *), void *u) {
+  g_ag = ag;
+  g_ag_u = u;
+}
+
+static void *dalloc(size_t bytes, cudaStream_t s) {
+  if (bytes == 0) bytes = 16;
+  bytes = (bytes + 255) & ~size_t(255);  // slack for vector tails
+  void *p = nullptr;
+  if (g_alloc) {
+    p = g_alloc(bytes, (void *)s, g_alloc_u);
+    if (!p) GBE_FAIL(GBE_E_BUDGET, "allocator hook failed for %zu bytes", bytes);
+    return p;
+  }
+  cudaError_t e = cudaMallocAsync(&p, bytes, s);
+  if (e != cudaSuccess) GBE_FAIL(e == cudaErrorMemoryAllocation ? GBE_E_BUDGET : GBE_E_CUDA,
+                                 "device allocation of %zu bytes: %s", bytes, cudaGetErrorString(e));
+  return p;
+}
+static void dfree(void *p, cudaStream_t s) {
+  if (!p) return;
+  if (g_free) {
+    g_free(p, g_alloc_u);
+    return;
+  }
+  cudaFreeAsync(p, s);
+}
+
+// ---------------------------------------------------------------------------
+// per-plan device state
+
+struct DevPlan {
+  int device = 0, num_sms = 148;
+  std::vector<gbe_bucket_desc> h_desc;
+  std::vector<BkLaunchInfo> launch;
+  gbe_bucket_desc *d_desc = nullptr;
+  int64_t *d_off = nullptr;
+  int32_t *d_poff = nullptr, *d_prad = nullptr, *d_pstride = nullptr;
+  void *h_raw = nullptr;  // pinned copy of the declared-order tables
+  size_t raw_bytes = 0;
+  void *d_resident = nullptr;  // resident raw tables (resident_inputs)
+  bool resident = false;
+  ~DevPlan() {
+    cudaFree(d_desc);
+    cudaFree(d_off);
+    cudaFree(d_poff);
+    cudaFree(d_prad);
+    cudaFree(d_pstride);
+    cudaFree(d_resident);
+    if (h_raw) cudaFreeHost(h_raw);
+  }
+};
+
+static DevPlan *dev_plan(gbe_plan *gp) {
+  if (gp->dev) return (DevPlan *)gp->dev;
+  const Plan &P = *gp->plan;
+  const Problem &p = *P.prob;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    GBE_FAIL(GBE_E_CUDA, "no CUDA device: libgbe has no CPU fallback");
+  if (P.ex.device >= ndev) GBE_FAIL(GBE_E_INVALID, "device %d not present (%d devices)", P.ex.device, ndev);
+  CK(cudaSetDevice(P.ex.device));
+  auto *D = new DevPlan();
+  D->device = P.ex.device;
+  CK(cudaDeviceGetAttribute(&D->num_sms, cudaDevAttrMultiProcessorCount, D->device));
+  // descriptors with the per-rank input shifts (row-sharded messages kept local)
+  D->h_desc.resize(P.tasks.size());
+  D->launch.resize(P.tasks.size());
+  for (size_t ti = 0; ti < P.tasks.size(); ti++) {
+    const Task &t = P.tasks[ti];
+    gbe_bucket_desc h = t.desc;
+    for (int j = 0; j < h.ninputs; j++) {
+      h.shift[j] = 0;
+      const Member &m = t.members[j];
+      if (m.kind == 1) {
+        const Task &src = P.tasks[m.index];
+        if (src.shard.on && !src.shard.gather) h.shift[j] = src.shard.lo;
+      }
+    }
+    D->h_desc[ti] = h;
+    D->launch[ti] = bk_plan_launch(h, t.shard.lo, t.shard.hi, P.ex.kernel, D->num_sms);
+  }
+  size_t nt = std::max<size_t>(P.tasks.size(), 1);
+  CK(cudaMalloc(&D->d_desc, sizeof(gbe_bucket_desc) * nt));
+  if (!P.tasks.empty())
+    CK(cudaMemcpy(D->d_desc, D->h_desc.data(), sizeof(gbe_bucket_desc) * P.tasks.size(), cudaMemcpyHostToDevice));
+  // relayout metadata
+  std::vector<int32_t> poff(p.nf + 1, 0), prad;
+  for (int f = 0; f < p.nf; f++) poff[f + 1] = poff[f] + p.arity[f];
+  prad.resize(std::max<int32_t>(poff[p.nf], 1));
+  for (int f = 0; f < p.nf; f++) {
+    std::vector<int32_t> sc(p.scope(f), p.scope(f) + p.arity[f]);
+    std::sort(sc.begin(), sc.end(), [&](int a, int b) { return P.pos[a] < P.pos[b]; });
+    for (int q = 0; q < p.arity[f]; q++) prad[poff[f] + q] = p.dom[sc[q]];
+  }
+  std::vector<int32_t> pstr = P.perm_strides;
+  pstr.resize(std::max<size_t>(pstr.size(), 1));
+  CK(cudaMalloc(&D->d_off, sizeof(int64_t) * (p.nf + 1)));
+  CK(cudaMemcpy(D->d_off, p.table_off.data(), sizeof(int64_t) * (p.nf + 1), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&D->d_poff, sizeof(int32_t) * (p.nf + 1)));
+  CK(cudaMemcpy(D->d_poff, poff.data(), sizeof(int32_t) * (p.nf + 1), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&D->d_prad, sizeof(int32_t) * prad.size()));
+  CK(cudaMemcpy(D->d_prad, prad.data(), sizeof(int32_t) * prad.size(), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&D->d_pstride, sizeof(int32_t) * pstr.size()));
+  CK(cudaMemcpy(D->d_pstride, pstr.data(), sizeof(int32_t) * pstr.size(), cudaMemcpyHostToDevice));
+  // pinned host staging of the inputs (the H2D of every solve reads this)
+  D->raw_bytes = p.elem() * (size_t)p.table_off[p.nf];
+  CK(cudaMallocHost(&D->h_raw, std::max<size_t>(D->raw_bytes, 16)));
+  if (D->raw_bytes)
+    std::memcpy(D->h_raw, p.is_f64() ? (const void *)p.fcost.data() : (const void *)p.icost.data(), D->raw_bytes);
+  // stream-ordered pool: keep freed memory reserved between solves
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, D->device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  gp->dev = D;
+  return D;
+}
+
+void dev_plan_free(void *d) { delete (DevPlan *)d; }
+
+// ---------------------------------------------------------------------------
+// a run: device-resident messages / argmins of one UTIL phase
+
+struct RunImpl {
+  gbe_plan *gp = nullptr;
+  DevPlan *D = nullptr;
+  cudaStream_t stream = nullptr;
+  bool mbe = false;
+  void *d_raw = nullptr, *d_sorted = nullptr;
+  bool own_raw = true;
+  std::vector<void *> out, full;
+  std::vector<uint8_t *> arg;
+  std::vector<cudaEvent_t> ev;
+  std::vector<float> ms;
+  void *d_opt = nullptr;
+  int32_t *d_assign = nullptr, *d_gbuf = nullptr;
+  gbe_value optimum{};
+  bool util_done = false;
+  ~RunImpl() { release(); }
+  void release() {
+    if (!D) return;
+    cudaSetDevice(D->device);
+    for (auto p : out) dfree(p, stream);
+    for (auto p : full) dfree(p, stream);
+    for (auto p : arg) dfree(p, stream);
+    out.clear();
+    full.clear();
+    arg.clear();
+    if (own_raw) dfree(d_raw, stream);
+    dfree(d_sorted, stream);
+    dfree(d_opt, stream);
+    dfree(d_assign, stream);
+    dfree(d_gbuf, stream);
+    d_raw = d_sorted = d_opt = nullptr;
+    d_assign = d_gbuf = nullptr;
+    for (auto e : ev) cudaEventDestroy(e);
+    ev.clear();
+    cudaStreamSynchronize(stream);
+  }
+  const void *msg_ptr(int ti) const { return full[ti] ? full[ti] : out[ti]; }
+  const void *member_ptr(const Member &m) const {
+    const Problem &p = *gp->plan->prob;
+    if (m.kind == 0) return (const char *)d_sorted + p.elem() * p.table_off[m.index];
+    return msg_ptr(m.index);
+  }
+};
+
+static gbe_value read_value(const Problem &p, const void *host) {
+  gbe_value v{0, 0, 0.0};
+  if (p.is_f64()) {
+    v.f = *(const double *)host;
+    v.is_inf = std::isinf(v.f) ? 1 : 0;
+  } else {
+    v.i = *(const int32_t *)host;
+    v.is_inf = v.i >= kInfI32 ? 1 : 0;
+  }
+  return v;
+}
+
+// UTIL / elimination phase (Alg. 1 lines 1-5, Alg. 2 lines 1-7)
+static void run_util(RunImpl &R) {
+  gbe_plan *gp = R.gp;
+  const Plan &P = *gp->plan;
+  const Problem &p = *P.prob;
+  DevPlan *D = R.D;
+  cudaStream_t s = R.stream;
+  const size_t el = p.elem();
+  const int W = P.ex.world_size;
+  const size_t nt = P.tasks.size();
+
+  // pre-flight memory budget: plan estimate vs what the device has
+  {
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    uint64_t reserved = 0, used = 0;
+    cudaMemPool_t pool;
+    if (!g_alloc && cudaDeviceGetDefaultMemPool(&pool, D->device) == cudaSuccess) {
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    }
+    int64_t avail = (int64_t)fr + (int64_t)(reserved - used);
+    if (P.peak_bytes > avail) {
+      const Task *big = &P.tasks[0];
+      for (auto &t : P.tasks)
+        if (t.rows > big->rows) big = &t;
+      GBE_FAIL(GBE_E_BUDGET, "bucket x%d: %.3g rows; plan needs %.3g bytes > %.3g available on device %d",
+               big->var, (double)big->rows, (double)P.peak_bytes, (double)avail, D->device);
+    }
+  }
+
+  R.out.assign(nt, nullptr);
+  R.full.assign(nt, nullptr);
+  R.arg.assign(nt, nullptr);
+  if (P.ex.timing) {
+    R.ev.resize(2 * nt);
+    for (auto &e : R.ev) CK(cudaEventCreate(&e));
+    R.ms.assign(nt, 0.f);
+  }
+  // inputs: one batched H2D of the declared-order tables, then relayout
+  if (P.ex.resident_inputs) {
+    if (!D->resident) {
+      D->d_resident = nullptr;
+      CK(cudaMalloc(&D->d_resident, std::max<size_t>(D->raw_bytes, 16)));
+      CK(cudaMemcpy(D->d_resident, D->h_raw, D->raw_bytes, cudaMemcpyHostToDevice));
+      D->resident = true;
+    }
+    R.d_raw = D->d_resident;
+    R.own_raw = false;
+  } else {
+    R.d_raw = dalloc(D->raw_bytes, s);
+    CK(cudaMemcpyAsync(R.d_raw, D->h_raw, D->raw_bytes, cudaMemcpyHostToDevice, s));
+  }
+  R.d_sorted = dalloc(D->raw_bytes, s);
+  CK(relayout_launch(R.d_raw, R.d_sorted, (int)el, p.nf, D->d_off, D->d_poff, D->d_prad,
+                     D->d_pstride, s));
+  const bool want_arg = !R.mbe || P.ex.retain >= 2;
+  for (size_t ti = 0; ti < nt; ti++) {
+    const Task &t = P.tasks[ti];
+    const Shard &sh = t.shard;
+    int64_t local = sh.on ? sh.hi - sh.lo : t.rows;
+    int64_t cap = sh.on ? sh.per * sh.block_rows : t.rows;
+    R.out[ti] = dalloc(el * cap, s);
+    if (want_arg) R.arg[ti] = (uint8_t *)dalloc(std::max<int64_t>(local, 1), s);
+    InPtrs in{};
+    for (int j = 0; j < t.desc.ninputs; j++) in.p[j] = R.member_ptr(t.members[j]);
+    if (P.ex.timing) CK(cudaEventRecord(R.ev[2 * ti], s));
+    CK(bk_launch(D->h_desc[ti], D->d_desc + ti, in, R.out[ti], R.arg[ti], sh.lo, sh.hi,
+                 D->launch[ti], s));
+    if (P.ex.timing) CK(cudaEventRecord(R.ev[2 * ti + 1], s));
+    if (sh.on && sh.gather) {
+      if (!g_ag) GBE_FAIL(GBE_E_COMM, "bucket x%d is row-sharded but no all-gather hook is set", t.var);
+      size_t bytes = el * (size_t)cap;
+      R.full[ti] = dalloc(bytes * W, s);
+      if (g_ag(R.out[ti], R.full[ti], bytes, (void *)s, g_ag_u) != 0)
+        GBE_FAIL(GBE_E_COMM, "all-gather of the message of x%d failed", t.var);
+      dfree(R.out[ti], s);
+      R.out[ti] = nullptr;
+    }
+    // consumed messages are dead (BE/DPOP; MBE keeps them for its value phase, A7)
+    if (!R.mbe && P.ex.retain < 2)
+      for (auto &m : t.members)
+        if (m.kind == 1) {
+          dfree(R.out[m.index], s);
+          dfree(R.full[m.index], s);
+          R.out[m.index] = R.full[m.index] = nullptr;
+        }
+  }
+  // optimum / lower bound = sum of the constants
+  std::vector<const void *> cptrs;
+  for (auto &m : P.constants) cptrs.push_back(R.member_ptr(m));
+  R.d_opt = dalloc(8, s);
+  void *d_cp = dalloc(sizeof(void *) * std::max<size_t>(cptrs.size(), 1), s);
+  if (!cptrs.empty()) CK(cudaMemcpyAsync(d_cp, cptrs.data(), sizeof(void *) * cptrs.size(), cudaMemcpyHostToDevice, s));
+  R.d_assign = (int32_t *)dalloc(sizeof(int32_t) * std::max(p.n, 1), s);
+  CK(value_launch(p.is_f64(), nullptr, 0, 0, nullptr, nullptr, R.d_assign, nullptr, -1, W,
+                  (const void *const *)d_cp, (int)cptrs.size(), R.d_opt, s));
+  alignas(8) unsigned char hopt[8] = {0};
+  CK(cudaMemcpyAsync(hopt, R.d_opt, el, cudaMemcpyDeviceToHost, s));
+  dfree(d_cp, s);
+  CK(cudaStreamSynchronize(s));
+  R.optimum = read_value(p, hopt);
+  if (P.ex.timing)
+    for (size_t ti = 0; ti < nt; ti++) CK(cudaEventElapsedTime(&R.ms[ti], R.ev[2 * ti], R.ev[2 * ti + 1]));
+  R.util_done = true;
+}
+
+// VALUE / assignment phase (Alg. 1 lines 6-7)
+static void run_value(RunImpl &R, int32_t *assign_out) {
+  const Plan &P = *R.gp->plan;
+  const Problem &p = *P.prob;
+  cudaStream_t s = R.stream;
+  const int W = P.ex.world_size;
+  std::vector<VStep> steps;
+  std::vector<VMember> mems;
+  std::vector<VTerm> terms;
+  std::vector<char> sharded;
+  for (int i = 0; i < p.n; i++) {
+    int x = P.order[i];
+    VStep st{};
+    st.var = x;
+    st.d = p.dom[x];
+    if (!R.mbe) {
+      int ti = P.var_task[x];
+      const Task &t = P.tasks[ti];
+      if (!R.arg[ti]) GBE_FAIL(GBE_E_INTERNAL, "argmin table of x%d not retained", x);
+      st.kind = 0;
+      st.term_off = (int64_t)terms.size();
+      st.nterm = (int32_t)t.sep.size();
+      int64_t rs = 1;
+      std::vector<VTerm> tt(t.sep.size());
+      for (int q = (int)t.sep.size() - 1; q >= 0; q--) {
+        tt[q] = VTerm{t.sep[q], 0, rs};
+        rs *= p.dom[t.sep[q]];
+      }
+      terms.insert(terms.end(), tt.begin(), tt.end());
+      st.lo = t.shard.lo;
+      st.hi = t.shard.hi;
+      st.ptr = R.arg[ti];
+      sharded.push_back(t.shard.on ? 1 : 0);
+    } else {
+      st.kind = 1;
+      st.mem_off = (int64_t)mems.size();
+      st.nmem = (int32_t)P.bucket[x].size();
+      for (auto &m : P.bucket[x]) {
+        VMember vm{};
+        vm.ptr = R.member_ptr(m);
+        vm.term_off = (int64_t)terms.size();
+        // member scope ascending by position, x last: strides
+        std::vector<int32_t> sc;
+        if (m.kind == 0) {
+          sc.assign(p.scope(m.index), p.scope(m.index) + p.arity[m.index]);
+          std::sort(sc.begin(), sc.end(), [&](int a, int b) { return P.pos[a] < P.pos[b]; });
+        } else {
+          sc = P.tasks[m.index].sep;
+        }
+        int64_t st2 = 1;
+        std::vector<VTerm> tt;
+        for (int q = (int)sc.size() - 1; q >= 0; q--) {
+          if (sc[q] != x) tt.push_back(VTerm{sc[q], 0, st2});
+          st2 *= p.dom[sc[q]];
+        }
+        vm.nterm = (int32_t)tt.size();
+        terms.insert(terms.end(), tt.begin(), tt.end());
+        mems.push_back(vm);
+      }
+      sharded.push_back(0);
+    }
+    steps.push_back(st);
+  }
+  size_t b_steps = sizeof(VStep) * std::max<size_t>(steps.size(), 1);
+  size_t b_mems = sizeof(VMember) * std::max<size_t>(mems.size(), 1);
+  size_t b_terms = sizeof(VTerm) * std::max<size_t>(terms.size(), 1);
+  char *buf = (char *)dalloc(b_steps + b_mems + b_terms, s);
+  VStep *d_steps = (VStep *)buf;
+  VMember *d_mems = (VMember *)(buf + b_steps);
+  VTerm *d_terms = (VTerm *)(buf + b_steps + b_mems);
+  if (!steps.empty()) CK(cudaMemcpyAsync(d_steps, steps.data(), sizeof(VStep) * steps.size(), cudaMemcpyHostToDevice, s));
+  if (!mems.empty()) CK(cudaMemcpyAsync(d_mems, mems.data(), sizeof(VMember) * mems.size(), cudaMemcpyHostToDevice, s));
+  if (!terms.empty()) CK(cudaMemcpyAsync(d_terms, terms.data(), sizeof(VTerm) * terms.size(), cudaMemcpyHostToDevice, s));
+  if (W > 1 && !R.d_gbuf) R.d_gbuf = (int32_t *)dalloc(sizeof(int32_t) * W, s);
+  // segments end at row-sharded steps: the owner's lookup is exchanged
+  int s0 = 0, gvar = -1;
+  for (int i = 0; i < (int)steps.size(); i++) {
+    if (!(W > 1 && sharded[i])) continue;
+    CK(value_launch(p.is_f64(), d_steps, s0, i + 1, d_mems, d_terms, R.d_assign, R.d_gbuf, gvar,
+                    W, nullptr, -1, nullptr, s));
+    if (!g_ag) GBE_FAIL(GBE_E_COMM, "sharded value phase needs the all-gather hook");
+    if (g_ag(R.d_assign + steps[i].var, R.d_gbuf, sizeof(int32_t), (void *)s, g_ag_u) != 0)
+      GBE_FAIL(GBE_E_COMM, "all-gather of the value of x%d failed", steps[i].var);
+    gvar = steps[i].var;
+    s0 = i + 1;
+  }
+  CK(value_launch(p.is_f64(), d_steps, s0, (int)steps.size(), d_mems, d_terms, R.d_assign,
+                  R.d_gbuf, gvar, W, nullptr, -1, nullptr, s));
+  CK(cudaMemcpyAsync(assign_out, R.d_assign, sizeof(int32_t) * p.n, cudaMemcpyDeviceToHost, s));
+  dfree(buf, s);
+  CK(cudaStreamSynchronize(s));
+}
+
+static std::string stats_json(const RunImpl &R) {
+  const Plan &P = *R.gp->plan;
+  const Problem &p = *P.prob;
+  std::ostringstream o;
+  o << "{\"total_cells\":" << P.total_cells << ",\"total_bytes\":" << P.total_bytes << ",\"tasks\":[";
+  for (size_t ti = 0; ti < P.tasks.size(); ti++) {
+    const Task &t = P.tasks[ti];
+    int64_t local = t.shard.hi - t.shard.lo;
+    int64_t frac_in = t.rows ? (int64_t)((double)t.in_cells * local / t.rows) : 0;
+    int64_t bytes = (int64_t)p.elem() * (frac_in + local) + ((!R.mbe || P.ex.retain >= 2) ? local : 0);
+    o << (ti ? "," : "") << "{\"var\":" << t.var << ",\"mb\":" << t.mb << ",\"rows\":" << local
+      << ",\"d\":" << t.d << ",\"k\":" << t.desc.ninputs << ",\"cells\":" << local * t.d
+      << ",\"bytes\":" << bytes << ",\"variant\":" << R.D->launch[ti].variant
+      << ",\"ms\":" << (ti < R.ms.size() ? R.ms[ti] : -1.0f) << "}";
+  }
+  o << "]}";
+  return o.str();
+}
+
+static void copy_stats(const RunImpl &R, char *buf, size_t cap) {
+  if (!buf || cap == 0) return;
+  std::string s = stats_json(R);
+  size_t n = std::min(cap - 1, s.size());
+  std::memcpy(buf, s.data(), n);
+  buf[n] = 0;
+}
+
+// ---------------------------------------------------------------------------
+// entry points used by capi.cpp
+
+RunImpl *run_create(gbe_plan *gp, void *stream, bool mbe) {
+  auto *R = new RunImpl();
+  R->gp = gp;
+  try {
+    R->D = dev_plan(gp);
+    CK(cudaSetDevice(R->D->device));
+    R->stream = (cudaStream_t)stream;
+    R->mbe = mbe;
+    run_util(*R);
+  } catch (...) {
+    delete R;
+    throw;
+  }
+  return R;
+}
+
+void run_destroy(RunImpl *R) { delete R; }
+
+gbe_value run_optimum(const RunImpl *R) { return R->optimum; }
+
+void run_value_phase(RunImpl *R, int32_t *assign_out) {
+  CK(cudaSetDevice(R->D->device));
+  run_value(*R, assign_out);
+}
+
+void run_stats(const RunImpl *R, char *buf, size_t cap) { copy_stats(*R, buf, cap); }
+
+void run_table(const RunImpl *R, int32_t t, void *host_out, uint8_t *host_arg) {
+  const Plan &P = *R->gp->plan;
+  if (t < 0 || t >= (int)P.tasks.size()) GBE_FAIL(GBE_E_INVALID, "table %d out of range", t);
+  const Task &T = P.tasks[t];
+  int64_t local = T.shard.hi - T.shard.lo;
+  CK(cudaSetDevice(R->D->device));
+  if (host_out) {
+    const void *src = R->out[t] ? R->out[t] : R->full[t];
+    if (!src) GBE_FAIL(GBE_E_INVALID, "table %d not retained (plan needs \"retain\":\"all\")", t);
+    if (R->full[t] && !R->out[t])  // gathered: this rank's rows start at lo
+      src = (const char *)src + P.prob->elem() * T.shard.lo;
+    CK(cudaMemcpyAsync(host_out, src, P.prob->elem() * local, cudaMemcpyDeviceToHost, R->stream));
+  }
+  if (host_arg) {
+    if (!R->arg[t]) GBE_FAIL(GBE_E_INVALID, "argmin table %d not retained", t);
+    CK(cudaMemcpyAsync(host_arg, R->arg[t], local, cudaMemcpyDeviceToHost, R->stream));
+  }
+  CK(cudaStreamSynchronize(R->stream));
+}
+
+void solve(gbe_plan *gp, void *stream, bool mbe, gbe_value *opt, gbe_value *upper,
+           int32_t *assign_out, char *stats, size_t cap) {
+  RunImpl *R = run_create(gp, stream, mbe);
+  try {
+    if (opt) *opt = R->optimum;
+    std::vector<int32_t> a(std::max(gp->plan->prob->n, 1));
+    run_value(*R, a.data());
+    if (assign_out) std::memcpy(assign_out, a.data(), sizeof(int32_t) * gp->plan->prob->n);
+    if (upper) *upper = problem_evaluate(*gp->plan->prob, a.data());
+    copy_stats(*R, stats, cap);
+  } catch (...) {
+    delete R;
+    throw;
+  }
+  delete R;
+}
+
+// the bare hot primitive
+void bucket_kernel(const gbe_bucket_desc *h, const void *const *dev_inputs, void *dev_out,
+                   uint8_t *dev_arg, int64_t row_begin, int64_t row_end, void *stream) {
+  if (!h) GBE_FAIL(GBE_E_INVALID, "null descriptor");
+  if (h->semiring != GBE_MINSUM_I32 && h->semiring != GBE_MINSUM_F64) GBE_FAIL(GBE_E_INVALID, "bad semiring");
+  if (h->nsep < 0 || h->nsep > GBE_MAX_SEP || h->ninputs < 0 || h->ninputs > GBE_MAX_INPUTS)
+    GBE_FAIL(GBE_E_INVALID, "nsep/ninputs out of range");
+  if (h->d < 1 || h->d > GBE_MAX_DOMAIN) GBE_FAIL(GBE_E_INVALID, "d=%d outside [1,%d]", h->d, GBE_MAX_DOMAIN);
+  int64_t rows = 1;
+  for (int q = 0; q < h->nsep; q++) {
+    if (h->radix[q] < 1) GBE_FAIL(GBE_E_INVALID, "radix[%d] < 1", q);
+    rows *= h->radix[q];
+  }
+  if (rows != h->rows) GBE_FAIL(GBE_E_INVALID, "rows (%lld) != prod(radix) (%lld)", (long long)h->rows, (long long)rows);
+  if (row_begin < 0 || row_end > rows || row_begin > row_end) GBE_FAIL(GBE_E_INVALID, "bad row range");
+  if (h->ninputs && !dev_inputs) GBE_FAIL(GBE_E_INVALID, "null inputs");
+  if (row_end > row_begin && !dev_out) GBE_FAIL(GBE_E_INVALID, "null output");
+  int dev = 0, nsm = 148;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  cudaStream_t s = (cudaStream_t)stream;
+  gbe_bucket_desc *d_desc = (gbe_bucket_desc *)dalloc(sizeof(gbe_bucket_desc), s);
+  CK(cudaMemcpyAsync(d_desc, h, sizeof(gbe_bucket_desc), cudaMemcpyHostToDevice, s));
+  InPtrs in{};
+  for (int j = 0; j < h->ninputs; j++) in.p[j] = dev_inputs[j];
+  BkLaunchInfo li = bk_plan_launch(*h, row_begin, row_end, -1, nsm);
+  CK(bk_launch(*h, d_desc, in, dev_out, dev_arg, row_begin, row_end, li, s));
+  dfree(d_desc, s);
+}
+
+}  // namespace gbe

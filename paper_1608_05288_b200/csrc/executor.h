@@ -1,0 +1,29 @@
+// executor.h — device executor entry points (executor.cpp).
+#pragma once
+#include "common.h"
+
+namespace gbe {
+
+struct RunImpl;
+
+void set_allocator(void *(*a)(size_t, void *, void *), void (*f)(void *, void *), void *u);
+void set_allgather(int (*ag)(const void *, void *, size_t, void *, void *), void *u);
+void dev_plan_free(void *d);
+
+RunImpl *run_create(gbe_plan *gp, void *stream, bool mbe);
+void run_destroy(RunImpl *R);
+gbe_value run_optimum(const RunImpl *R);
+void run_value_phase(RunImpl *R, int32_t *assign_out);
+void run_stats(const RunImpl *R, char *buf, size_t cap);
+void run_table(const RunImpl *R, int32_t t, void *host_out, uint8_t *host_arg);
+
+void solve(gbe_plan *gp, void *stream, bool mbe, gbe_value *opt, gbe_value *upper,
+           int32_t *assign_out, char *stats, size_t cap);
+void bucket_kernel(const gbe_bucket_desc *h, const void *const *dev_inputs, void *dev_out,
+                   uint8_t *dev_arg, int64_t row_begin, int64_t row_end, void *stream);
+
+}  // namespace gbe
+
+struct gbe_run {
+  gbe::RunImpl *impl = nullptr;
+};

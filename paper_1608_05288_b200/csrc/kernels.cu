@@ -1,0 +1,265 @@
+// kernels.cu — sm_100a kernels of the bucket (UTIL-message) computation.
+//
+// BK fuses Gpu::Aggregate (Proc. 4) and Gpu::Eliminate (Proc. 5,
+// P:781-792): for each output row r of a (mini-)bucket and each value v of
+// the eliminated variable, s_v = (+)_j T_j[off_j(r) + v]; out[r] = min_v s_v,
+// arg[r] = first minimiser (A8).  The d^{|sep|+1} aggregated table of the
+// paper is never materialised.  off_j(r) restates the index map Eq.
+// as precomputed per-input strides ("mul/div/mod").
+//
+// Semirings: int32 min-sum with INF = 2^30 and clamp after every add (A9);
+// float64 min-sum (MPE on -log p, A10), inputs added in canonical order.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace gbe {
+namespace {
+
+constexpr uint32_t kInf = GBE_INF_I32;
+
+// ---------------------------------------------------------------------------
+// semiring traits
+
+template <typename T>
+struct Sr;
+
+template <>
+struct Sr<int32_t> {
+  using Acc = uint32_t;  // a, b <= 2^30 -> a + b <= 2^31: no wrap
+  __device__ __forceinline__ static Acc zero() { return 0u; }
+  __device__ __forceinline__ static Acc load(const int32_t *p, int64_t i) {
+    return (uint32_t)__ldg(p + i);
+  }
+  __device__ __forceinline__ static Acc add(Acc a, Acc b) {
+    uint32_t s = a + b;
+    return s < kInf ? s : kInf;
+  }
+  __device__ __forceinline__ static int32_t out(Acc a) { return (int32_t)a; }
+};
+
+template <>
+struct Sr<double> {
+  using Acc = double;
+  __device__ __forceinline__ static Acc zero() { return 0.0; }
+  __device__ __forceinline__ static Acc load(const double *p, int64_t i) { return __ldg(p + i); }
+  __device__ __forceinline__ static Acc add(Acc a, Acc b) { return __dadd_rn(a, b); }
+  __device__ __forceinline__ static double out(Acc a) { return a; }
+};
+
+// ---------------------------------------------------------------------------
+// BK generic: tiles of `plow` consecutive rows (= all values of the `nlow`
+// least-significant output digits).  Per CTA: the low-digit offsets of every
+// input are built once in shared memory; per tile: one base offset per input
+// from the high digits.  Per row: k shared-memory offsets + k*d loads.
+
+template <typename T>
+__global__ void __launch_bounds__(256) bk_generic(const gbe_bucket_desc *__restrict__ D,
+                                                  InPtrs in, T *__restrict__ out,
+                                                  uint8_t *__restrict__ arg, int64_t row_begin,
+                                                  int64_t row_end, int nlow, int plow) {
+  using S = Sr<T>;
+  using Acc = typename S::Acc;
+  extern __shared__ int32_t loff[];  // [k][plow]
+  __shared__ int64_t base[GBE_MAX_INPUTS];
+  const int m = D->nsep, k = D->ninputs, d = D->d;
+  for (int idx = threadIdx.x; idx < k * plow; idx += blockDim.x) {
+    int j = idx / plow, l = idx - j * plow;
+    int64_t o = 0;
+    for (int q = m - 1; q >= m - nlow; q--) {
+      int r = D->radix[q];
+      o += (int64_t)(l % r) * D->stride[j][q];
+      l /= r;
+    }
+    loff[idx] = (int32_t)o;
+  }
+  const int64_t t0 = row_begin / plow, t1 = (row_end - 1) / plow;
+  for (int64_t t = t0 + blockIdx.x; t <= t1; t += gridDim.x) {
+    __syncthreads();
+    if (threadIdx.x < k) {
+      int j = threadIdx.x;
+      int64_t rem = t, o = 0;
+      for (int q = m - nlow - 1; q >= 0; q--) {
+        int r = D->radix[q];
+        o += (rem % r) * D->stride[j][q];
+        rem /= r;
+      }
+      base[j] = o - D->shift[j];
+    }
+    __syncthreads();
+    for (int l = threadIdx.x; l < plow; l += blockDim.x) {
+      int64_t r = t * plow + l;
+      if (r < row_begin || r >= row_end) continue;
+      Acc best = S::zero();
+      int bv = 0;
+      for (int v = 0; v < d; v++) {
+        Acc s = S::zero();
+        for (int j = 0; j < k; j++)
+          s = S::add(s, S::load((const T *)in.p[j], base[j] + loff[j * plow + l] + v));
+        if (v == 0 || s < best) {
+          best = s;
+          bv = v;
+        }
+      }
+      out[r - row_begin] = S::out(best);
+      if (arg) arg[r - row_begin] = (uint8_t)bv;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// relayout of the original tables (declared -> ascending position order)
+
+template <typename T>
+__global__ void relayout_kernel(const T *__restrict__ in, T *__restrict__ out, int nf,
+                                const int64_t *__restrict__ off, const int32_t *__restrict__ poff,
+                                const int32_t *__restrict__ prad,
+                                const int32_t *__restrict__ pstride) {
+  for (int f = blockIdx.x; f < nf; f += gridDim.x) {
+    const int64_t a = off[f], cells = off[f + 1] - a;
+    const int q0 = poff[f], ar = poff[f + 1] - q0;
+    for (int64_t i = threadIdx.x; i < cells; i += blockDim.x) {
+      int64_t rem = i, src = 0;
+      for (int q = ar - 1; q >= 0; q--) {
+        int r = prad[q0 + q];
+        src += (rem % r) * pstride[q0 + q];
+        rem /= r;
+      }
+      out[a + i] = in[a + src];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// value phase: one warp walks the forward order
+
+template <typename T>
+__global__ void value_kernel(const VStep *__restrict__ steps, int s0, int s1,
+                             const VMember *__restrict__ mems, const VTerm *__restrict__ terms,
+                             int32_t *assign, const int32_t *__restrict__ gathered, int gvar, int W,
+                             const void *const *__restrict__ cptrs, int nconst, T *optimum) {
+  using S = Sr<T>;
+  using Acc = typename S::Acc;
+  const int lane = threadIdx.x;
+  if (lane == 0) {
+    if (nconst >= 0) {  // optimum = sum of the constants
+      Acc s = S::zero();
+      for (int c = 0; c < nconst; c++) s = S::add(s, S::load((const T *)cptrs[c], 0));
+      *optimum = S::out(s);
+    }
+    if (gvar >= 0) {
+      int v = -1;
+      for (int w = 0; w < W; w++) v = max(v, gathered[w]);
+      assign[gvar] = v;
+    }
+  }
+  __syncwarp();
+  for (int si = s0; si < s1; si++) {
+    const VStep st = steps[si];
+    if (st.kind == 0) {
+      if (lane == 0) {
+        int64_t row = 0;
+        for (int q = 0; q < st.nterm; q++) row += (int64_t)assign[terms[st.term_off + q].var] * terms[st.term_off + q].stride;
+        assign[st.var] = (row >= st.lo && row < st.hi) ? (int)((const uint8_t *)st.ptr)[row - st.lo] : -1;
+      }
+    } else {
+      Acc best = S::zero();
+      int bv = 1 << 30;
+      for (int v = lane; v < st.d; v += 32) {
+        Acc s = S::zero();
+        for (int mi = 0; mi < st.nmem; mi++) {
+          const VMember mm = mems[st.mem_off + mi];
+          int64_t b = 0;
+          for (int q = 0; q < mm.nterm; q++) b += (int64_t)assign[terms[mm.term_off + q].var] * terms[mm.term_off + q].stride;
+          s = S::add(s, S::load((const T *)mm.ptr, b + v));
+        }
+        if (bv == (1 << 30) || s < best) {
+          best = s;
+          bv = v;
+        }
+      }
+      // lexicographic (value, index) min over the warp
+      for (int o = 16; o > 0; o >>= 1) {
+        Acc ob = __shfl_down_sync(0xffffffffu, best, o);
+        int ov = __shfl_down_sync(0xffffffffu, bv, o);
+        if (ov != (1 << 30) && (bv == (1 << 30) || ob < best || (!(best < ob) && ov < bv))) {
+          best = ob;
+          bv = ov;
+        }
+      }
+      if (lane == 0) assign[st.var] = bv;
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launchers
+
+BkLaunchInfo bk_plan_launch(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end,
+                            int variant, int num_sms) {
+  BkLaunchInfo li{};
+  li.variant = BK_GENERIC;
+  const int k = h.ninputs > 0 ? h.ninputs : 1;
+  const int plow_max = std::max(1, std::min(1024, 12288 / k));  // <= 48 KB smem
+  int nlow = 0, plow = 1;
+  while (nlow < h.nsep && (int64_t)plow * h.radix[h.nsep - 1 - nlow] <= plow_max) {
+    plow *= h.radix[h.nsep - 1 - nlow];
+    nlow++;
+  }
+  li.nlow = nlow;
+  li.plow = plow;
+  li.block = plow >= 256 ? 256 : (plow >= 128 ? 128 : (plow >= 64 ? 64 : 32));
+  li.smem = (size_t)h.ninputs * plow * sizeof(int32_t);
+  int64_t tiles = row_end > row_begin ? (row_end - 1) / plow - row_begin / plow + 1 : 0;
+  int64_t g = std::min<int64_t>(tiles, (int64_t)num_sms * 8);
+  li.grid = (int)std::max<int64_t>(g, 1);
+  (void)variant;
+  return li;
+}
+
+cudaError_t bk_launch(const gbe_bucket_desc &h, const gbe_bucket_desc *dev_desc,
+                      const InPtrs &in, void *out, uint8_t *arg, int64_t row_begin,
+                      int64_t row_end, const BkLaunchInfo &li, cudaStream_t stream) {
+  if (row_end <= row_begin) return cudaSuccess;
+  if (h.semiring == GBE_MINSUM_F64)
+    bk_generic<double><<<li.grid, li.block, li.smem, stream>>>(dev_desc, in, (double *)out, arg,
+                                                                row_begin, row_end, li.nlow, li.plow);
+  else
+    bk_generic<int32_t><<<li.grid, li.block, li.smem, stream>>>(dev_desc, in, (int32_t *)out, arg,
+                                                                 row_begin, row_end, li.nlow, li.plow);
+  return cudaGetLastError();
+}
+
+cudaError_t relayout_launch(const void *in, void *out, int elem, int nf, const int64_t *off,
+                            const int32_t *poff, const int32_t *prad, const int32_t *pstride,
+                            cudaStream_t stream) {
+  if (nf <= 0) return cudaSuccess;
+  int grid = nf < 4096 ? nf : 4096;
+  if (elem == 8)
+    relayout_kernel<double><<<grid, 128, 0, stream>>>((const double *)in, (double *)out, nf, off,
+                                                      poff, prad, pstride);
+  else
+    relayout_kernel<int32_t><<<grid, 128, 0, stream>>>((const int32_t *)in, (int32_t *)out, nf,
+                                                       off, poff, prad, pstride);
+  return cudaGetLastError();
+}
+
+cudaError_t value_launch(bool f64, const VStep *steps, int s0, int s1, const VMember *mems,
+                         const VTerm *terms, int32_t *assign, const int32_t *gathered, int gvar,
+                         int W, const void *const *cptrs, int nconst, void *optimum,
+                         cudaStream_t stream) {
+  if (f64)
+    value_kernel<double><<<1, 32, 0, stream>>>(steps, s0, s1, mems, terms, assign, gathered, gvar,
+                                                W, cptrs, nconst, (double *)optimum);
+  else
+    value_kernel<int32_t><<<1, 32, 0, stream>>>(steps, s0, s1, mems, terms, assign, gathered,
+                                                 gvar, W, cptrs, nconst, (int32_t *)optimum);
+  return cudaGetLastError();
+}
+
+}  // namespace gbe

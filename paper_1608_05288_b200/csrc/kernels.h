@@ -1,0 +1,75 @@
+// kernels.h — host-side launchers of the sm_100a kernels (kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "gbe.h"
+
+namespace gbe {
+
+struct InPtrs {
+  const void *p[GBE_MAX_INPUTS];
+};
+
+// Value-phase program (Alg. 1 lines 6-7; MBE reading A7)
+struct VStep {
+  int32_t var;      // variable assigned by this step
+  int32_t kind;     // 0: argmin lookup in `ptr` (uint8); 1: member sum
+  int32_t d;        // domain size of var
+  int32_t nterm;    // kind 0: row terms
+  int64_t term_off; // kind 0: first VTerm
+  int64_t lo, hi;   // kind 0: rows held locally [lo, hi) (row sharding)
+  const void *ptr;  // kind 0: argmin table (first local row)
+  int32_t nmem;     // kind 1: members
+  int32_t pad;
+  int64_t mem_off;  // kind 1: first VMember
+};
+struct VMember {
+  const void *ptr;  // member table (scope ascending by position, var last)
+  int64_t term_off; // first VTerm
+  int32_t nterm;
+  int32_t pad;
+};
+struct VTerm {
+  int32_t var;
+  int32_t pad;
+  int64_t stride;
+};
+
+// Kernel variants for the fused aggregate+project bucket kernel (BK)
+enum BkVariant { BK_AUTO = -1, BK_GENERIC = 0 };
+
+// Describes how the launcher tiles one bucket (computed on the host from the
+// descriptor; see kernels.cu).
+struct BkLaunchInfo {
+  int variant;
+  int nlow, plow;  // low digits per tile, rows per tile
+  int grid, block;
+  size_t smem;
+};
+
+BkLaunchInfo bk_plan_launch(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end,
+                            int variant, int num_sms);
+
+// dev_desc: device copy of `h` (the launcher reads scalars from `h`).
+cudaError_t bk_launch(const gbe_bucket_desc &h, const gbe_bucket_desc *dev_desc,
+                      const InPtrs &in, void *out, uint8_t *arg, int64_t row_begin,
+                      int64_t row_end, const BkLaunchInfo &li, cudaStream_t stream);
+
+// Relayout of the original tables from declared to sorted scope order
+// (P:624): for each function f, out[off[f] + i] = in[off[f] + sum_q
+// digit_q(i) * pstride[poff[f] + q]] with digits over radices prad.
+cudaError_t relayout_launch(const void *in, void *out, int elem, int nf, const int64_t *off,
+                            const int32_t *poff, const int32_t *prad, const int32_t *pstride,
+                            cudaStream_t stream);
+
+// Value phase over steps [s0, s1); single warp.  If gvar >= 0 the kernel
+// first sets assign[gvar] = max(gathered[0..W)).  If nconst >= 0 it first
+// sums the nconst constants (canonical order) into *optimum.
+cudaError_t value_launch(bool f64, const VStep *steps, int s0, int s1, const VMember *mems,
+                         const VTerm *terms, int32_t *assign, const int32_t *gathered, int gvar,
+                         int W, const void *const *cptrs, int nconst, void *optimum,
+                         cudaStream_t stream);
+
+}  // namespace gbe

@@ -1,0 +1,406 @@
+// planner.cpp — host planner: primal graph, orderings, induced width,
+// (mini-)bucket construction, canonical layouts, stride maps, row-shard plan.
+//
+// Alg. 3 lines 1-4 and §6.2 re-designed: the whole
+// symbolic elimination is planned once, so the device loop only launches
+// kernels.  Readings: A1 (bucket of the latest-ordered variable), A2 (scopes
+// ascending by order position, eliminated variable last = stride 1), A3
+// (min-fill ties), A5/A6 (i-bound = generated arity, greedy first-fit).
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <sstream>
+
+#include "common.h"
+
+namespace gbe {
+
+// ---------------------------------------------------------------------------
+// graph structure
+
+std::vector<std::vector<char>> primal_adjacency(const Problem &p) {
+  std::vector<std::vector<char>> adj(p.n, std::vector<char>(p.n, 0));
+  for (int f = 0; f < p.nf; f++) {
+    const int32_t *sc = p.scope(f);
+    for (int a = 0; a < p.arity[f]; a++)
+      for (int b = a + 1; b < p.arity[f]; b++) adj[sc[a]][sc[b]] = adj[sc[b]][sc[a]] = 1;
+  }
+  return adj;
+}
+
+namespace {
+// bitset adjacency for the O(n^3)-ish greedy heuristics
+struct Bits {
+  int n, w;
+  std::vector<uint64_t> b;
+  Bits(int n_) : n(n_), w((n_ + 63) / 64), b((size_t)n_ * ((n_ + 63) / 64), 0) {}
+  uint64_t *row(int v) { return b.data() + (size_t)v * w; }
+  bool get(int u, int v) const { return (b[(size_t)u * w + v / 64] >> (v % 64)) & 1; }
+  void set(int u, int v) { b[(size_t)u * w + v / 64] |= 1ull << (v % 64); }
+};
+}  // namespace
+
+// greedy min-fill: key (fill-in edges, current degree, id), first eliminated
+// variable = last in the ordering (A3)
+void order_minfill(const Problem &p, std::vector<int32_t> &order) {
+  int n = p.n;
+  Bits g(n);
+  auto adj = primal_adjacency(p);
+  for (int u = 0; u < n; u++)
+    for (int v = 0; v < n; v++)
+      if (adj[u][v]) g.set(u, v);
+  std::vector<char> alive(n, 1);
+  order.assign(n, -1);
+  std::vector<int> nb;
+  for (int step = 0; step < n; step++) {
+    int best = -1;
+    long long bfill = 0, bdeg = 0;
+    for (int v = 0; v < n; v++) {
+      if (!alive[v]) continue;
+      nb.clear();
+      for (int u = 0; u < n; u++)
+        if (alive[u] && g.get(v, u)) nb.push_back(u);
+      long long fill = 0;
+      for (size_t a = 0; a < nb.size(); a++)
+        for (size_t c = a + 1; c < nb.size(); c++)
+          if (!g.get(nb[a], nb[c])) fill++;
+      long long deg = (long long)nb.size();
+      if (best < 0 || fill < bfill || (fill == bfill && deg < bdeg)) {
+        best = v;
+        bfill = fill;
+        bdeg = deg;
+      }
+    }
+    nb.clear();
+    for (int u = 0; u < n; u++)
+      if (alive[u] && g.get(best, u)) nb.push_back(u);
+    for (int a : nb)
+      for (int c : nb)
+        if (a != c) g.set(a, c);
+    alive[best] = 0;
+    order[n - 1 - step] = best;
+  }
+}
+
+// x_i before x_j iff |N(x_i)| < |N(x_j)|, ties by id (stable sort)
+void order_degree(const Problem &p, std::vector<int32_t> &order) {
+  auto adj = primal_adjacency(p);
+  std::vector<int> deg(p.n, 0);
+  for (int v = 0; v < p.n; v++)
+    for (int u = 0; u < p.n; u++) deg[v] += adj[v][u];
+  order.resize(p.n);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return deg[a] < deg[b]; });
+}
+
+// Definition
+int32_t induced_width(const Problem &p, const std::vector<int32_t> &order) {
+  int n = p.n;
+  Bits g(n);
+  auto adj = primal_adjacency(p);
+  for (int u = 0; u < n; u++)
+    for (int v = 0; v < n; v++)
+      if (adj[u][v]) g.set(u, v);
+  std::vector<int> pos(n);
+  for (int i = 0; i < n; i++) pos[order[i]] = i;
+  int32_t w = 0;
+  std::vector<int> prev;
+  for (int i = n - 1; i >= 0; i--) {
+    int v = order[i];
+    prev.clear();
+    for (int u = 0; u < n; u++)
+      if (g.get(v, u) && pos[u] < i) prev.push_back(u);
+    w = std::max<int32_t>(w, (int32_t)prev.size());
+    for (int a : prev)
+      for (int c : prev)
+        if (a != c) g.set(a, c);
+  }
+  return w;
+}
+
+// ---------------------------------------------------------------------------
+// plan
+
+namespace {
+
+int64_t mul_sat(int64_t a, int64_t b) {
+  if (a != 0 && b > (int64_t(1) << 62) / a) return int64_t(1) << 62;
+  return a * b;
+}
+
+}  // namespace
+
+std::unique_ptr<Plan> make_plan(std::shared_ptr<const Problem> pp, const int32_t *order_in,
+                                int32_t ibound, const ExecOptions &ex) {
+  const Problem &p = *pp;
+  auto plan = std::make_unique<Plan>();
+  plan->prob = pp;
+  plan->ibound = ibound;
+  plan->ex = ex;
+  int n = p.n;
+  if (ex.world_size < 1 || ex.rank < 0 || ex.rank >= ex.world_size)
+    GBE_FAIL(GBE_E_INVALID, "bad world_size/rank (%d/%d)", ex.world_size, ex.rank);
+  plan->order.assign(order_in, order_in + n);
+  plan->pos.assign(n, -1);
+  for (int i = 0; i < n; i++) {
+    int v = plan->order[i];
+    if (v < 0 || v >= n || plan->pos[v] >= 0) GBE_FAIL(GBE_E_INVALID, "order is not a permutation (entry %d)", i);
+    plan->pos[v] = i;
+  }
+  const auto &pos = plan->pos;
+  plan->width = induced_width(p, plan->order);
+
+  // relayout of the originals: sorted scope (ascending position), eliminated
+  // (latest) variable last; perm_strides[f][q] = stride in the DECLARED table
+  // of the q-th sorted scope variable
+  plan->sorted_off.assign(p.nf + 1, 0);
+  for (int f = 0; f < p.nf; f++) plan->sorted_off[f + 1] = p.table_off[f + 1];
+  std::vector<std::vector<int32_t>> sorted_scope(p.nf);
+  plan->perm_strides.clear();
+  for (int f = 0; f < p.nf; f++) {
+    const int32_t *sc = p.scope(f);
+    std::vector<int32_t> s(sc, sc + p.arity[f]);
+    std::vector<int64_t> decl_stride(p.arity[f]);
+    int64_t st = 1;
+    for (int a = p.arity[f] - 1; a >= 0; a--) {
+      decl_stride[a] = st;
+      st *= p.dom[sc[a]];
+    }
+    std::vector<int> idx(p.arity[f]);
+    std::iota(idx.begin(), idx.end(), 0);
+    std::sort(idx.begin(), idx.end(), [&](int a, int b) { return pos[sc[a]] < pos[sc[b]]; });
+    for (int a = 0; a < p.arity[f]; a++) {
+      s[a] = sc[idx[a]];
+      plan->perm_strides.push_back((int32_t)decl_stride[idx[a]]);
+    }
+    sorted_scope[f] = s;
+  }
+
+  // bucket membership (A1): latest-ordered scope variable
+  plan->bucket.assign(n, {});
+  for (int f = 0; f < p.nf; f++) {
+    if (p.arity[f] == 0) {
+      plan->constants.push_back({0, f});
+      continue;
+    }
+    plan->bucket[sorted_scope[f].back()].push_back({0, f});
+  }
+
+  std::vector<std::vector<Member>> pending = plan->bucket;  // grows with messages
+  auto scope_of = [&](const Member &m) -> const std::vector<int32_t> & {
+    return m.kind == 0 ? sorted_scope[m.index] : plan->tasks[m.index].sep;
+  };
+  auto cells_of = [&](const Member &m) -> int64_t {
+    if (m.kind == 0) return p.table_off[m.index + 1] - p.table_off[m.index];
+    return plan->tasks[m.index].rows;
+  };
+
+  plan->var_task.assign(n, -1);
+  std::vector<char> inU(n, 0);
+  for (int i = n - 1; i >= 0; i--) {
+    int x = plan->order[i];
+    const std::vector<Member> &B = pending[x];
+    plan->bucket[x] = B;  // canonical B_x (originals, then messages by creation)
+    int nm = (int)B.size();
+    std::vector<int> mb_of(nm, 0);
+    int nmb = 1;
+    if (ibound >= 0 && nm > 0) {
+      // A6: members by descending arity (stable), first fit with |U| <= i+1
+      std::vector<int> ordm(nm);
+      std::iota(ordm.begin(), ordm.end(), 0);
+      std::stable_sort(ordm.begin(), ordm.end(), [&](int a, int b) {
+        return scope_of(B[a]).size() > scope_of(B[b]).size();
+      });
+      std::vector<std::vector<char>> sets;
+      std::vector<int> sizes;
+      for (int a : ordm) {
+        const auto &sc = scope_of(B[a]);
+        if ((int)sc.size() > ibound + 1)
+          GBE_FAIL(GBE_E_INVALID, "i-bound %d below a member of arity %zu in the bucket of x%d",
+                   ibound, sc.size(), x);
+        int placed = -1;
+        for (int b = 0; b < (int)sets.size() && placed < 0; b++) {
+          int extra = 0;
+          for (int v : sc) extra += !sets[b][v];
+          if (sizes[b] + extra <= ibound + 1) placed = b;
+        }
+        if (placed < 0) {
+          placed = (int)sets.size();
+          sets.emplace_back(n, 0);
+          sizes.push_back(0);
+        }
+        for (int v : sc)
+          if (!sets[placed][v]) {
+            sets[placed][v] = 1;
+            sizes[placed]++;
+          }
+        mb_of[a] = placed;
+      }
+      nmb = (int)sets.size();
+    }
+    for (int b = 0; b < nmb; b++) {
+      Task t;
+      t.var = x;
+      t.mb = b;
+      t.d = p.dom[x];
+      for (int k = 0; k < nm; k++)
+        if (mb_of[k] == b) t.members.push_back(B[k]);
+      if ((int)t.members.size() > GBE_MAX_INPUTS)
+        GBE_FAIL(GBE_E_INVALID, "bucket of x%d has %zu inputs (> %d)", x, t.members.size(), GBE_MAX_INPUTS);
+      std::fill(inU.begin(), inU.end(), 0);
+      for (auto &m : t.members)
+        for (int v : scope_of(m)) inU[v] = 1;
+      for (int v = 0; v < n; v++)
+        if (inU[v] && v != x) t.sep.push_back(v);
+      std::sort(t.sep.begin(), t.sep.end(), [&](int a, int c) { return pos[a] < pos[c]; });
+      if ((int)t.sep.size() > GBE_MAX_SEP)
+        GBE_FAIL(GBE_E_BUDGET, "bucket x%d: separator of %zu variables (> %d)", x, t.sep.size(), GBE_MAX_SEP);
+      t.rows = 1;
+      for (int v : t.sep) t.rows = mul_sat(t.rows, p.dom[v]);
+      if (t.rows >= (int64_t(1) << 62) / 256)
+        GBE_FAIL(GBE_E_BUDGET, "bucket x%d: %.3g rows exceed addressable memory", x, (double)t.rows);
+      t.dest = t.sep.empty() ? -1 : t.sep.back();
+      // descriptor: radices + stride maps (Eq. P:673-697 as per-input strides)
+      gbe_bucket_desc &D = t.desc;
+      D.semiring = p.sr;
+      D.nsep = (int32_t)t.sep.size();
+      D.d = t.d;
+      D.ninputs = (int32_t)t.members.size();
+      D.rows = t.rows;
+      for (int q = 0; q < D.nsep; q++) D.radix[q] = p.dom[t.sep[q]];
+      t.in_cells = 0;
+      for (int j = 0; j < D.ninputs; j++) {
+        const auto &sc = scope_of(t.members[j]);
+        // member tables are ascending by position with x last
+        int64_t st = 1;
+        std::vector<int64_t> stv(n, 0);
+        for (int a = (int)sc.size() - 1; a >= 0; a--) {
+          stv[sc[a]] = st;
+          st *= p.dom[sc[a]];
+        }
+        if (sc.empty() || sc.back() != x) GBE_FAIL(GBE_E_INTERNAL, "member of x%d does not end with x", x);
+        for (int q = 0; q < D.nsep; q++) D.stride[j][q] = stv[t.sep[q]];
+        D.shift[j] = 0;
+        t.in_cells += cells_of(t.members[j]);
+        if (t.members[j].kind == 1) plan->tasks[t.members[j].index].consumer = (int)plan->tasks.size();
+      }
+      int h = 0;
+      for (auto &m : t.members)
+        if (m.kind == 1) h = std::max(h, plan->tasks[m.index].height + 1);
+      t.height = h;
+      int tid = (int)plan->tasks.size();
+      if (plan->var_task[x] < 0) plan->var_task[x] = tid;
+      plan->tasks.push_back(t);
+      if (t.dest >= 0)
+        pending[t.dest].push_back({1, tid});
+      else
+        plan->constants.push_back({1, tid});
+    }
+  }
+
+  // totals: algorithmic bytes = inputs once + output + argmin
+  const int64_t el = (int64_t)p.elem();
+  plan->total_cells = 0;
+  plan->total_bytes = 0;
+  for (auto &t : plan->tasks) {
+    plan->total_cells += t.rows * t.d;
+    plan->total_bytes += el * t.in_cells + el * t.rows + t.rows;
+  }
+
+  // row-shard plan: only tasks with >= shard_min_rows rows
+  const int W = ex.world_size;
+  for (auto &t : plan->tasks) {
+    Shard &s = t.shard;
+    s = Shard{};
+    s.lo = 0;
+    s.hi = t.rows;
+    if (W <= 1 || t.rows < ex.shard_min_rows || t.sep.empty()) continue;
+    int64_t blocks = 1;
+    int kd = 0;
+    while (kd < (int)t.sep.size() && blocks < 16LL * W) blocks *= p.dom[t.sep[kd++]];
+    if (blocks < W) continue;
+    s.on = true;
+    s.key_digits = kd;
+    s.blocks = blocks;
+    s.block_rows = t.rows / blocks;
+    s.per = (blocks + W - 1) / W;
+    int64_t b0 = std::min<int64_t>((int64_t)ex.rank * s.per, blocks);
+    int64_t b1 = std::min<int64_t>(b0 + s.per, blocks);
+    s.lo = b0 * s.block_rows;
+    s.hi = b1 * s.block_rows;
+  }
+  // a sharded message can stay sharded only if its consumer is sharded on
+  // the same key variables (then the consumer's rows need exactly the local
+  // block range); otherwise it is all-gathered after it is produced
+  for (size_t ti = 0; ti < plan->tasks.size(); ti++) {
+    Task &t = plan->tasks[ti];
+    if (!t.shard.on) continue;
+    bool keep = false;
+    if (t.consumer >= 0) {
+      const Task &c = plan->tasks[t.consumer];
+      if (c.shard.on && c.shard.key_digits <= (int)t.sep.size()) {
+        keep = c.shard.key_digits == t.shard.key_digits;
+        for (int q = 0; keep && q < c.shard.key_digits; q++) keep = c.sep[q] == t.sep[q];
+      }
+    }
+    t.shard.gather = !keep || ibound >= 0;  // MBE value phase reads whole messages
+  }
+
+  // device memory estimate (executor allocation sequence)
+  int64_t live = 0, peak = 0;
+  live += 2 * el * p.table_off[p.nf];
+  std::vector<int64_t> msg_bytes(plan->tasks.size(), 0);
+  for (size_t ti = 0; ti < plan->tasks.size(); ti++) {
+    const Task &t = plan->tasks[ti];
+    int64_t local = t.shard.on ? (t.shard.hi - t.shard.lo) : t.rows;
+    int64_t full = t.shard.on && t.shard.gather ? t.shard.per * t.shard.block_rows * W : 0;
+    msg_bytes[ti] = el * (local + full);
+    live += msg_bytes[ti] + local;  // message + argmin
+    peak = std::max(peak, live);
+    if (plan->ex.retain < 2 && ibound < 0)
+      for (auto &m : t.members)
+        if (m.kind == 1) live -= msg_bytes[m.index];
+    if (plan->ex.retain == 0) live -= local;
+  }
+  plan->peak_bytes = peak;
+  if (ex.budget_bytes > 0 && peak > ex.budget_bytes) {
+    // name the largest bucket
+    const Task *big = &plan->tasks[0];
+    for (auto &t : plan->tasks)
+      if (t.rows > big->rows) big = &t;
+    GBE_FAIL(GBE_E_BUDGET, "bucket x%d: %.3g rows; plan needs %.3g bytes > budget %.3g", big->var,
+             (double)big->rows, (double)peak, (double)ex.budget_bytes);
+  }
+  return plan;
+}
+
+std::string plan_json(const Plan &plan) {
+  std::ostringstream o;
+  o << "{\"n\":" << plan.prob->n << ",\"ibound\":" << plan.ibound << ",\"width\":" << plan.width
+    << ",\"total_cells\":" << plan.total_cells << ",\"total_bytes\":" << plan.total_bytes
+    << ",\"peak_bytes\":" << plan.peak_bytes << ",\"world_size\":" << plan.ex.world_size
+    << ",\"rank\":" << plan.ex.rank << ",\"order\":[";
+  for (size_t i = 0; i < plan.order.size(); i++) o << (i ? "," : "") << plan.order[i];
+  o << "],\"constants\":[";
+  for (size_t i = 0; i < plan.constants.size(); i++)
+    o << (i ? "," : "") << "[" << plan.constants[i].kind << "," << plan.constants[i].index << "]";
+  o << "],\"tables\":[";
+  for (size_t ti = 0; ti < plan.tasks.size(); ti++) {
+    const Task &t = plan.tasks[ti];
+    o << (ti ? "," : "") << "{\"var\":" << t.var << ",\"mb\":" << t.mb << ",\"rows\":" << t.rows
+      << ",\"d\":" << t.d << ",\"dest\":" << t.dest << ",\"consumer\":" << t.consumer
+      << ",\"height\":" << t.height << ",\"in_cells\":" << t.in_cells << ",\"sep\":[";
+    for (size_t q = 0; q < t.sep.size(); q++) o << (q ? "," : "") << t.sep[q];
+    o << "],\"members\":[";
+    for (size_t k = 0; k < t.members.size(); k++)
+      o << (k ? "," : "") << "[" << t.members[k].kind << "," << t.members[k].index << "]";
+    o << "],\"shard\":{\"on\":" << (t.shard.on ? "true" : "false") << ",\"key_digits\":"
+      << t.shard.key_digits << ",\"blocks\":" << t.shard.blocks << ",\"per\":" << t.shard.per
+      << ",\"lo\":" << t.shard.lo << ",\"hi\":" << t.shard.hi
+      << ",\"gather\":" << (t.shard.gather ? "true" : "false") << "}}";
+  }
+  o << "]}";
+  return o.str();
+}
+
+}  // namespace gbe

@@ -1,0 +1,186 @@
+"""Host-side checks of libgbe (-m "not gpu"): the library loads, exports every
+symbol include/gbe.h declares, and its host logic (orderings, induced width,
+pseudo-tree, bucket plan, mini-bucket partition, loaders, evaluate, shard
+plan) agrees with the independent oracle.  No kernel is launched here."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+import paper_1608_05288_b200 as G
+from gen import configs
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_every_declared_symbol_is_exported():
+    hdr = open(os.path.join(ROOT, "include", "gbe.h")).read()
+    declared = set(re.findall(r"\b(gbe_[a-z_0-9]+)\s*\(", hdr))
+    declared -= {"gbe_bucket_desc"}
+    L = G.lib()
+    missing = [s for s in sorted(declared) if not hasattr(L, s)]
+    assert not missing, missing
+    assert set(G.gbe.EXPORTED) <= declared
+
+
+def test_solve_without_device_fails_loudly():
+    """No CPU fallback: a solve on a box without a GPU must raise."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a device is present")
+    inst = gen.random_graph(6, 2, 7, 0, 0.0, 1)
+    P = G.Problem.from_instance(inst)
+    plan = G.Plan(P, P.order()[0])
+    with pytest.raises(G.GbeError) as e:
+        plan.solve_be()
+    assert e.value.status == 4
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_orderings_and_width_match_oracle(seed):
+    inst = gen.scalefree(40, 3, 0.0, seed) if seed % 2 else gen.random_graph(30, 3, 60, 0, 0.0, seed)
+    P = G.Problem.from_instance(inst)
+    o, w = P.order(G.ORDER_MINFILL)
+    assert list(o) == list(oracle.minfill_order(inst))
+    assert w == oracle.induced_width(inst, o)
+    o2, w2 = P.order(G.ORDER_PAPER_DEGREE)
+    assert list(o2) == list(oracle.degree_order(inst))
+    assert w2 == oracle.induced_width(inst, o2)
+    par, ss = P.pseudotree(o)
+    assert list(par) == list(oracle.elim_tree(inst, o))
+
+
+def _same_structure(plan_info, run):
+    tabs = plan_info["tables"]
+    assert len(tabs) == len(run.tables)
+    for a, b in zip(tabs, run.tables):
+        assert a["var"] == b.var and a["mb"] == b.mb and a["rows"] == b.rows
+        assert a["sep"] == [int(v) for v in b.sep]
+        assert [tuple(m) for m in a["members"]] == list(b.members)
+        assert a["dest"] == b.dest
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_be_plan_matches_oracle_buckets(seed):
+    inst = gen.random_network(14, 2, 4, 18, 1, 3, 100, 0.2, seed)
+    P = G.Problem.from_instance(inst)
+    o, _ = P.order()
+    _same_structure(G.Plan(P, o).info(), oracle.solve_be(inst, o))
+
+
+@pytest.mark.parametrize("ib", [1, 2, 3, 4, 6])
+def test_mbe_partition_matches_oracle(ib):
+    inst = gen.random_graph(16, 3, 40, 0, 0.0, ib)
+    P = G.Problem.from_instance(inst)
+    o, _ = P.order()
+    _same_structure(G.Plan(P, o, ib).info(), oracle.solve_mbe(inst, o, ib))
+
+
+def test_example4_partition_through_the_abi():
+    """Example 4, z = 1: B4 splits into three singletons."""
+    inst = gen.Instance.from_functions([2] * 4, [((0, 1), [1, 2, 3, 4]), ((0, 3), [1, 2, 3, 4]),
+                                                 ((1, 2), [1, 2, 3, 4]), ((1, 3), [1, 2, 3, 4]),
+                                                 ((2, 3), [1, 2, 3, 4])])
+    info = G.Plan(G.Problem.from_instance(inst), [0, 1, 2, 3], 1).info()
+    b4 = [t for t in info["tables"] if t["var"] == 3]
+    assert [t["members"] for t in b4] == [[[0, 1]], [[0, 3]], [[0, 4]]]
+    with pytest.raises(G.GbeError) as e:
+        G.Plan(G.Problem.from_instance(inst), [0, 1, 2, 3], 0)
+    assert e.value.status == 1
+
+
+def test_invalid_inputs_rejected():
+    with pytest.raises(G.GbeError):
+        G.Problem.create([2, 2], [2], [0, 0], [0, 0, 0, 0])  # duplicate scope var
+    with pytest.raises(G.GbeError):
+        G.Problem.create([2, 300], [1], [1], [0] * 300)  # domain > 256
+    with pytest.raises(G.GbeError):
+        G.Problem.create([2], [1], [0], [-1, 0])  # negative cost
+    p = G.Problem.create([2, 2], [2], [0, 1], [0, 1, 2, 3])
+    with pytest.raises(G.GbeError):
+        G.Plan(p, [0, 0])  # not a permutation
+    with pytest.raises(G.GbeError):
+        G.Plan(p, [0, 1], -1, retain="sometimes")
+
+
+def test_budget_error_names_the_bucket():
+    """a plan that exceeds the memory budget is refused up front."""
+    inst = configs.c4()
+    P = G.Problem.from_instance(inst)
+    o, w = P.order()
+    with pytest.raises(G.GbeError) as e:
+        G.Plan(P, o, budget_bytes=1 << 30)
+    assert e.value.status == 3 and "rows" in str(e.value) and "bucket x" in str(e.value)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_evaluate_matches_oracle(seed):
+    for inst in (gen.random_network(10, 2, 4, 12, 0, 3, 100, 0.3, seed),
+                 gen.belief_net(12, 2, 4, 3, 5, seed)):
+        P = G.Problem.from_instance(inst)
+        rng = np.random.default_rng(seed)
+        for _ in range(5):
+            a = np.array([rng.integers(d) for d in inst.dom], dtype=np.int32)
+            assert P.evaluate(a) == oracle.evaluate(inst, a)
+
+
+def test_wcsp_roundtrip(tmp_path):
+    inst = gen.random_network(9, 2, 4, 11, 0, 3, 100, 0.3, 5)
+    path = str(tmp_path / "x.wcsp")
+    gen.write_wcsp(inst, path)
+    P = G.Problem.load_wcsp(path)
+    rng = np.random.default_rng(0)
+    for _ in range(20):
+        a = np.array([rng.integers(d) for d in inst.dom], dtype=np.int32)
+        assert P.evaluate(a) == oracle.evaluate(inst, a)
+
+
+def test_wcsp_parse_error_has_line(tmp_path):
+    path = tmp_path / "bad.wcsp"
+    path.write_text("x 2 2 1 1000\n2 2\n2 0 1 0 2\n0 0 5\n0 1\n")
+    with pytest.raises(G.GbeError) as e:
+        G.Problem.load_wcsp(str(path))
+    assert e.value.status == 2 and "line 5" in str(e.value)
+
+
+def test_uai_roundtrip_and_evidence(tmp_path):
+    inst = gen.belief_net(8, 2, 3, 2, 4, 3)
+    path = str(tmp_path / "x.uai")
+    gen.write_uai(inst, path)
+    P = G.Problem.load_uai(path)
+    a = np.zeros(8, np.int32)
+    assert P.evaluate(a) == pytest.approx(oracle.evaluate(inst, a), rel=1e-12)
+    ev = tmp_path / "x.evid"
+    ev.write_text("1 3 1\n")
+    Pe = G.Problem.load_uai(path, str(ev))
+    a[3] = 0
+    assert Pe.evaluate(a) == float("inf")
+    a[3] = 1
+    assert Pe.evaluate(a) == pytest.approx(oracle.evaluate(inst, a), rel=1e-12)
+    ev.write_text("1 3 7\n")
+    with pytest.raises(G.GbeError) as e:
+        G.Problem.load_uai(path, str(ev))
+    assert e.value.status == 1
+
+
+def test_generate_matches_gen_module():
+    """gbe_generate uses the same seeded generator module as gen/."""
+    P = G.Problem.generate(topology="scalefree", n=50, d=3, seed=4)
+    inst = gen.scalefree(50, 3, 0.0, 4)
+    rng = np.random.default_rng(1)
+    for _ in range(10):
+        a = np.array([rng.integers(3) for _ in range(50)], dtype=np.int32)
+        assert P.evaluate(a) == oracle.evaluate(inst, a)
+
+
+def test_c4_plan_shape():
+    """BASELINE C4 (BA n=200, d=3, w*=20): largest UTIL table 3^20 rows."""
+    P = G.Problem.from_instance(configs.c4())
+    o, w = P.order()
+    assert w == 20
+    info = G.Plan(P, o).info()
+    assert max(t["rows"] for t in info["tables"]) == 3 ** 20
+    assert info["total_cells"] == sum(t["rows"] * t["d"] for t in info["tables"])
