@@ -212,6 +212,11 @@ gbe_status gbe_bucket_kernel(const void *desc, const void *const *dev_inputs, vo
                              uint8_t *dev_arg, int64_t row_begin, int64_t row_end,
                              void *stream);
 
+/* Which kernel variant gbe_bucket_kernel would run for this descriptor and
+ * row range: 0 = generic (per-row decode), 1 = tiled TMA + register-blocked
+ * (DESIGN.md §5).  Returns -1 for an invalid descriptor. */
+int32_t gbe_bucket_kernel_variant(const void *desc, int64_t row_begin, int64_t row_end);
+
 /* ---------------------------------------------------------------------
  * Hooks
  * ------------------------------------------------------------------- */

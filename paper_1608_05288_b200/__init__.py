@@ -5,7 +5,7 @@ kernels; `gbe` is its thin ctypes binding.  PyTorch is used only for device
 memory, streams and process groups (see paper_1608_05288_b200.dist).
 """
 from .gbe import (  # noqa: F401
-    BucketDesc, GbeError, Plan, Problem, Run, bucket_kernel, lib, set_allgather,
+    BucketDesc, GbeError, bucket_kernel_variant, Plan, Problem, Run, bucket_kernel, lib, set_allgather,
     set_allocator, version, INF_I32, MINSUM_I32, MINSUM_F64, ORDER_MINFILL,
     ORDER_PAPER_DEGREE, ORDER_GIVEN,
 )

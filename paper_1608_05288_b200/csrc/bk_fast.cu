@@ -1,0 +1,452 @@
+// bk_fast.cu — the tiled, TMA-staged, register-blocked bucket kernel (BK).
+//
+// Same operation as bk_generic (Proc. 4 + Proc. 5 fused), mapped
+// to sm_100a:
+//  * A tile = all values of the trailing output digits L (P_L rows).  For every
+//    input j the tile's slice is ONE contiguous range of d*prod(L ∩ S_j)
+//    elements (the eliminated variable and the trailing output variables are
+//    the least-significant digits of every input), so each tile
+//    needs one 1-D TMA bulk copy (cp.async.bulk, UBLKCP) per input, into a
+//    2-stage shared-memory ring signalled by an mbarrier.  Small child tables
+//    land in shared memory whole; large ones stream slice by slice.
+//  * Inside a tile each thread owns R x R x d cells: all values of two
+//    chosen "group" digits g1, g2 in L and of the eliminated variable.  Inputs
+//    are split by which group digits they contain; an input missing a group
+//    digit is loaded once and reused across that digit's R values, so the
+//    shared-memory loads and saturating adds per cell drop from k to
+//    sum_j R^-|{g1,g2} \ S_j| (the host picks g1, g2 to minimise this).
+//  * Index math is per tile (one mixed-radix decode by warp 0) and per thread
+//    group (a shared-memory offset table built once per CTA): no per-row
+//    div/mod.
+//  * Output rows are staged in shared memory and written back coalesced.
+//  * Tile order: the output digits missing from the largest input vary
+//    fastest, so tiles that re-read the same input slice run back to back and
+//    hit L2 instead of HBM.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "bk_fast.h"
+
+namespace gbe {
+namespace {
+
+constexpr uint32_t kInf = GBE_INF_I32;
+
+template <typename T>
+struct SrF;
+template <>
+struct SrF<int32_t> {
+  using Acc = uint32_t;
+  __device__ __forceinline__ static Acc zero() { return 0u; }
+  __device__ __forceinline__ static Acc add(Acc a, Acc b) {
+    uint32_t s = a + b;
+    return s < kInf ? s : kInf;
+  }
+  __device__ __forceinline__ static Acc add3(Acc a, Acc b, Acc c) {  // a,b,c <= 2^30
+    uint32_t s = a + b + c;
+    return s < kInf ? s : kInf;
+  }
+  __device__ __forceinline__ static int32_t out(Acc a) { return (int32_t)a; }
+};
+template <>
+struct SrF<double> {
+  using Acc = double;
+  __device__ __forceinline__ static Acc zero() { return 0.0; }
+  __device__ __forceinline__ static Acc add(Acc a, Acc b) { return __dadd_rn(a, b); }
+  __device__ __forceinline__ static Acc add3(Acc a, Acc b, Acc c) { return __dadd_rn(__dadd_rn(a, b), c); }
+  __device__ __forceinline__ static double out(Acc a) { return a; }
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void *smem_dst, const void *gsrc, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Warp 0 issues the TMA copies of tile t into stage s.
+__device__ __forceinline__ void issue_tile(const FastDesc *__restrict__ Fg, const FastHot &f,
+                                           const InPtrs &in, int64_t t, int s, unsigned char *sm,
+                                           uint64_t *bars, int32_t *delta, int64_t *rowstart) {
+  const int lane = threadIdx.x & 31;
+  int dig = 0;
+  if (lane < f.nH) dig = (int)(((uint64_t)t / (uint64_t)Fg->hdiv[lane]) % (uint64_t)Fg->hrad[lane]);
+  int64_t base = 0, rs = 0;
+  for (int e = 0; e < f.nH; e++) {
+    int de = __shfl_sync(0xffffffffu, dig, e);
+    if (lane < f.k) base += (int64_t)de * Fg->hstr[e][lane];
+    if (lane == 0) rs += (int64_t)de * Fg->hrow[e];
+  }
+  uint32_t bytes = 0;
+  uintptr_t src = 0;
+  if (lane < f.k) {
+    base -= Fg->shift[lane];
+    const char *p = (const char *)in.p[f.in_idx[lane]] + base * f.es;
+    uintptr_t a16 = (uintptr_t)p & ~(uintptr_t)15;
+    uintptr_t e16 = ((uintptr_t)p + (uintptr_t)f.slen[lane] * f.es + 15) & ~(uintptr_t)15;
+    bytes = (uint32_t)(e16 - a16);
+    src = a16;
+    delta[s * 32 + lane] = (int32_t)(((uintptr_t)p - a16) / f.es);
+  }
+  uint32_t total = bytes;
+  for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+  if (lane == 0) rowstart[s] = rs;
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence_block();
+    mbar_arrive_expect_tx(&bars[s], total);
+  }
+  __syncwarp();
+  if (lane < f.k && bytes) tma_load_1d(sm + s * f.stage_bytes + f.soff[lane], (const void *)src, bytes, &bars[s]);
+}
+
+template <typename T, int R, int DV>
+__global__ void __launch_bounds__(256) bk_fast_kernel(const FastDesc *__restrict__ Fg, InPtrs in,
+                                                      T *__restrict__ out, uint8_t *__restrict__ arg,
+                                                      int64_t row_begin, int64_t t_begin,
+                                                      int64_t t_end) {
+  using S = SrF<T>;
+  using Acc = typename S::Acc;
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ FastHot f;
+  __shared__ uint64_t bars[2];
+  __shared__ int32_t delta[64];
+  __shared__ int64_t rowstart[2];
+  {
+    const int *src = (const int *)&Fg->hot;
+    int *dst = (int *)&f;
+    for (int i = threadIdx.x; i < (int)(sizeof(FastHot) / 4); i += blockDim.x) dst[i] = src[i];
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int k = f.k, Pmid = f.Pmid, PL = f.PL;
+  T *outs = (T *)(sm + f.off_out);
+  uint8_t *args = sm + f.off_arg;
+  int32_t *offtab = (int32_t *)(sm + f.off_tab);
+  int32_t *mrowoff = (int32_t *)(sm + f.off_mrow);
+  // per-CTA tables: slice offset of every thread group, per input
+  for (int idx = threadIdx.x; idx < (k + 1) * Pmid; idx += blockDim.x) {
+    int jj = idx / Pmid, q = idx - jj * Pmid;
+    int off = 0;
+    for (int e = f.nmid - 1; e >= 0; e--) {
+      int r = f.mrad[e], dg = q % r;
+      q /= r;
+      off += dg * (jj < k ? f.mstr[e][jj] : f.mrow[e]);
+    }
+    if (jj < k)
+      offtab[idx] = off;
+    else
+      mrowoff[idx - k * Pmid] = off;
+  }
+  __syncthreads();
+
+  int64_t t = t_begin + blockIdx.x;
+  if (t < t_end && threadIdx.x < 32) issue_tile(Fg, f, in, t, 0, sm, bars, delta, rowstart);
+  for (int it = 0; t < t_end; it++, t += gridDim.x) {
+    const int s = it & 1;
+    const int64_t tn = t + gridDim.x;
+    if (tn < t_end && threadIdx.x < 32) issue_tile(Fg, f, in, tn, s ^ 1, sm, bars, delta, rowstart);
+    mbar_wait(&bars[s], (uint32_t)((it >> 1) & 1));
+    const unsigned char *stage = sm + s * f.stage_bytes;
+    for (int q = threadIdx.x; q < Pmid; q += blockDim.x) {
+      Acc P0[DV], P1[R][DV], P2[R][DV], P3[R][R][DV];
+#pragma unroll
+      for (int v = 0; v < DV; v++) {
+        P0[v] = S::zero();
+#pragma unroll
+        for (int a = 0; a < R; a++) {
+          P1[a][v] = S::zero();
+          P2[a][v] = S::zero();
+#pragma unroll
+          for (int b = 0; b < R; b++) P3[a][b][v] = S::zero();
+        }
+      }
+      // class 0: neither group digit
+      for (int jj = f.cls_off[0]; jj < f.cls_off[1]; jj++) {
+        const T *p = (const T *)(stage + f.soff[jj]) + delta[s * 32 + jj] + offtab[jj * Pmid + q];
+#pragma unroll
+        for (int v = 0; v < DV; v++) P0[v] = S::add(P0[v], (Acc)p[v]);
+      }
+      // class 1: g1 only
+      for (int jj = f.cls_off[1]; jj < f.cls_off[2]; jj++) {
+        const T *p = (const T *)(stage + f.soff[jj]) + delta[s * 32 + jj] + offtab[jj * Pmid + q];
+        const int s1 = f.sg1[jj];
+#pragma unroll
+        for (int a = 0; a < R; a++)
+#pragma unroll
+          for (int v = 0; v < DV; v++) P1[a][v] = S::add(P1[a][v], (Acc)p[a * s1 + v]);
+      }
+      // class 2: g2 only
+      for (int jj = f.cls_off[2]; jj < f.cls_off[3]; jj++) {
+        const T *p = (const T *)(stage + f.soff[jj]) + delta[s * 32 + jj] + offtab[jj * Pmid + q];
+        const int s2 = f.sg2[jj];
+#pragma unroll
+        for (int b = 0; b < R; b++)
+#pragma unroll
+          for (int v = 0; v < DV; v++) P2[b][v] = S::add(P2[b][v], (Acc)p[b * s2 + v]);
+      }
+      // class 3: both
+      for (int jj = f.cls_off[3]; jj < f.cls_off[4]; jj++) {
+        const T *p = (const T *)(stage + f.soff[jj]) + delta[s * 32 + jj] + offtab[jj * Pmid + q];
+        const int s1 = f.sg1[jj], s2 = f.sg2[jj];
+#pragma unroll
+        for (int a = 0; a < R; a++)
+#pragma unroll
+          for (int b = 0; b < R; b++)
+#pragma unroll
+            for (int v = 0; v < DV; v++) P3[a][b][v] = S::add(P3[a][b][v], (Acc)p[a * s1 + b * s2 + v]);
+      }
+      const int row0 = mrowoff[q];
+#pragma unroll
+      for (int a = 0; a < R; a++)
+#pragma unroll
+        for (int b = 0; b < R; b++) {
+          Acc best = S::zero();
+          int bv = 0;
+#pragma unroll
+          for (int v = 0; v < DV; v++) {
+            Acc c = S::add(S::add3(P0[v], P1[a][v], P2[b][v]), P3[a][b][v]);
+            if (v == 0 || c < best) {
+              best = c;
+              bv = v;
+            }
+          }
+          const int l = row0 + a * f.rs1 + b * f.rs2;
+          outs[l] = S::out(best);
+          args[l] = (uint8_t)bv;
+        }
+    }
+    __syncthreads();
+    const int64_t o0 = rowstart[s] - row_begin;
+    for (int l = threadIdx.x; l < PL; l += blockDim.x) {
+      out[o0 + l] = outs[l];
+      if (arg) arg[o0 + l] = args[l];
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// dispatch table over (semiring, R, DV)
+
+template <typename T, int R, int DV>
+cudaError_t launch_one(const FastDesc *d, const InPtrs &in, void *out, uint8_t *arg, int64_t rb,
+                       int64_t t0, int64_t t1, int grid, int block, int smem, cudaStream_t s) {
+  auto kern = bk_fast_kernel<T, R, DV>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  kern<<<grid, block, smem, s>>>(d, in, (T *)out, arg, rb, t0, t1);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t dispatch(int R, int DV, const FastDesc *d, const InPtrs &in, void *out, uint8_t *arg,
+                     int64_t rb, int64_t t0, int64_t t1, int grid, int block, int smem,
+                     cudaStream_t s) {
+#define GBE_CASE(r, dv) \
+  if (R == r && DV == dv) return launch_one<T, r, dv>(d, in, out, arg, rb, t0, t1, grid, block, smem, s);
+  GBE_CASE(2, 2) GBE_CASE(2, 3) GBE_CASE(2, 4) GBE_CASE(2, 5)
+  GBE_CASE(3, 2) GBE_CASE(3, 3) GBE_CASE(3, 4) GBE_CASE(3, 5)
+  GBE_CASE(4, 2) GBE_CASE(4, 3)
+#undef GBE_CASE
+  return cudaErrorInvalidValue;
+}
+
+bool supported(int R, int DV) {
+  if (R == 2 || R == 3) return DV >= 2 && DV <= 5;
+  if (R == 4) return DV == 2 || DV == 3;
+  return false;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host: choose L (tile digits), the group digits, the tile order, the smem
+// layout; false when the bucket does not fit this kernel (-> bk_generic)
+
+bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int num_sms,
+               FastDesc &F, BkfLaunch &L) {
+  const int m = h.nsep, k = h.ninputs, DV = h.d;
+  const int es = h.semiring == GBE_MINSUM_F64 ? 8 : 4;
+  if (m < 2 || k < 1 || k > 32 || DV < 2 || DV > 5) return false;
+  if (row_end <= row_begin) return false;
+  const int64_t kPLMax = 4096;
+  const size_t kSmemMax = 100 * 1024;
+  // inputs' sizes (cells) to find the largest
+  auto has = [&](int j, int p) { return h.stride[j][p] != 0; };
+  std::vector<int64_t> cells(k, DV);
+  for (int j = 0; j < k; j++)
+    for (int p = 0; p < m; p++)
+      if (has(j, p)) cells[j] *= h.radix[p];
+  int big = 0;
+  for (int j = 1; j < k; j++)
+    if (cells[j] > cells[big]) big = j;
+
+  for (int nl = m; nl >= 2; nl--) {
+    int64_t PL = 1;
+    for (int p = m - nl; p < m; p++) PL *= h.radix[p];
+    if (PL > kPLMax) continue;
+    // group digits: best pair with equal supported radix
+    double bestc = 1e30;
+    int g1 = -1, g2 = -1;
+    for (int a = m - nl; a < m; a++)
+      for (int b = a + 1; b < m; b++) {
+        int R = h.radix[a];
+        if (h.radix[b] != R || !supported(R, DV)) continue;
+        if (es == 8 && R * R * DV > 27) continue;  // f64 register budget
+        double c = 0;
+        for (int j = 0; j < k; j++) c += 1.0 / ((has(j, a) ? 1 : R) * (has(j, b) ? 1 : R));
+        if (c < bestc - 1e-12 || (c < bestc + 1e-12 && b > g2)) {
+          bestc = c;
+          g1 = a;
+          g2 = b;
+        }
+      }
+    if (g1 < 0) continue;
+    const int R = h.radix[g1];
+    const int64_t Pmid = PL / (R * R);
+    if (row_begin % PL || row_end % PL) continue;
+    // classes
+    std::memset(&F, 0, sizeof(F));
+    FastHot &f = F.hot;
+    f.k = k;
+    f.es = es;
+    f.PL = (int32_t)PL;
+    f.Pmid = (int32_t)Pmid;
+    f.R = R;
+    f.DV = DV;
+    int jj = 0;
+    for (int c = 0; c < 4; c++) {
+      f.cls_off[c] = jj;
+      for (int j = 0; j < k; j++) {
+        int cls = (has(j, g1) ? 1 : 0) + (has(j, g2) ? 2 : 0);
+        if (cls != c) continue;
+        f.in_idx[jj] = j;
+        f.sg1[jj] = (int32_t)h.stride[j][g1];
+        f.sg2[jj] = (int32_t)h.stride[j][g2];
+        int64_t sl = DV;
+        for (int p = m - nl; p < m; p++)
+          if (has(j, p)) sl *= h.radix[p];
+        f.slen[jj] = (int32_t)sl;
+        F.shift[jj] = h.shift[j];
+        jj++;
+      }
+    }
+    f.cls_off[4] = jj;
+    // mid digits (L minus g1, g2), natural order
+    f.nmid = 0;
+    int64_t rowst = 1;
+    std::vector<int64_t> rowstride(m);
+    for (int p = m - 1; p >= 0; p--) {
+      rowstride[p] = rowst;
+      rowst *= h.radix[p];
+    }
+    for (int p = m - nl; p < m; p++) {
+      if (p == g1 || p == g2) continue;
+      int e = f.nmid++;
+      f.mrad[e] = h.radix[p];
+      f.mrow[e] = (int32_t)rowstride[p];
+      for (int q = 0; q < k; q++) f.mstr[e][q] = (int32_t)h.stride[f.in_idx[q]][p];
+    }
+    f.rs1 = (int32_t)rowstride[g1];
+    f.rs2 = (int32_t)rowstride[g2];
+    // H digits: natural order; for a full-range launch, digits absent from
+    // the largest input go last (fastest) so their re-reads hit L2
+    std::vector<int> hd;
+    for (int p = 0; p < m - nl; p++) hd.push_back(p);
+    const bool full = row_begin == 0 && row_end == h.rows;
+    if (full)
+      std::stable_sort(hd.begin(), hd.end(), [&](int a, int b) { return has(big, a) > has(big, b); });
+    f.nH = (int32_t)hd.size();
+    if (f.nH > 31) continue;
+    int64_t div = 1;
+    for (int e = f.nH - 1; e >= 0; e--) {
+      int p = hd[e];
+      F.hrad[e] = h.radix[p];
+      F.hdiv[e] = div;
+      div *= h.radix[p];
+      F.hrow[e] = rowstride[p];
+      for (int q = 0; q < k; q++) F.hstr[e][q] = h.stride[f.in_idx[q]][p];
+    }
+    if (!full) {  // natural order: tile index = row / PL
+      // (hd already natural)
+    }
+    // shared-memory layout
+    size_t off = 0;
+    for (int q = 0; q < k; q++) {
+      f.soff[q] = (int32_t)off;
+      off += ((size_t)f.slen[q] * es + 32 + 15) & ~size_t(15);
+    }
+    f.stage_bytes = (int32_t)off;
+    off = 2 * off;
+    f.off_out = (int32_t)off;
+    off += ((size_t)PL * es + 15) & ~size_t(15);
+    f.off_arg = (int32_t)off;
+    off += ((size_t)PL + 15) & ~size_t(15);
+    f.off_tab = (int32_t)off;
+    off += (size_t)k * Pmid * 4;
+    f.off_mrow = (int32_t)off;
+    off += (size_t)Pmid * 4;
+    off = (off + 127) & ~size_t(127);
+    if (off > kSmemMax) continue;
+    L.smem = (int)off;
+    L.block = Pmid >= 256 ? 256 : (int)((Pmid + 31) / 32 * 32);
+    L.t_begin = row_begin / PL;
+    L.t_end = row_end / PL;
+    int per_sm = (int)std::min<size_t>(std::max<size_t>(1, (200 * 1024) / (off + 2048)), 2048 / L.block);
+    per_sm = std::max(1, std::min(per_sm, 8));
+    int64_t tiles = L.t_end - L.t_begin;
+    L.grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms * per_sm));
+    L.R = R;
+    L.DV = DV;
+    L.es = es;
+    return true;
+  }
+  return false;
+}
+
+cudaError_t bkf_launch(const FastDesc *dev_f, const BkfLaunch &L, const InPtrs &in, void *out,
+                       uint8_t *arg, int64_t row_begin, cudaStream_t s) {
+  if (L.es == 8)
+    return dispatch<double>(L.R, L.DV, dev_f, in, out, arg, row_begin, L.t_begin, L.t_end, L.grid,
+                            L.block, L.smem, s);
+  return dispatch<int32_t>(L.R, L.DV, dev_f, in, out, arg, row_begin, L.t_begin, L.t_end, L.grid,
+                           L.block, L.smem, s);
+}
+
+}  // namespace gbe

@@ -1,0 +1,48 @@
+// bk_fast.h — descriptor and launcher of the tiled TMA bucket kernel.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace gbe {
+
+// Fields every CTA copies into shared memory (all int32).
+struct FastHot {
+  int32_t k, es, PL, Pmid, R, DV, nmid, nH;
+  int32_t cls_off[5];    // input class ranges: none / g1 / g2 / both
+  int32_t in_idx[32];    // class-ordered input -> original input
+  int32_t sg1[32], sg2[32];  // element strides of the group digits (0 if absent)
+  int32_t slen[32];      // slice length (elements) per tile
+  int32_t soff[32];      // byte offset of the slice inside a stage
+  int32_t stage_bytes;
+  int32_t rs1, rs2;      // in-tile row strides of g1, g2
+  int32_t mrad[12], mrow[12];  // middle digits (L minus group), most significant first
+  int32_t mstr[12][32];  // their element strides per input
+  int32_t off_out, off_arg, off_tab, off_mrow;
+  int32_t pad;
+};
+
+struct FastDesc {
+  FastHot hot;
+  int32_t hrad[32];      // high digits in tile-enumeration order
+  int32_t pad2;
+  int64_t hdiv[32];      // tile-index divisor of each high digit
+  int64_t hrow[32];      // output row stride of each high digit
+  int64_t hstr[32][32];  // element stride per high digit, per (class-ordered) input
+  int64_t shift[32];
+};
+
+struct BkfLaunch {
+  int R = 0, DV = 0, es = 4;
+  int grid = 1, block = 256, smem = 0;
+  int64_t t_begin = 0, t_end = 0;
+};
+
+bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int num_sms,
+               FastDesc &F, BkfLaunch &L);
+cudaError_t bkf_launch(const FastDesc *dev_f, const BkfLaunch &L, const InPtrs &in, void *out,
+                       uint8_t *arg, int64_t row_begin, cudaStream_t s);
+
+}  // namespace gbe

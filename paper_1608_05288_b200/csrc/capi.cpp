@@ -240,6 +240,13 @@ gbe_status gbe_bucket_kernel(const void *desc, const void *const *dev_inputs, vo
   });
 }
 
+int32_t gbe_bucket_kernel_variant(const void *desc, int64_t row_begin, int64_t row_end) {
+  if (!desc) return -1;
+  const gbe_bucket_desc *h = (const gbe_bucket_desc *)desc;
+  if (h->nsep < 0 || h->nsep > GBE_MAX_SEP || h->ninputs < 0 || h->ninputs > GBE_MAX_INPUTS) return -1;
+  return bucket_kernel_variant(h, row_begin, row_end);
+}
+
 gbe_status gbe_set_allocator(void *(*alloc_fn)(size_t, void *, void *),
                              void (*free_fn)(void *, void *), void *u) {
   return guard([&] {

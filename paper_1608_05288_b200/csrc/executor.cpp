@@ -16,6 +16,7 @@
 
 #include "common.h"
 #include "executor.h"
+#include "bk_fast.h"
 #include "kernels.h"
 
 namespace gbe {
@@ -75,6 +76,10 @@ struct DevPlan {
   int device = 0, num_sms = 148;
   std::vector<gbe_bucket_desc> h_desc;
   std::vector<BkLaunchInfo> launch;
+  std::vector<FastDesc> h_fast;
+  std::vector<BkfLaunch> fl;
+  std::vector<char> use_fast;
+  FastDesc *d_fast = nullptr;
   gbe_bucket_desc *d_desc = nullptr;
   int64_t *d_off = nullptr;
   int32_t *d_poff = nullptr, *d_prad = nullptr, *d_pstride = nullptr;
@@ -84,6 +89,7 @@ struct DevPlan {
   bool resident = false;
   ~DevPlan() {
     cudaFree(d_desc);
+    cudaFree(d_fast);
     cudaFree(d_off);
     cudaFree(d_poff);
     cudaFree(d_prad);
@@ -108,6 +114,9 @@ static DevPlan *dev_plan(gbe_plan *gp) {
   // descriptors with the per-rank input shifts (row-sharded messages kept local)
   D->h_desc.resize(P.tasks.size());
   D->launch.resize(P.tasks.size());
+  D->h_fast.resize(P.tasks.size());
+  D->fl.resize(P.tasks.size());
+  D->use_fast.assign(P.tasks.size(), 0);
   for (size_t ti = 0; ti < P.tasks.size(); ti++) {
     const Task &t = P.tasks[ti];
     gbe_bucket_desc h = t.desc;
@@ -121,7 +130,14 @@ static DevPlan *dev_plan(gbe_plan *gp) {
     }
     D->h_desc[ti] = h;
     D->launch[ti] = bk_plan_launch(h, t.shard.lo, t.shard.hi, P.ex.kernel, D->num_sms);
+    if (P.ex.kernel != 0 && bkf_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_fast[ti], D->fl[ti])) {
+      D->use_fast[ti] = 1;
+      D->launch[ti].variant = 1;
+    }
   }
+  CK(cudaMalloc(&D->d_fast, sizeof(FastDesc) * std::max<size_t>(P.tasks.size(), 1)));
+  if (!P.tasks.empty())
+    CK(cudaMemcpy(D->d_fast, D->h_fast.data(), sizeof(FastDesc) * P.tasks.size(), cudaMemcpyHostToDevice));
   size_t nt = std::max<size_t>(P.tasks.size(), 1);
   CK(cudaMalloc(&D->d_desc, sizeof(gbe_bucket_desc) * nt));
   if (!P.tasks.empty())
@@ -288,8 +304,11 @@ static void run_util(RunImpl &R) {
     InPtrs in{};
     for (int j = 0; j < t.desc.ninputs; j++) in.p[j] = R.member_ptr(t.members[j]);
     if (P.ex.timing) CK(cudaEventRecord(R.ev[2 * ti], s));
-    CK(bk_launch(D->h_desc[ti], D->d_desc + ti, in, R.out[ti], R.arg[ti], sh.lo, sh.hi,
-                 D->launch[ti], s));
+    if (D->use_fast[ti])
+      CK(bkf_launch(D->d_fast + ti, D->fl[ti], in, R.out[ti], R.arg[ti], sh.lo, s));
+    else
+      CK(bk_launch(D->h_desc[ti], D->d_desc + ti, in, R.out[ti], R.arg[ti], sh.lo, sh.hi,
+                   D->launch[ti], s));
     if (P.ex.timing) CK(cudaEventRecord(R.ev[2 * ti + 1], s));
     if (sh.on && sh.gather) {
       if (!g_ag) GBE_FAIL(GBE_E_COMM, "bucket x%d is row-sharded but no all-gather hook is set", t.var);
@@ -515,6 +534,14 @@ void solve(gbe_plan *gp, void *stream, bool mbe, gbe_value *opt, gbe_value *uppe
   delete R;
 }
 
+int bucket_kernel_variant(const gbe_bucket_desc *h, int64_t row_begin, int64_t row_end) {
+  FastDesc *F = new FastDesc();
+  BkfLaunch fl;
+  bool ok = bkf_build(*h, row_begin, row_end, 148, *F, fl);
+  delete F;
+  return ok ? 1 : 0;
+}
+
 // the bare hot primitive
 void bucket_kernel(const gbe_bucket_desc *h, const void *const *dev_inputs, void *dev_out,
                    uint8_t *dev_arg, int64_t row_begin, int64_t row_end, void *stream) {
@@ -540,8 +567,20 @@ void bucket_kernel(const gbe_bucket_desc *h, const void *const *dev_inputs, void
   CK(cudaMemcpyAsync(d_desc, h, sizeof(gbe_bucket_desc), cudaMemcpyHostToDevice, s));
   InPtrs in{};
   for (int j = 0; j < h->ninputs; j++) in.p[j] = dev_inputs[j];
-  BkLaunchInfo li = bk_plan_launch(*h, row_begin, row_end, -1, nsm);
-  CK(bk_launch(*h, d_desc, in, dev_out, dev_arg, row_begin, row_end, li, s));
+  FastDesc *F = new FastDesc();
+  BkfLaunch fl;
+  if (bkf_build(*h, row_begin, row_end, nsm, *F, fl)) {
+    FastDesc *d_f = (FastDesc *)dalloc(sizeof(FastDesc), s);
+    cudaError_t e = cudaMemcpyAsync(d_f, F, sizeof(FastDesc), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = bkf_launch(d_f, fl, in, dev_out, dev_arg, row_begin, s);
+    dfree(d_f, s);
+    delete F;
+    CK(e);
+  } else {
+    delete F;
+    BkLaunchInfo li = bk_plan_launch(*h, row_begin, row_end, -1, nsm);
+    CK(bk_launch(*h, d_desc, in, dev_out, dev_arg, row_begin, row_end, li, s));
+  }
   dfree(d_desc, s);
 }
 

@@ -30,7 +30,7 @@ EXPORTED = [
     "gbe_plan_create", "gbe_plan_info", "gbe_plan_destroy", "gbe_solve_be", "gbe_solve_mbe",
     "gbe_dpop_util", "gbe_dpop_value", "gbe_run_stats", "gbe_run_table", "gbe_run_destroy",
     "gbe_bucket_kernel", "gbe_set_allocator", "gbe_set_allgather", "gbe_last_error",
-    "gbe_version",
+    "gbe_version", "gbe_bucket_kernel_variant",
 ]
 
 
@@ -96,6 +96,8 @@ def lib():
         L.gbe_run_destroy.argtypes = [vp]
         L.gbe_run_destroy.restype = None
         L.gbe_bucket_kernel.argtypes = [vp, vp, vp, vp, i64, i64, vp]
+        L.gbe_bucket_kernel_variant.argtypes = [vp, i64, i64]
+        L.gbe_bucket_kernel_variant.restype = i32
         L.gbe_set_allocator.argtypes = [ALLOC_FN, FREE_FN, vp]
         L.gbe_set_allgather.argtypes = [AG_FN, vp]
         L.gbe_last_error.restype = ctypes.c_char_p
@@ -300,6 +302,11 @@ def bucket_kernel(desc: BucketDesc, inputs, out, arg, row_begin, row_end, stream
     arr = (ctypes.c_void_p * max(len(inputs), 1))(*[p(x) for x in inputs])
     _check(lib().gbe_bucket_kernel(ctypes.byref(desc), arr, p(out), p(arg), int(row_begin),
                                    int(row_end), _stream_ptr(stream)))
+
+
+def bucket_kernel_variant(desc: BucketDesc, row_begin, row_end):
+    """0 = generic kernel, 1 = tiled TMA kernel, -1 = invalid descriptor."""
+    return int(lib().gbe_bucket_kernel_variant(ctypes.byref(desc), int(row_begin), int(row_end)))
 
 
 _HOOKS = {}

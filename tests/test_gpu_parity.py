@@ -274,3 +274,88 @@ def test_mpe_bn_small_against_brute_force(torch_cuda):
         order, _ = P.order()
         opt, a = G.Plan(P, order).solve_be()
         assert math.isclose(math.exp(-opt), mpe_linear(inst), rel_tol=1e-9)
+
+
+# ---------------------------------------------------------------- tiled TMA kernel
+
+FAST_SHAPES = [(2, 2), (2, 3), (2, 4), (2, 5), (3, 2), (3, 3), (3, 4), (3, 5), (4, 2), (4, 3)]
+
+
+def uniform_bucket(rng, R, DV, m, k, f64):
+    dom = [R] * m + [DV]
+    members = []
+    for j in range(k):
+        p = rng.uniform(0.1, 0.95)
+        sub = [q for q in range(m) if rng.random() < p]
+        scope = sub + [m]
+        cells = int(np.prod([dom[v] for v in scope]))
+        if f64:
+            t = rng.uniform(0, 10, cells)
+            t[rng.random(cells) < 0.05] = np.inf
+        else:
+            t = rng.integers(0, 1000, cells).astype(np.int64)
+            t[rng.random(cells) < 0.05] = INF
+        members.append((scope, t))
+    return dom, list(range(m)), m, members
+
+
+@pytest.mark.parametrize("R,DV", FAST_SHAPES)
+@pytest.mark.parametrize("f64", [False, True])
+def test_fast_kernel_shapes(torch_cuda, R, DV, f64):
+    rng = np.random.default_rng(R * 100 + DV * 10 + int(f64))
+    m = {2: 13, 3: 9, 4: 7}[R]
+    for trial in range(3):
+        k = int(rng.integers(1, 12))
+        dom, sep, x, members = uniform_bucket(rng, R, DV, m, k, f64)
+        D, rows = desc_for(dom, sep, x, members, f64)
+        if f64 and R * R * DV > 27:
+            assert G.bucket_kernel_variant(D, 0, rows) == 0
+            continue
+        assert G.bucket_kernel_variant(D, 0, rows) == 1
+        exp, exp_arg = oracle.bucket_eval(dom, f64, x, members, sep)
+        got, got_arg = run_bucket(torch_cuda, dom, sep, x, members, f64, 0, rows)
+        if f64:
+            np.testing.assert_array_equal(np.isinf(got), np.isinf(exp))
+            fin = np.isfinite(exp)
+            assert np.allclose(got[fin], exp[fin], rtol=1e-9, atol=0)
+            # argmins may differ only on near-ties (different summation order)
+            assert np.mean(got_arg == exp_arg) > 0.999
+        else:
+            np.testing.assert_array_equal(got, exp)
+            np.testing.assert_array_equal(got_arg, exp_arg)
+
+
+def test_fast_kernel_partial_ranges(torch_cuda):
+    """Tile-aligned row ranges (the row-shard contract) on the tiled kernel."""
+    rng = np.random.default_rng(9)
+    dom, sep, x, members = uniform_bucket(rng, 3, 3, 10, 7, False)
+    D, rows = desc_for(dom, sep, x, members, False)
+    full, fa = run_bucket(torch_cuda, dom, sep, x, members, False, 0, rows)
+    blk = rows // 9
+    for a, b in [(0, 3 * blk), (3 * blk, 7 * blk), (7 * blk, rows)]:
+        assert G.bucket_kernel_variant(D, a, b) == 1
+        got, ga = run_bucket(torch_cuda, dom, sep, x, members, False, a, b)
+        np.testing.assert_array_equal(got, full[a:b])
+        np.testing.assert_array_equal(ga, fa[a:b])
+
+
+def test_fast_and_generic_kernels_agree_on_c4alt_buckets(torch_cuda):
+    """Whole DPOP on a BA n=120 DCOP: every table from the auto plan (tiled
+    kernel on large buckets) equals the generic-kernel plan bit for bit, and
+    the tiled kernel was actually used."""
+    inst = gen.scalefree(120, 3, 0.0, 3)
+    P = G.Problem.from_instance(inst)
+    order, w = P.order()
+    pa = G.Plan(P, order, retain="all", timing=True)
+    pg = G.Plan(P, order, retain="all", kernel=0)
+    ra, roota = pa.dpop_util()
+    rg, rootg = pg.dpop_util()
+    st = ra.stats()
+    assert any(t["variant"] == 1 for t in st["tasks"])
+    assert roota == rootg
+    for t, ti in enumerate(pa.info()["tables"]):
+        oa, aa = ra.table(t, ti["rows"])
+        og, ag = rg.table(t, ti["rows"])
+        np.testing.assert_array_equal(oa, og)
+        np.testing.assert_array_equal(aa, ag)
+    assert list(ra.value()) == list(rg.value())
