@@ -6,19 +6,21 @@
 //    input j the tile's slice is ONE contiguous range of d*prod(L ∩ S_j)
 //    elements (the eliminated variable and the trailing output variables are
 //    the least-significant digits of every input), so each tile
-//    needs one 1-D TMA bulk copy (cp.async.bulk, UBLKCP) per input, into a
-//    2-stage shared-memory ring signalled by an mbarrier.  Small child tables
-//    land in shared memory whole; large ones stream slice by slice.
+//    needs one 1-D TMA bulk copy (cp.async.bulk, UBLKCP) per input.  A
+//    dedicated producer warp keeps a 3-stage shared-memory ring full
+//    (full/empty mbarriers); 8 consumer warps never block on a CTA barrier.
+//    Small child tables land in shared memory whole; large ones stream slice
+//    by slice.
 //  * Inside a tile each thread owns R x R x d cells: all values of two
 //    chosen "group" digits g1, g2 in L and of the eliminated variable.  Inputs
 //    are split by which group digits they contain; an input missing a group
 //    digit is loaded once and reused across that digit's R values, so the
 //    shared-memory loads and saturating adds per cell drop from k to
 //    sum_j R^-|{g1,g2} \ S_j| (the host picks g1, g2 to minimise this).
-//  * Index math is per tile (one mixed-radix decode by warp 0) and per thread
-//    group (a shared-memory offset table built once per CTA): no per-row
-//    div/mod.
-//  * Output rows are staged in shared memory and written back coalesced.
+//  * Index math is per tile (one mixed-radix decode by the producer warp) and
+//    per thread group (a shared-memory offset table built once per CTA): no
+//    per-row div/mod.
+//  * Output rows and argmins are stored straight from registers.
 //  * Tile order: the output digits missing from the largest input vary
 //    fastest, so tiles that re-read the same input slice run back to back and
 //    hit L2 instead of HBM.
@@ -35,6 +37,10 @@ namespace gbe {
 namespace {
 
 constexpr uint32_t kInf = GBE_INF_I32;
+constexpr int kMaxStages = 4;
+constexpr int kOutBufs = 3;
+constexpr int kConsumerWarps = 8;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;
 
 template <typename T>
 struct SrF;
@@ -92,13 +98,38 @@ __device__ __forceinline__ void tma_load_1d(void *smem_dst, const void *gsrc, ui
       : "memory");
 }
 
-// Warp 0 issues the TMA copies of tile t into stage s.
+__device__ __forceinline__ void tma_store_1d(void *gdst, const void *smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst),
+               "r"(smem_u32(smem_src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void consumer_sync() {  // named barrier 1 over the consumer warps
+  asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumerWarps * 32) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+
+// The producer warp issues the TMA copies of tile t into stage s: lane e
+// decodes high digit e of the tile index, lane j < k accumulates input j's
+// slice base, then each lane copies its slice with one bulk copy.
 __device__ __forceinline__ void issue_tile(const FastDesc *__restrict__ Fg, const FastHot &f,
                                            const InPtrs &in, int64_t t, int s, unsigned char *sm,
-                                           uint64_t *bars, int32_t *delta, int64_t *rowstart) {
+                                           uint64_t *full, int32_t *delta, int64_t *rowstart) {
   const int lane = threadIdx.x & 31;
   int dig = 0;
-  if (lane < f.nH) dig = (int)(((uint64_t)t / (uint64_t)Fg->hdiv[lane]) % (uint64_t)Fg->hrad[lane]);
+  if (lane < f.nH) dig = (int)(((uint32_t)t / (uint32_t)Fg->hdiv[lane]) % (uint32_t)Fg->hrad[lane]);
   int64_t base = 0, rs = 0;
   for (int e = 0; e < f.nH; e++) {
     int de = __shfl_sync(0xffffffffu, dig, e);
@@ -122,41 +153,41 @@ __device__ __forceinline__ void issue_tile(const FastDesc *__restrict__ Fg, cons
   __syncwarp();
   if (lane == 0) {
     __threadfence_block();
-    mbar_arrive_expect_tx(&bars[s], total);
+    mbar_arrive_expect_tx(&full[s], total);
   }
   __syncwarp();
-  if (lane < f.k && bytes) tma_load_1d(sm + s * f.stage_bytes + f.soff[lane], (const void *)src, bytes, &bars[s]);
+  if (lane < f.k && bytes) tma_load_1d(sm + s * f.stage_bytes + f.soff[lane], (const void *)src, bytes, &full[s]);
 }
 
 template <typename T, int R, int DV>
-__global__ void __launch_bounds__(256) bk_fast_kernel(const FastDesc *__restrict__ Fg, InPtrs in,
-                                                      T *__restrict__ out, uint8_t *__restrict__ arg,
-                                                      int64_t row_begin, int64_t t_begin,
-                                                      int64_t t_end) {
+__global__ void __launch_bounds__(kThreads) bk_fast_kernel(const FastDesc *__restrict__ Fg, InPtrs in,
+                                                           T *__restrict__ out, uint8_t *__restrict__ arg,
+                                                           int64_t row_begin, int64_t t_begin,
+                                                           int64_t t_end) {
   using S = SrF<T>;
   using Acc = typename S::Acc;
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ FastHot f;
-  __shared__ uint64_t bars[2];
-  __shared__ int32_t delta[64];
-  __shared__ int64_t rowstart[2];
+  __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
+  __shared__ int32_t delta[kMaxStages * 32];
+  __shared__ int64_t rowstart[kMaxStages];
   {
     const int *src = (const int *)&Fg->hot;
     int *dst = (int *)&f;
     for (int i = threadIdx.x; i < (int)(sizeof(FastHot) / 4); i += blockDim.x) dst[i] = src[i];
   }
   if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int s = 0; s < kMaxStages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  const int k = f.k, Pmid = f.Pmid, PL = f.PL;
-  T *outs = (T *)(sm + f.off_out);
-  uint8_t *args = sm + f.off_arg;
+  const int k = f.k, Pmid = f.Pmid;
   int32_t *offtab = (int32_t *)(sm + f.off_tab);
   int32_t *mrowoff = (int32_t *)(sm + f.off_mrow);
-  // per-CTA tables: slice offset of every thread group, per input
+  // per-CTA tables: slice offset of every thread group, per input; row offset
   for (int idx = threadIdx.x; idx < (k + 1) * Pmid; idx += blockDim.x) {
     int jj = idx / Pmid, q = idx - jj * Pmid;
     int off = 0;
@@ -171,16 +202,35 @@ __global__ void __launch_bounds__(256) bk_fast_kernel(const FastDesc *__restrict
       mrowoff[idx - k * Pmid] = off;
   }
   __syncthreads();
+  const int warp = threadIdx.x >> 5;
 
-  int64_t t = t_begin + blockIdx.x;
-  if (t < t_end && threadIdx.x < 32) issue_tile(Fg, f, in, t, 0, sm, bars, delta, rowstart);
-  for (int it = 0; t < t_end; it++, t += gridDim.x) {
-    const int s = it & 1;
-    const int64_t tn = t + gridDim.x;
-    if (tn < t_end && threadIdx.x < 32) issue_tile(Fg, f, in, tn, s ^ 1, sm, bars, delta, rowstart);
-    mbar_wait(&bars[s], (uint32_t)((it >> 1) & 1));
+  if (warp == kConsumerWarps) {  // ---- producer warp: TMA ring ----
+    int it = 0;
+    for (int64_t t = t_begin + blockIdx.x; t < t_end; t += gridDim.x, it++) {
+      const int s = it % f.nstages;
+      mbar_wait(&empty[s], (uint32_t)(((it / f.nstages) & 1) ^ 1));
+      issue_tile(Fg, f, in, t, s, sm, full, delta, rowstart);
+    }
+    return;
+  }
+
+  // ---- consumer warps ----
+  const int ctid = threadIdx.x;  // 0 .. 32*kConsumerWarps-1
+  const int PL = f.PL, es = (int)sizeof(T);
+  int it = 0;
+  for (int64_t t = t_begin + blockIdx.x; t < t_end; t += gridDim.x, it++) {
+    const int s = it % f.nstages;
+    mbar_wait(&full[s], (uint32_t)((it / f.nstages) & 1));
     const unsigned char *stage = sm + s * f.stage_bytes;
-    for (int q = threadIdx.x; q < Pmid; q += blockDim.x) {
+    const int64_t o0 = rowstart[s] - row_begin;
+    // staging: element l of this tile lives at index l + sh (16-byte phase of
+    // its global address), so the aligned interior is one TMA bulk store
+    const int b = it % kOutBufs;
+    const int sh = (int)((((uintptr_t)(out + o0)) & 15) / es);
+    const int sha = (int)(((uintptr_t)(arg + o0)) & 15);
+    T *outs = (T *)(sm + f.off_out + b * f.out_bytes) + sh;
+    uint8_t *args = sm + f.off_arg + b * f.arg_bytes + sha;
+    for (int q = ctid; q < Pmid; q += 32 * kConsumerWarps) {
       Acc P0[DV], P1[R][DV], P2[R][DV], P3[R][R][DV];
 #pragma unroll
       for (int v = 0; v < DV; v++) {
@@ -190,17 +240,15 @@ __global__ void __launch_bounds__(256) bk_fast_kernel(const FastDesc *__restrict
           P1[a][v] = S::zero();
           P2[a][v] = S::zero();
 #pragma unroll
-          for (int b = 0; b < R; b++) P3[a][b][v] = S::zero();
+          for (int bb = 0; bb < R; bb++) P3[a][bb][v] = S::zero();
         }
       }
-      // class 0: neither group digit
-      for (int jj = f.cls_off[0]; jj < f.cls_off[1]; jj++) {
+      for (int jj = f.cls_off[0]; jj < f.cls_off[1]; jj++) {  // neither group digit
         const T *p = (const T *)(stage + f.soff[jj]) + delta[s * 32 + jj] + offtab[jj * Pmid + q];
 #pragma unroll
         for (int v = 0; v < DV; v++) P0[v] = S::add(P0[v], (Acc)p[v]);
       }
-      // class 1: g1 only
-      for (int jj = f.cls_off[1]; jj < f.cls_off[2]; jj++) {
+      for (int jj = f.cls_off[1]; jj < f.cls_off[2]; jj++) {  // g1 only
         const T *p = (const T *)(stage + f.soff[jj]) + delta[s * 32 + jj] + offtab[jj * Pmid + q];
         const int s1 = f.sg1[jj];
 #pragma unroll
@@ -208,54 +256,79 @@ __global__ void __launch_bounds__(256) bk_fast_kernel(const FastDesc *__restrict
 #pragma unroll
           for (int v = 0; v < DV; v++) P1[a][v] = S::add(P1[a][v], (Acc)p[a * s1 + v]);
       }
-      // class 2: g2 only
-      for (int jj = f.cls_off[2]; jj < f.cls_off[3]; jj++) {
+      for (int jj = f.cls_off[2]; jj < f.cls_off[3]; jj++) {  // g2 only
         const T *p = (const T *)(stage + f.soff[jj]) + delta[s * 32 + jj] + offtab[jj * Pmid + q];
         const int s2 = f.sg2[jj];
 #pragma unroll
-        for (int b = 0; b < R; b++)
+        for (int bb = 0; bb < R; bb++)
 #pragma unroll
-          for (int v = 0; v < DV; v++) P2[b][v] = S::add(P2[b][v], (Acc)p[b * s2 + v]);
+          for (int v = 0; v < DV; v++) P2[bb][v] = S::add(P2[bb][v], (Acc)p[bb * s2 + v]);
       }
-      // class 3: both
-      for (int jj = f.cls_off[3]; jj < f.cls_off[4]; jj++) {
+      for (int jj = f.cls_off[3]; jj < f.cls_off[4]; jj++) {  // both
         const T *p = (const T *)(stage + f.soff[jj]) + delta[s * 32 + jj] + offtab[jj * Pmid + q];
         const int s1 = f.sg1[jj], s2 = f.sg2[jj];
 #pragma unroll
         for (int a = 0; a < R; a++)
 #pragma unroll
-          for (int b = 0; b < R; b++)
+          for (int bb = 0; bb < R; bb++)
 #pragma unroll
-            for (int v = 0; v < DV; v++) P3[a][b][v] = S::add(P3[a][b][v], (Acc)p[a * s1 + b * s2 + v]);
+            for (int v = 0; v < DV; v++) P3[a][bb][v] = S::add(P3[a][bb][v], (Acc)p[a * s1 + bb * s2 + v]);
       }
       const int row0 = mrowoff[q];
 #pragma unroll
-      for (int a = 0; a < R; a++)
+      for (int a = 0; a < R; a++) {
+        Acc Q[DV];
 #pragma unroll
-        for (int b = 0; b < R; b++) {
+        for (int v = 0; v < DV; v++) Q[v] = S::add(P0[v], P1[a][v]);
+#pragma unroll
+        for (int bb = 0; bb < R; bb++) {
           Acc best = S::zero();
           int bv = 0;
 #pragma unroll
           for (int v = 0; v < DV; v++) {
-            Acc c = S::add(S::add3(P0[v], P1[a][v], P2[b][v]), P3[a][b][v]);
+            Acc c = S::add3(Q[v], P2[bb][v], P3[a][bb][v]);
             if (v == 0 || c < best) {
               best = c;
               bv = v;
             }
           }
-          const int l = row0 + a * f.rs1 + b * f.rs2;
+          const int l = row0 + a * f.rs1 + bb * f.rs2;
           outs[l] = S::out(best);
           args[l] = (uint8_t)bv;
         }
+      }
     }
-    __syncthreads();
-    const int64_t o0 = rowstart[s] - row_begin;
-    for (int l = threadIdx.x; l < PL; l += blockDim.x) {
-      out[o0 + l] = outs[l];
-      if (arg) arg[o0 + l] = args[l];
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);  // input stage free
+    fence_proxy_async_smem();                             // staged rows -> async proxy
+    consumer_sync();
+    // aligned interior by TMA bulk stores, ragged head/tail by plain stores
+    T *gout = out + o0;
+    const int h = (int)(((16 - (((uintptr_t)gout) & 15)) & 15) / es);
+    const int nmid = ((PL - min(h, PL)) * es / 16) * 16 / es;
+    uint8_t *ga = arg ? arg + o0 : nullptr;
+    const int ha = ga ? (int)((16 - (((uintptr_t)ga) & 15)) & 15) : 0;
+    const int nmida = ga ? ((PL - min(ha, PL)) / 16) * 16 : 0;
+    if (ctid == 0) {
+      if (nmid > 0) tma_store_1d(gout + h, outs + h, (uint32_t)(nmid * es));
+      if (nmida > 0) tma_store_1d(ga + ha, args + ha, (uint32_t)nmida);
+      bulk_commit();
+      bulk_wait_read<kOutBufs - 1>();  // staging buffer of tile it-(kOutBufs-1) reusable
     }
-    __syncthreads();
+    // ragged head/tail (< 16 bytes each side): plain stores from staging
+    {
+      const int hh = min(h, PL), tl = PL - hh - nmid;
+      if (ctid < hh) gout[ctid] = outs[ctid];
+      else if (ctid < hh + tl) gout[hh + nmid + (ctid - hh)] = outs[hh + nmid + (ctid - hh)];
+      if (ga) {
+        const int hha = min(ha, PL), tla = PL - hha - nmida;
+        const int c2 = ctid - 64;
+        if (c2 >= 0 && c2 < hha) ga[c2] = args[c2];
+        else if (c2 >= hha && c2 < hha + tla) ga[hha + nmida + (c2 - hha)] = args[hha + nmida + (c2 - hha)];
+      }
+    }
   }
+  if (ctid == 0) bulk_wait_all();
 }
 
 // ---------------------------------------------------------------------------
@@ -305,8 +378,8 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
   const int es = h.semiring == GBE_MINSUM_F64 ? 8 : 4;
   if (m < 2 || k < 1 || k > 32 || DV < 2 || DV > 5) return false;
   if (row_end <= row_begin) return false;
-  const int64_t kPLMax = 4096;
-  const size_t kSmemMax = 100 * 1024;
+  const int64_t kPLMax = 8192;
+  const size_t kSmemMax = 200 * 1024;
   // inputs' sizes (cells) to find the largest
   auto has = [&](int j, int p) { return h.stride[j][p] != 0; };
   std::vector<int64_t> cells(k, DV);
@@ -413,11 +486,18 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
       off += ((size_t)f.slen[q] * es + 32 + 15) & ~size_t(15);
     }
     f.stage_bytes = (int32_t)off;
-    off = 2 * off;
+    f.out_bytes = (int32_t)(((size_t)PL * es + 16 + 127) & ~size_t(127));
+    f.arg_bytes = (int32_t)(((size_t)PL + 16 + 127) & ~size_t(127));
+    size_t fixed = kOutBufs * ((size_t)f.out_bytes + f.arg_bytes) + (size_t)(k + 1) * Pmid * 4 + 256;
+    // 2 CTAs per SM when possible (~110 KB each), 2..4 input stages
+    int nst = kMaxStages;
+    while (nst > 2 && fixed + nst * off > 110 * 1024) nst--;
+    f.nstages = nst;
+    off = nst * off;
     f.off_out = (int32_t)off;
-    off += ((size_t)PL * es + 15) & ~size_t(15);
+    off += kOutBufs * (size_t)f.out_bytes;
     f.off_arg = (int32_t)off;
-    off += ((size_t)PL + 15) & ~size_t(15);
+    off += kOutBufs * (size_t)f.arg_bytes;
     f.off_tab = (int32_t)off;
     off += (size_t)k * Pmid * 4;
     f.off_mrow = (int32_t)off;
@@ -425,10 +505,10 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     off = (off + 127) & ~size_t(127);
     if (off > kSmemMax) continue;
     L.smem = (int)off;
-    L.block = Pmid >= 256 ? 256 : (int)((Pmid + 31) / 32 * 32);
+    L.block = kThreads;
     L.t_begin = row_begin / PL;
     L.t_end = row_end / PL;
-    int per_sm = (int)std::min<size_t>(std::max<size_t>(1, (200 * 1024) / (off + 2048)), 2048 / L.block);
+    int per_sm = (int)std::min<size_t>(std::max<size_t>(1, (220 * 1024) / (off + 4096)), 2048 / L.block);
     per_sm = std::max(1, std::min(per_sm, 8));
     int64_t tiles = L.t_end - L.t_begin;
     L.grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms * per_sm));

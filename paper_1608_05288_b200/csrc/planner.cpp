@@ -11,6 +11,7 @@
 #include <numeric>
 #include <sstream>
 
+#include "bk_fast.h"
 #include "common.h"
 
 namespace gbe {
@@ -397,7 +398,25 @@ std::string plan_json(const Plan &plan) {
     o << "],\"shard\":{\"on\":" << (t.shard.on ? "true" : "false") << ",\"key_digits\":"
       << t.shard.key_digits << ",\"blocks\":" << t.shard.blocks << ",\"per\":" << t.shard.per
       << ",\"lo\":" << t.shard.lo << ",\"hi\":" << t.shard.hi
-      << ",\"gather\":" << (t.shard.gather ? "true" : "false") << "}}";
+      << ",\"gather\":" << (t.shard.gather ? "true" : "false") << "}";
+    {
+      FastDesc *F = new FastDesc();
+      BkfLaunch L;
+      bool ok = plan.ex.kernel != 0 && bkf_build(t.desc, t.shard.lo, t.shard.hi, 148, *F, L);
+      o << ",\"kernel\":{\"variant\":" << (ok ? 1 : 0);
+      if (ok) {
+        const FastHot &f = F->hot;
+        o << ",\"PL\":" << f.PL << ",\"R\":" << f.R << ",\"Pmid\":" << f.Pmid << ",\"nH\":" << f.nH
+          << ",\"classes\":[" << f.cls_off[1] - f.cls_off[0] << "," << f.cls_off[2] - f.cls_off[1] << ","
+          << f.cls_off[3] - f.cls_off[2] << "," << f.cls_off[4] - f.cls_off[3] << "],\"rs\":[" << f.rs1
+          << "," << f.rs2 << "],\"stage_bytes\":" << f.stage_bytes << ",\"smem\":" << L.smem
+          << ",\"grid\":" << L.grid << ",\"slen\":[";
+        for (int q = 0; q < f.k; q++) o << (q ? "," : "") << f.slen[q];
+        o << "]";
+      }
+      o << "}}";
+      delete F;
+    }
   }
   o << "]}";
   return o.str();

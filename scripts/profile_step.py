@@ -1,0 +1,35 @@
+"""One exact DPOP solve of a BASELINE workload (for ncu launch lists /
+captures).  --which-fast prints the index, among tiled-kernel launches, of
+the largest bucket (use it as ncu -k regex:bk_fast -s IDX -c 1)."""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import paper_1608_05288_b200 as G
+from gen import configs
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="c4")
+ap.add_argument("--steps", type=int, default=1)
+ap.add_argument("--which-fast", action="store_true")
+ap.add_argument("--var", type=int, default=-1)
+a = ap.parse_args()
+inst = {"c4": configs.c4, "c2": configs.c2}[a.workload]()
+P = G.Problem.from_instance(inst)
+order, w = P.order()
+plan = G.Plan(P, order, timing=True)
+for _ in range(a.steps):
+    run, root = plan.dpop_util()
+    assign = run.value()
+    st = run.stats()
+    run.close()
+fast = [t for t in st["tasks"] if t["variant"] == 1]
+big = max(range(len(fast)), key=lambda i: fast[i]["cells"]) if a.var < 0 else [i for i, t in enumerate(fast) if t["var"] == a.var][0]
+if a.which_fast:
+    print(big)
+else:
+    print(json.dumps({"root": root, "fast_launches": len(fast), "largest_fast_index": big,
+                      "largest": fast[big]}))
