@@ -87,7 +87,21 @@ struct DevPlan {
   size_t raw_bytes = 0;
   void *d_resident = nullptr;  // resident raw tables (resident_inputs)
   bool resident = false;
+  // static memory plans (exact / MBE mode): every large buffer of a run at a
+  // fixed offset of one arena allocation, reused by consecutive runs
+  struct Arena {
+    bool planned = false;
+    size_t bytes = 0, off_raw = 0, off_sorted = 0;
+    std::vector<size_t> off_out, off_full, off_arg;
+    void *mem = nullptr;
+    bool busy = false, hook = false;
+  } arena[2];
   ~DevPlan() {
+    for (auto &a : arena)
+      if (a.mem) {
+        if (a.hook && g_free) g_free(a.mem, g_alloc_u);
+        else cudaFree(a.mem);
+      }
     cudaFree(d_desc);
     cudaFree(d_fast);
     cudaFree(d_off);
@@ -98,6 +112,85 @@ struct DevPlan {
     if (h_raw) cudaFreeHost(h_raw);
   }
 };
+
+// First-fit offsets for the run's buffers in the exact order run_util
+// allocates and frees them (DESIGN.md §5 "memory plan").
+namespace {
+struct FreeList {
+  std::vector<std::pair<size_t, size_t>> iv{{0, SIZE_MAX}};  // [start, end)
+  size_t top = 0;
+  size_t alloc(size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    if (bytes == 0) bytes = 256;
+    for (size_t i = 0; i < iv.size(); i++)
+      if (iv[i].second - iv[i].first >= bytes) {
+        size_t o = iv[i].first;
+        iv[i].first += bytes;
+        if (iv[i].first == iv[i].second) iv.erase(iv.begin() + i);
+        top = std::max(top, o + bytes);
+        return o;
+      }
+    return SIZE_MAX;
+  }
+  void release(size_t o, size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    if (bytes == 0) bytes = 256;
+    auto it = std::lower_bound(iv.begin(), iv.end(), std::make_pair(o, size_t(0)));
+    it = iv.insert(it, {o, o + bytes});
+    size_t i = it - iv.begin();
+    if (i + 1 < iv.size() && iv[i].second == iv[i + 1].first) {
+      iv[i].second = iv[i + 1].second;
+      iv.erase(iv.begin() + i + 1);
+    }
+    if (i > 0 && iv[i - 1].second == iv[i].first) {
+      iv[i - 1].second = iv[i].second;
+      iv.erase(iv.begin() + i);
+    }
+  }
+};
+}  // namespace
+
+static void plan_arena(const Plan &P, DevPlan *D, bool mbe_mode) {
+  const Problem &p = *P.prob;
+  const size_t el = p.elem();
+  const int W = P.ex.world_size;
+  const size_t nt = P.tasks.size();
+  FreeList fl;
+  DevPlan::Arena &A = D->arena[mbe_mode ? 1 : 0];
+  A.off_out.assign(nt, SIZE_MAX);
+  A.off_full.assign(nt, SIZE_MAX);
+  A.off_arg.assign(nt, SIZE_MAX);
+  size_t raw = D->raw_bytes;
+  A.off_raw = fl.alloc(raw);
+  A.off_sorted = fl.alloc(raw);
+  fl.release(A.off_raw, raw);  // raw tables are dead after the relayout
+  const bool want_arg = !mbe_mode || P.ex.retain >= 2;
+  std::vector<size_t> out_b(nt, 0), full_b(nt, 0);
+  for (size_t ti = 0; ti < nt; ti++) {
+    const Task &t = P.tasks[ti];
+    const Shard &sh = t.shard;
+    int64_t local = sh.on ? sh.hi - sh.lo : t.rows;
+    int64_t cap = sh.on ? sh.per * sh.block_rows : t.rows;
+    out_b[ti] = el * (size_t)cap;
+    A.off_out[ti] = fl.alloc(out_b[ti]);
+    if (want_arg) A.off_arg[ti] = fl.alloc((size_t)std::max<int64_t>(local, 1));
+    if (sh.on && sh.gather) {
+      full_b[ti] = out_b[ti] * W;
+      A.off_full[ti] = fl.alloc(full_b[ti]);
+      fl.release(A.off_out[ti], out_b[ti]);
+      out_b[ti] = 0;
+    }
+    if (!mbe_mode && P.ex.retain < 2)
+      for (auto &m : t.members)
+        if (m.kind == 1) {
+          if (out_b[m.index]) fl.release(A.off_out[m.index], out_b[m.index]);
+          if (full_b[m.index]) fl.release(A.off_full[m.index], full_b[m.index]);
+          out_b[m.index] = full_b[m.index] = 0;
+        }
+  }
+  A.bytes = std::max<size_t>(fl.top, 256);
+  A.planned = true;
+}
 
 static DevPlan *dev_plan(gbe_plan *gp) {
   if (gp->dev) return (DevPlan *)gp->dev;
@@ -187,7 +280,9 @@ struct RunImpl {
   cudaStream_t stream = nullptr;
   bool mbe = false;
   void *d_raw = nullptr, *d_sorted = nullptr;
-  bool own_raw = true;
+  char *base = nullptr;         // arena of this run
+  DevPlan::Arena *A = nullptr;  // its layout
+  bool arena_own = false;       // base allocated for this run (cached arena busy)
   std::vector<void *> out, full;
   std::vector<uint8_t *> arg;
   std::vector<cudaEvent_t> ev;
@@ -200,14 +295,15 @@ struct RunImpl {
   void release() {
     if (!D) return;
     cudaSetDevice(D->device);
-    for (auto p : out) dfree(p, stream);
-    for (auto p : full) dfree(p, stream);
-    for (auto p : arg) dfree(p, stream);
+    cudaStreamSynchronize(stream);  // the arena may be handed to the next run
     out.clear();
     full.clear();
     arg.clear();
-    if (own_raw) dfree(d_raw, stream);
-    dfree(d_sorted, stream);
+    if (base) {
+      if (arena_own) dfree(base, stream);
+      else A->busy = false;
+      base = nullptr;
+    }
     dfree(d_opt, stream);
     dfree(d_assign, stream);
     dfree(d_gbuf, stream);
@@ -271,6 +367,28 @@ static void run_util(RunImpl &R) {
   R.out.assign(nt, nullptr);
   R.full.assign(nt, nullptr);
   R.arg.assign(nt, nullptr);
+  {
+    DevPlan::Arena &A = D->arena[R.mbe ? 1 : 0];
+    if (!A.planned) plan_arena(P, D, R.mbe);
+    R.A = &A;
+    if (!A.busy) {
+      if (!A.mem) {
+        A.hook = g_alloc != nullptr;
+        A.mem = A.hook ? g_alloc(A.bytes, (void *)s, g_alloc_u) : nullptr;
+        if (!A.hook) {
+          cudaError_t e = cudaMalloc(&A.mem, A.bytes);
+          if (e != cudaSuccess)
+            GBE_FAIL(GBE_E_BUDGET, "device arena of %.3g bytes: %s", (double)A.bytes, cudaGetErrorString(e));
+        }
+        if (!A.mem) GBE_FAIL(GBE_E_BUDGET, "device arena of %.3g bytes", (double)A.bytes);
+      }
+      A.busy = true;
+      R.base = (char *)A.mem;
+    } else {
+      R.base = (char *)dalloc(A.bytes, s);
+      R.arena_own = true;
+    }
+  }
   if (P.ex.timing) {
     R.ev.resize(2 * nt);
     for (auto &e : R.ev) CK(cudaEventCreate(&e));
@@ -285,12 +403,11 @@ static void run_util(RunImpl &R) {
       D->resident = true;
     }
     R.d_raw = D->d_resident;
-    R.own_raw = false;
   } else {
-    R.d_raw = dalloc(D->raw_bytes, s);
+    R.d_raw = R.base + R.A->off_raw;
     CK(cudaMemcpyAsync(R.d_raw, D->h_raw, D->raw_bytes, cudaMemcpyHostToDevice, s));
   }
-  R.d_sorted = dalloc(D->raw_bytes, s);
+  R.d_sorted = R.base + R.A->off_sorted;
   CK(relayout_launch(R.d_raw, R.d_sorted, (int)el, p.nf, D->d_off, D->d_poff, D->d_prad,
                      D->d_pstride, s));
   const bool want_arg = !R.mbe || P.ex.retain >= 2;
@@ -299,8 +416,10 @@ static void run_util(RunImpl &R) {
     const Shard &sh = t.shard;
     int64_t local = sh.on ? sh.hi - sh.lo : t.rows;
     int64_t cap = sh.on ? sh.per * sh.block_rows : t.rows;
-    R.out[ti] = dalloc(el * cap, s);
-    if (want_arg) R.arg[ti] = (uint8_t *)dalloc(std::max<int64_t>(local, 1), s);
+    (void)local;
+    (void)cap;
+    R.out[ti] = R.base + R.A->off_out[ti];
+    if (want_arg) R.arg[ti] = (uint8_t *)(R.base + R.A->off_arg[ti]);
     InPtrs in{};
     for (int j = 0; j < t.desc.ninputs; j++) in.p[j] = R.member_ptr(t.members[j]);
     if (P.ex.timing) CK(cudaEventRecord(R.ev[2 * ti], s));
@@ -313,20 +432,15 @@ static void run_util(RunImpl &R) {
     if (sh.on && sh.gather) {
       if (!g_ag) GBE_FAIL(GBE_E_COMM, "bucket x%d is row-sharded but no all-gather hook is set", t.var);
       size_t bytes = el * (size_t)cap;
-      R.full[ti] = dalloc(bytes * W, s);
+      R.full[ti] = R.base + R.A->off_full[ti];
       if (g_ag(R.out[ti], R.full[ti], bytes, (void *)s, g_ag_u) != 0)
         GBE_FAIL(GBE_E_COMM, "all-gather of the message of x%d failed", t.var);
-      dfree(R.out[ti], s);
       R.out[ti] = nullptr;
     }
     // consumed messages are dead (BE/DPOP; MBE keeps them for its value phase, A7)
     if (!R.mbe && P.ex.retain < 2)
       for (auto &m : t.members)
-        if (m.kind == 1) {
-          dfree(R.out[m.index], s);
-          dfree(R.full[m.index], s);
-          R.out[m.index] = R.full[m.index] = nullptr;
-        }
+        if (m.kind == 1) R.out[m.index] = R.full[m.index] = nullptr;
   }
   // optimum / lower bound = sum of the constants
   std::vector<const void *> cptrs;
