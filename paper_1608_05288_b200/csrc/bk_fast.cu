@@ -39,6 +39,7 @@ namespace {
 constexpr uint32_t kInf = GBE_INF_I32;
 constexpr int kMaxStages = 4;
 constexpr int kOutBufs = 3;
+constexpr int kPrefetch = 0;  // tiles ahead (per CTA) prefetched into L2 (0 = off: measured slower)
 constexpr int kConsumerWarps = 8;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 
@@ -98,6 +99,9 @@ __device__ __forceinline__ void tma_load_1d(void *smem_dst, const void *gsrc, ui
       : "memory");
 }
 
+__device__ __forceinline__ void prefetch_l2(const void *gsrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(gsrc), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void tma_store_1d(void *gdst, const void *smem_src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst),
                "r"(smem_u32(smem_src)), "r"(bytes)
@@ -121,12 +125,15 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 }
 
 
-// The producer warp issues the TMA copies of tile t into stage s: lane e
-// decodes high digit e of the tile index, lane j < k accumulates input j's
-// slice base, then each lane copies its slice with one bulk copy.
-__device__ __forceinline__ void issue_tile(const FastDesc *__restrict__ Fg, const FastHot &f,
-                                           const InPtrs &in, int64_t t, int s, unsigned char *sm,
-                                           uint64_t *full, int32_t *delta, int64_t *rowstart) {
+// Slice of input `lane` (< k) for tile t: 16-byte aligned source range and the
+// byte offset of the slice start inside it.  Lane e also decodes digit e of t.
+struct SliceRange {
+  uintptr_t a16;
+  uint32_t bytes, skew;
+  int64_t rowstart;  // lane 0 only
+};
+__device__ __forceinline__ SliceRange tile_slice(const FastDesc *__restrict__ Fg, const FastHot &f,
+                                                 const InPtrs &in, int64_t t) {
   const int lane = threadIdx.x & 31;
   int dig = 0;
   if (lane < f.nH) dig = (int)(((uint32_t)t / (uint32_t)Fg->hdiv[lane]) % (uint32_t)Fg->hrad[lane]);
@@ -136,27 +143,90 @@ __device__ __forceinline__ void issue_tile(const FastDesc *__restrict__ Fg, cons
     if (lane < f.k) base += (int64_t)de * Fg->hstr[e][lane];
     if (lane == 0) rs += (int64_t)de * Fg->hrow[e];
   }
-  uint32_t bytes = 0;
-  uintptr_t src = 0;
+  SliceRange r{0, 0, 0, rs};
   if (lane < f.k) {
     base -= Fg->shift[lane];
     const char *p = (const char *)in.p[f.in_idx[lane]] + base * f.es;
     uintptr_t a16 = (uintptr_t)p & ~(uintptr_t)15;
     uintptr_t e16 = ((uintptr_t)p + (uintptr_t)f.slen[lane] * f.es + 15) & ~(uintptr_t)15;
-    bytes = (uint32_t)(e16 - a16);
-    src = a16;
-    delta[s * 32 + lane] = (int32_t)(((uintptr_t)p - a16) / f.es);
+    r.a16 = a16;
+    r.bytes = (uint32_t)(e16 - a16);
+    r.skew = (uint32_t)((uintptr_t)p - a16);
   }
-  uint32_t total = bytes;
+  return r;
+}
+
+// The producer warp issues the TMA copies of tile t into stage s (one 1-D
+// bulk copy per input) and publishes the slice bases for the consumers.
+__device__ __forceinline__ void issue_tile(const FastDesc *__restrict__ Fg, const FastHot &f,
+                                           const InPtrs &in, int64_t t, int s, unsigned char *sm,
+                                           uint64_t *full, int32_t *sbase, int64_t *rowstart) {
+  const int lane = threadIdx.x & 31;
+  SliceRange r = tile_slice(Fg, f, in, t);
+  if (lane < f.k) sbase[s * 32 + lane] = s * f.stage_bytes + f.soff[lane] + (int32_t)r.skew;
+  uint32_t total = r.bytes;
   for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
-  if (lane == 0) rowstart[s] = rs;
+  if (lane == 0) rowstart[s] = r.rowstart;
   __syncwarp();
   if (lane == 0) {
     __threadfence_block();
     mbar_arrive_expect_tx(&full[s], total);
   }
   __syncwarp();
-  if (lane < f.k && bytes) tma_load_1d(sm + s * f.stage_bytes + f.soff[lane], (const void *)src, bytes, &full[s]);
+  if (lane < f.k && r.bytes) tma_load_1d(sm + s * f.stage_bytes + f.soff[lane], (const void *)r.a16, r.bytes, &full[s]);
+}
+
+// L2 prefetch of the large slices of a future tile: the DRAM latency is paid
+// off the critical path, the TMA load of that tile then hits L2.
+__device__ __forceinline__ void prefetch_tile(const FastDesc *__restrict__ Fg, const FastHot &f,
+                                              const InPtrs &in, int64_t t) {
+  SliceRange r = tile_slice(Fg, f, in, t);
+  const int lane = threadIdx.x & 31;
+  if (lane < f.k && r.bytes >= 2048) prefetch_l2((const void *)r.a16, r.bytes);
+}
+
+// cell (a, b, v) = P0[v] (+ P1[a][v]) (+ P2[b][v]) (+ P3[a][b][v]) with the
+// saturating adds of A9; min over v, first minimiser (A8); staged in smem.
+template <typename T, int R, int DV, bool H1, bool H2, bool H3>
+__device__ __forceinline__ void combine(const typename SrF<T>::Acc (&P0)[DV],
+                                        const typename SrF<T>::Acc (&P1)[R][DV],
+                                        const typename SrF<T>::Acc (&P2)[R][DV],
+                                        const typename SrF<T>::Acc (&P3)[R][R][DV], T *outs,
+                                        uint8_t *args, int row0, int rs1, int rs2) {
+  using S = SrF<T>;
+  using Acc = typename S::Acc;
+#pragma unroll
+  for (int a = 0; a < R; a++) {
+    Acc Q[DV];
+#pragma unroll
+    for (int v = 0; v < DV; v++) Q[v] = H1 ? S::add(P0[v], P1[a][v]) : P0[v];
+#pragma unroll
+    for (int b = 0; b < R; b++) {
+      Acc c[DV];
+#pragma unroll
+      for (int v = 0; v < DV; v++) {
+        if (H2 && H3)
+          c[v] = S::add3(Q[v], P2[b][v], P3[a][b][v]);
+        else if (H2)
+          c[v] = S::add(Q[v], P2[b][v]);
+        else if (H3)
+          c[v] = S::add(Q[v], P3[a][b][v]);
+        else
+          c[v] = Q[v];
+      }
+      Acc best = c[0];
+      int bv = 0;
+#pragma unroll
+      for (int v = 1; v < DV; v++)
+        if (c[v] < best) {
+          best = c[v];
+          bv = v;
+        }
+      const int l = row0 + a * rs1 + b * rs2;
+      outs[l] = S::out(best);
+      args[l] = (uint8_t)bv;
+    }
+  }
 }
 
 template <typename T, int R, int DV>
@@ -169,7 +239,7 @@ __global__ void __launch_bounds__(kThreads) bk_fast_kernel(const FastDesc *__res
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ FastHot f;
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
-  __shared__ int32_t delta[kMaxStages * 32];
+  __shared__ int32_t sbase[kMaxStages * 32];
   __shared__ int64_t rowstart[kMaxStages];
   {
     const int *src = (const int *)&Fg->hot;
@@ -197,7 +267,7 @@ __global__ void __launch_bounds__(kThreads) bk_fast_kernel(const FastDesc *__res
       off += dg * (jj < k ? f.mstr[e][jj] : f.mrow[e]);
     }
     if (jj < k)
-      offtab[idx] = off;
+      offtab[idx] = off * (int)sizeof(T);
     else
       mrowoff[idx - k * Pmid] = off;
   }
@@ -205,11 +275,22 @@ __global__ void __launch_bounds__(kThreads) bk_fast_kernel(const FastDesc *__res
   const int warp = threadIdx.x >> 5;
 
   if (warp == kConsumerWarps) {  // ---- producer warp: TMA ring ----
-    int it = 0;
-    for (int64_t t = t_begin + blockIdx.x; t < t_end; t += gridDim.x, it++) {
-      const int s = it % f.nstages;
-      mbar_wait(&empty[s], (uint32_t)(((it / f.nstages) & 1) ^ 1));
-      issue_tile(Fg, f, in, t, s, sm, full, delta, rowstart);
+    for (int i = 1; i < kPrefetch; i++)  // warm the prefetch window
+      if (t_begin + blockIdx.x + (int64_t)i * gridDim.x < t_end)
+        prefetch_tile(Fg, f, in, t_begin + blockIdx.x + (int64_t)i * gridDim.x);
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = t_begin + blockIdx.x; t < t_end; t += gridDim.x) {
+      mbar_wait(&empty[s], ph ^ 1u);
+      issue_tile(Fg, f, in, t, s, sm, full, sbase, rowstart);
+      if (kPrefetch > 0) {
+        const int64_t tp = t + (int64_t)kPrefetch * gridDim.x;
+        if (tp < t_end) prefetch_tile(Fg, f, in, tp);
+      }
+      if (++s == f.nstages) {
+        s = 0;
+        ph ^= 1u;
+      }
     }
     return;
   }
@@ -217,116 +298,139 @@ __global__ void __launch_bounds__(kThreads) bk_fast_kernel(const FastDesc *__res
   // ---- consumer warps ----
   const int ctid = threadIdx.x;  // 0 .. 32*kConsumerWarps-1
   const int PL = f.PL, es = (int)sizeof(T);
-  int it = 0;
-  for (int64_t t = t_begin + blockIdx.x; t < t_end; t += gridDim.x, it++) {
-    const int s = it % f.nstages;
-    mbar_wait(&full[s], (uint32_t)((it / f.nstages) & 1));
+  int s = 0, b = 0;
+  uint32_t ph = 0;
+  for (int64_t t = t_begin + blockIdx.x; t < t_end; t += gridDim.x) {
+    mbar_wait(&full[s], ph);
     const unsigned char *stage = sm + s * f.stage_bytes;
     const int64_t o0 = rowstart[s] - row_begin;
     // staging: element l of this tile lives at index l + sh (16-byte phase of
     // its global address), so the aligned interior is one TMA bulk store
-    const int b = it % kOutBufs;
     const int sh = (int)((((uintptr_t)(out + o0)) & 15) / es);
     const int sha = (int)(((uintptr_t)(arg + o0)) & 15);
     T *outs = (T *)(sm + f.off_out + b * f.out_bytes) + sh;
     uint8_t *args = sm + f.off_arg + b * f.arg_bytes + sha;
+    const int c0 = f.cls_off[0], c1 = f.cls_off[1], c2 = f.cls_off[2], c3 = f.cls_off[3], c4 = f.cls_off[4];
+    const int sel = (c2 > c1 ? 1 : 0) | (c3 > c2 ? 2 : 0) | (c4 > c3 ? 4 : 0);
     for (int q = ctid; q < Pmid; q += 32 * kConsumerWarps) {
       Acc P0[DV], P1[R][DV], P2[R][DV], P3[R][R][DV];
+      // class 0 (no group digit): P0[v]
+      if (c1 > c0) {
+        const unsigned char *p = sm + sbase[s * 32 + c0] + offtab[c0 * Pmid + q];
 #pragma unroll
-      for (int v = 0; v < DV; v++) {
-        P0[v] = S::zero();
+        for (int v = 0; v < DV; v++) P0[v] = (Acc)((const T *)p)[v];
+        for (int jj = c0 + 1; jj < c1; jj++) {
+          const unsigned char *pj = sm + sbase[s * 32 + jj] + offtab[jj * Pmid + q];
 #pragma unroll
-        for (int a = 0; a < R; a++) {
-          P1[a][v] = S::zero();
-          P2[a][v] = S::zero();
-#pragma unroll
-          for (int bb = 0; bb < R; bb++) P3[a][bb][v] = S::zero();
+          for (int v = 0; v < DV; v++) P0[v] = S::add(P0[v], (Acc)((const T *)pj)[v]);
         }
-      }
-      for (int jj = f.cls_off[0]; jj < f.cls_off[1]; jj++) {  // neither group digit
-        const T *p = (const T *)(stage + f.soff[jj]) + delta[s * 32 + jj] + offtab[jj * Pmid + q];
+      } else {
 #pragma unroll
-        for (int v = 0; v < DV; v++) P0[v] = S::add(P0[v], (Acc)p[v]);
+        for (int v = 0; v < DV; v++) P0[v] = S::zero();
       }
-      for (int jj = f.cls_off[1]; jj < f.cls_off[2]; jj++) {  // g1 only
-        const T *p = (const T *)(stage + f.soff[jj]) + delta[s * 32 + jj] + offtab[jj * Pmid + q];
-        const int s1 = f.sg1[jj];
+      // class 1 (g1 only): P1[a][v]
+      if (sel & 1) {
+        const unsigned char *p = sm + sbase[s * 32 + c1] + offtab[c1 * Pmid + q];
+        const int s1 = f.sg1[c1];
 #pragma unroll
         for (int a = 0; a < R; a++)
 #pragma unroll
-          for (int v = 0; v < DV; v++) P1[a][v] = S::add(P1[a][v], (Acc)p[a * s1 + v]);
+          for (int v = 0; v < DV; v++) P1[a][v] = (Acc)((const T *)(p + a * s1))[v];
+        for (int jj = c1 + 1; jj < c2; jj++) {
+          const unsigned char *pj = sm + sbase[s * 32 + jj] + offtab[jj * Pmid + q];
+          const int t1 = f.sg1[jj];
+#pragma unroll
+          for (int a = 0; a < R; a++)
+#pragma unroll
+            for (int v = 0; v < DV; v++) P1[a][v] = S::add(P1[a][v], (Acc)((const T *)(pj + a * t1))[v]);
+        }
       }
-      for (int jj = f.cls_off[2]; jj < f.cls_off[3]; jj++) {  // g2 only
-        const T *p = (const T *)(stage + f.soff[jj]) + delta[s * 32 + jj] + offtab[jj * Pmid + q];
-        const int s2 = f.sg2[jj];
+      // class 2 (g2 only): P2[b][v]
+      if (sel & 2) {
+        const unsigned char *p = sm + sbase[s * 32 + c2] + offtab[c2 * Pmid + q];
+        const int s2 = f.sg2[c2];
 #pragma unroll
         for (int bb = 0; bb < R; bb++)
 #pragma unroll
-          for (int v = 0; v < DV; v++) P2[bb][v] = S::add(P2[bb][v], (Acc)p[bb * s2 + v]);
+          for (int v = 0; v < DV; v++) P2[bb][v] = (Acc)((const T *)(p + bb * s2))[v];
+        for (int jj = c2 + 1; jj < c3; jj++) {
+          const unsigned char *pj = sm + sbase[s * 32 + jj] + offtab[jj * Pmid + q];
+          const int t2 = f.sg2[jj];
+#pragma unroll
+          for (int bb = 0; bb < R; bb++)
+#pragma unroll
+            for (int v = 0; v < DV; v++) P2[bb][v] = S::add(P2[bb][v], (Acc)((const T *)(pj + bb * t2))[v]);
+        }
       }
-      for (int jj = f.cls_off[3]; jj < f.cls_off[4]; jj++) {  // both
-        const T *p = (const T *)(stage + f.soff[jj]) + delta[s * 32 + jj] + offtab[jj * Pmid + q];
-        const int s1 = f.sg1[jj], s2 = f.sg2[jj];
+      // class 3 (both): P3[a][b][v]
+      if (sel & 4) {
+        const unsigned char *p = sm + sbase[s * 32 + c3] + offtab[c3 * Pmid + q];
+        const int s1 = f.sg1[c3], s2 = f.sg2[c3];
 #pragma unroll
         for (int a = 0; a < R; a++)
 #pragma unroll
           for (int bb = 0; bb < R; bb++)
 #pragma unroll
-            for (int v = 0; v < DV; v++) P3[a][bb][v] = S::add(P3[a][bb][v], (Acc)p[a * s1 + bb * s2 + v]);
+            for (int v = 0; v < DV; v++) P3[a][bb][v] = (Acc)((const T *)(p + a * s1 + bb * s2))[v];
+        for (int jj = c3 + 1; jj < c4; jj++) {
+          const unsigned char *pj = sm + sbase[s * 32 + jj] + offtab[jj * Pmid + q];
+          const int t1 = f.sg1[jj], t2 = f.sg2[jj];
+#pragma unroll
+          for (int a = 0; a < R; a++)
+#pragma unroll
+            for (int bb = 0; bb < R; bb++)
+#pragma unroll
+              for (int v = 0; v < DV; v++)
+                P3[a][bb][v] = S::add(P3[a][bb][v], (Acc)((const T *)(pj + a * t1 + bb * t2))[v]);
+        }
       }
       const int row0 = mrowoff[q];
-#pragma unroll
-      for (int a = 0; a < R; a++) {
-        Acc Q[DV];
-#pragma unroll
-        for (int v = 0; v < DV; v++) Q[v] = S::add(P0[v], P1[a][v]);
-#pragma unroll
-        for (int bb = 0; bb < R; bb++) {
-          Acc best = S::zero();
-          int bv = 0;
-#pragma unroll
-          for (int v = 0; v < DV; v++) {
-            Acc c = S::add3(Q[v], P2[bb][v], P3[a][bb][v]);
-            if (v == 0 || c < best) {
-              best = c;
-              bv = v;
-            }
-          }
-          const int l = row0 + a * f.rs1 + bb * f.rs2;
-          outs[l] = S::out(best);
-          args[l] = (uint8_t)bv;
-        }
+      switch (sel) {
+        case 0: combine<T, R, DV, false, false, false>(P0, P1, P2, P3, outs, args, row0, f.rs1, f.rs2); break;
+        case 1: combine<T, R, DV, true, false, false>(P0, P1, P2, P3, outs, args, row0, f.rs1, f.rs2); break;
+        case 2: combine<T, R, DV, false, true, false>(P0, P1, P2, P3, outs, args, row0, f.rs1, f.rs2); break;
+        case 3: combine<T, R, DV, true, true, false>(P0, P1, P2, P3, outs, args, row0, f.rs1, f.rs2); break;
+        case 4: combine<T, R, DV, false, false, true>(P0, P1, P2, P3, outs, args, row0, f.rs1, f.rs2); break;
+        case 5: combine<T, R, DV, true, false, true>(P0, P1, P2, P3, outs, args, row0, f.rs1, f.rs2); break;
+        case 6: combine<T, R, DV, false, true, true>(P0, P1, P2, P3, outs, args, row0, f.rs1, f.rs2); break;
+        default: combine<T, R, DV, true, true, true>(P0, P1, P2, P3, outs, args, row0, f.rs1, f.rs2); break;
       }
     }
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);  // input stage free
     fence_proxy_async_smem();                             // staged rows -> async proxy
     consumer_sync();
-    // aligned interior by TMA bulk stores, ragged head/tail by plain stores
-    T *gout = out + o0;
-    const int h = (int)(((16 - (((uintptr_t)gout) & 15)) & 15) / es);
-    const int nmid = ((PL - min(h, PL)) * es / 16) * 16 / es;
-    uint8_t *ga = arg ? arg + o0 : nullptr;
-    const int ha = ga ? (int)((16 - (((uintptr_t)ga) & 15)) & 15) : 0;
-    const int nmida = ga ? ((PL - min(ha, PL)) / 16) * 16 : 0;
-    if (ctid == 0) {
-      if (nmid > 0) tma_store_1d(gout + h, outs + h, (uint32_t)(nmid * es));
-      if (nmida > 0) tma_store_1d(ga + ha, args + ha, (uint32_t)nmida);
-      bulk_commit();
-      bulk_wait_read<kOutBufs - 1>();  // staging buffer of tile it-(kOutBufs-1) reusable
-    }
-    // ragged head/tail (< 16 bytes each side): plain stores from staging
-    {
-      const int hh = min(h, PL), tl = PL - hh - nmid;
+    if (ctid < 32) {  // warp 0: aligned interior by TMA bulk stores, ragged ends plainly
+      T *gout = out + o0;
+      const int h = (int)(((16 - (((uintptr_t)gout) & 15)) & 15) / es);
+      const int hh = min(h, PL);
+      const int nmid = ((PL - hh) * es / 16) * 16 / es;
+      const int tl = PL - hh - nmid;
+      if (ctid == 0 && nmid > 0) tma_store_1d(gout + hh, outs + hh, (uint32_t)(nmid * es));
       if (ctid < hh) gout[ctid] = outs[ctid];
-      else if (ctid < hh + tl) gout[hh + nmid + (ctid - hh)] = outs[hh + nmid + (ctid - hh)];
-      if (ga) {
-        const int hha = min(ha, PL), tla = PL - hha - nmida;
-        const int c2 = ctid - 64;
-        if (c2 >= 0 && c2 < hha) ga[c2] = args[c2];
-        else if (c2 >= hha && c2 < hha + tla) ga[hha + nmida + (c2 - hha)] = args[hha + nmida + (c2 - hha)];
+      if (ctid < tl) gout[hh + nmid + ctid] = outs[hh + nmid + ctid];
+      if (arg) {
+        uint8_t *ga = arg + o0;
+        const int ha = min((int)((16 - (((uintptr_t)ga) & 15)) & 15), PL);
+        const int nmida = ((PL - ha) / 16) * 16;
+        const int tla = PL - ha - nmida;
+        if (ctid == 0 && nmida > 0) tma_store_1d(ga + ha, args + ha, (uint32_t)nmida);
+        if (ctid < ha) ga[ctid] = args[ctid];
+        if (ctid < tla) ga[ha + nmida + ctid] = args[ha + nmida + ctid];
+      }
+      if (ctid == 0) {
+        bulk_commit();
+        // staging buffer of tile (i - kOutBufs + 1) is free once its store has
+        // read it; ordered before that buffer's next writers by the next
+        // consumer_sync
+        bulk_wait_read<kOutBufs - 1>();
       }
     }
+    if (++s == f.nstages) {
+      s = 0;
+      ph ^= 1u;
+    }
+    if (++b == kOutBufs) b = 0;
   }
   if (ctid == 0) bulk_wait_all();
 }
@@ -353,9 +457,10 @@ cudaError_t dispatch(int R, int DV, const FastDesc *d, const InPtrs &in, void *o
                      cudaStream_t s) {
 #define GBE_CASE(r, dv) \
   if (R == r && DV == dv) return launch_one<T, r, dv>(d, in, out, arg, rb, t0, t1, grid, block, smem, s);
-  GBE_CASE(2, 2) GBE_CASE(2, 3) GBE_CASE(2, 4) GBE_CASE(2, 5)
-  GBE_CASE(3, 2) GBE_CASE(3, 3) GBE_CASE(3, 4) GBE_CASE(3, 5)
-  GBE_CASE(4, 2) GBE_CASE(4, 3)
+  GBE_CASE(2, 2) GBE_CASE(2, 3) GBE_CASE(2, 4) GBE_CASE(2, 5) GBE_CASE(3, 2) GBE_CASE(3, 3)
+  if constexpr (sizeof(T) == 4) {  // f64 keeps R*R*DV <= 27 (register budget)
+    GBE_CASE(3, 4) GBE_CASE(3, 5) GBE_CASE(4, 2) GBE_CASE(4, 3)
+  }
 #undef GBE_CASE
   return cudaErrorInvalidValue;
 }
@@ -378,8 +483,8 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
   const int es = h.semiring == GBE_MINSUM_F64 ? 8 : 4;
   if (m < 2 || k < 1 || k > 32 || DV < 2 || DV > 5) return false;
   if (row_end <= row_begin) return false;
-  const int64_t kPLMax = 8192;
-  const size_t kSmemMax = 200 * 1024;
+  const int64_t kPLMax = 16384;
+  const size_t kSmemMax = 112 * 1024;
   // inputs' sizes (cells) to find the largest
   auto has = [&](int j, int p) { return h.stride[j][p] != 0; };
   std::vector<int64_t> cells(k, DV);
@@ -430,8 +535,8 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
         int cls = (has(j, g1) ? 1 : 0) + (has(j, g2) ? 2 : 0);
         if (cls != c) continue;
         f.in_idx[jj] = j;
-        f.sg1[jj] = (int32_t)h.stride[j][g1];
-        f.sg2[jj] = (int32_t)h.stride[j][g2];
+        f.sg1[jj] = (int32_t)(h.stride[j][g1] * es);  // bytes
+        f.sg2[jj] = (int32_t)(h.stride[j][g2] * es);
         int64_t sl = DV;
         for (int p = m - nl; p < m; p++)
           if (has(j, p)) sl *= h.radix[p];
@@ -491,7 +596,7 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     size_t fixed = kOutBufs * ((size_t)f.out_bytes + f.arg_bytes) + (size_t)(k + 1) * Pmid * 4 + 256;
     // 2 CTAs per SM when possible (~110 KB each), 2..4 input stages
     int nst = kMaxStages;
-    while (nst > 2 && fixed + nst * off > 110 * 1024) nst--;
+    while (nst > 2 && fixed + nst * off > 112 * 1024) nst--;
     f.nstages = nst;
     off = nst * off;
     f.off_out = (int32_t)off;

@@ -13,7 +13,7 @@ struct FastHot {
   int32_t k, es, PL, Pmid, R, DV, nmid, nH;
   int32_t cls_off[5];    // input class ranges: none / g1 / g2 / both
   int32_t in_idx[32];    // class-ordered input -> original input
-  int32_t sg1[32], sg2[32];  // element strides of the group digits (0 if absent)
+  int32_t sg1[32], sg2[32];  // byte strides of the group digits (0 if absent)
   int32_t slen[32];      // slice length (elements) per tile
   int32_t soff[32];      // byte offset of the slice inside a stage
   int32_t stage_bytes;
