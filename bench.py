@@ -237,11 +237,14 @@ def main():
     big_ms = sum(t["ms"] for s in stats for t in s["tasks"] if t["var"] == big["var"] and t["mb"] == big["mb"]) / len(stats)
     peaks, peak_src = measured_peaks()
     achieved = bk_bytes / (bk_ms * 1e-3) / 1e9
-    traffic = None
+    traffic, traffic_note = None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(args.workload)
+            tr = json.load(open(tpath)).get(args.workload)
+            traffic = tr["dram_bytes_per_launch"]
+            traffic_note = (f"{tr['kernel']}: dram read+write per launch (algorithmic "
+                            f"{tr['algorithmic_bytes_per_launch']:.3e} B), {tr['source']}")
         except Exception:
             traffic = None
 
@@ -262,7 +265,7 @@ def main():
                    "parallelism": f"row-shard x{world}" if world > 1 else "1 GPU",
                    "l2": "no flush: every step writes >= 14 GB of UTIL tables (> 126 MB L2)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "traffic_note": traffic_note,
                      "kernel": "bk (all bucket launches of one step)", "peak_source": peak_src,
                      "bk_ms_per_step": bk_ms, "bk_share_of_step": bk_ms / ms_t,
                      "events_pass_ms_per_step": ms_t,

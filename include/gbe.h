@@ -233,6 +233,16 @@ gbe_status gbe_set_allgather(int (*ag)(const void *send, void *recv, size_t byte
                                        void *stream, void *u),
                              void *u);
 
+/* Built-in NCCL transport for the all-gather (NVLink 5 / NVSwitch), loaded
+ * with dlopen("libnccl.so.2").  Rank 0 calls gbe_comm_nccl_id(id[128]) and
+ * shares the 128 bytes with the other ranks (e.g. over torch.distributed);
+ * every rank then calls gbe_comm_nccl_init(id, nranks, rank, device), which
+ * installs the all-gather hook.  gbe_comm_finalize() destroys the
+ * communicator and removes the hook.  GBE_E_COMM if NCCL is unavailable. */
+gbe_status gbe_comm_nccl_id(void *id128);
+gbe_status gbe_comm_nccl_init(const void *id128, int32_t nranks, int32_t rank, int32_t device);
+gbe_status gbe_comm_finalize(void);
+
 /* Thread-local message of the last failing call ("" if none). */
 const char *gbe_last_error(void);
 

@@ -260,6 +260,24 @@ gbe_status gbe_set_allgather(int (*ag)(const void *, void *, size_t, void *, voi
   return guard([&] { set_allgather(ag, u); });
 }
 
+gbe_status gbe_comm_nccl_id(void *id128) {
+  return guard([&] {
+    if (!id128) GBE_FAIL(GBE_E_INVALID, "null id");
+    comm_nccl_id(id128);
+  });
+}
+
+gbe_status gbe_comm_nccl_init(const void *id128, int32_t nranks, int32_t rank, int32_t device) {
+  return guard([&] {
+    if (!id128) GBE_FAIL(GBE_E_INVALID, "null id");
+    comm_nccl_init(id128, nranks, rank, device);
+  });
+}
+
+gbe_status gbe_comm_finalize(void) {
+  return guard([&] { comm_finalize(); });
+}
+
 const char *gbe_last_error(void) { return last_error(); }
 
 const char *gbe_version(void) { return "gbe-b200 0.1 (sm_100a)"; }

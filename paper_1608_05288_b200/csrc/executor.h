@@ -9,6 +9,9 @@ struct RunImpl;
 void set_allocator(void *(*a)(size_t, void *, void *), void (*f)(void *, void *), void *u);
 void set_allgather(int (*ag)(const void *, void *, size_t, void *, void *), void *u);
 void dev_plan_free(void *d);
+void comm_nccl_id(void *id128);
+void comm_nccl_init(const void *id128, int nranks, int rank, int device);
+void comm_finalize();
 
 RunImpl *run_create(gbe_plan *gp, void *stream, bool mbe);
 void run_destroy(RunImpl *R);

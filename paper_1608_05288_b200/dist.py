@@ -97,12 +97,22 @@ def uninstall():
 
 
 def init(local_rank, backend="nccl"):
-    """torchrun-style init (127.0.0.1 rendezvous from the environment)."""
+    """torchrun-style init (127.0.0.1 rendezvous from the environment).
+    backend "nccl": libgbe's built-in NCCL communicator does the data-path
+    all-gather on the solve stream (no Python on the data path); the torch
+    process group only carries the 128-byte NCCL id, barriers and the
+    max-over-ranks timing.  backend "gloo": host-staged Python hook."""
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     if not dist.is_initialized():
         dist.init_process_group(backend=backend, device_id=torch.device("cuda", local_rank)
                                 if backend == "nccl" else None)
-    install(local_rank, backend)
+    if backend == "nccl":
+        obj = [_g.comm_nccl_id() if dist.get_rank() == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        _g.comm_nccl_init(obj[0], dist.get_world_size(), dist.get_rank(), local_rank)
+        _STATE.update(backend="nccl-builtin")
+    else:
+        install(local_rank, backend)
     return dist.group.WORLD
 
 
@@ -122,6 +132,10 @@ def max_over_ranks(x, pg):
 
 def finish(pg):
     if pg is not None and dist.is_initialized():
-        uninstall()
+        if _STATE.get("backend") == "nccl-builtin":
+            _g.comm_finalize()
+            _STATE.clear()
+        else:
+            uninstall()
         dist.barrier()
         dist.destroy_process_group()

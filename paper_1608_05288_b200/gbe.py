@@ -30,7 +30,8 @@ EXPORTED = [
     "gbe_plan_create", "gbe_plan_info", "gbe_plan_destroy", "gbe_solve_be", "gbe_solve_mbe",
     "gbe_dpop_util", "gbe_dpop_value", "gbe_run_stats", "gbe_run_table", "gbe_run_destroy",
     "gbe_bucket_kernel", "gbe_set_allocator", "gbe_set_allgather", "gbe_last_error",
-    "gbe_version", "gbe_bucket_kernel_variant",
+    "gbe_version", "gbe_bucket_kernel_variant", "gbe_comm_nccl_id", "gbe_comm_nccl_init",
+    "gbe_comm_finalize",
 ]
 
 
@@ -100,6 +101,9 @@ def lib():
         L.gbe_bucket_kernel_variant.restype = i32
         L.gbe_set_allocator.argtypes = [ALLOC_FN, FREE_FN, vp]
         L.gbe_set_allgather.argtypes = [AG_FN, vp]
+        L.gbe_comm_nccl_id.argtypes = [vp]
+        L.gbe_comm_nccl_init.argtypes = [vp, i32, i32, i32]
+        L.gbe_comm_finalize.argtypes = []
         L.gbe_last_error.restype = ctypes.c_char_p
         L.gbe_version.restype = ctypes.c_char_p
         for name in EXPORTED:
@@ -333,6 +337,23 @@ def set_allocator(alloc, free):
     f = FREE_FN(lambda p, u: free(p))
     _HOOKS["alloc"] = (a, f)
     _check(lib().gbe_set_allocator(a, f, None))
+
+
+def comm_nccl_id() -> bytes:
+    """128-byte NCCL unique id (rank 0)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().gbe_comm_nccl_id(buf))
+    return buf.raw
+
+
+def comm_nccl_init(uid: bytes, nranks: int, rank: int, device: int):
+    """Built-in NCCL all-gather for row-sharded plans (all ranks)."""
+    buf = ctypes.create_string_buffer(bytes(uid), 128)
+    _check(lib().gbe_comm_nccl_init(buf, int(nranks), int(rank), int(device)))
+
+
+def comm_finalize():
+    _check(lib().gbe_comm_finalize())
 
 
 def version():
