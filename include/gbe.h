@@ -155,7 +155,8 @@ void gbe_plan_destroy(gbe_plan *plan);
 /* Exact BE (Alg. 1 / Alg. 3 with no partition): uploads the original tables
  * (one batched H2D), runs one bucket kernel per bucket with device-resident
  * messages, then the value phase; blocks until done.  opt = optimum,
- * assign_out[n] = the assignment (smallest-index tie-break, A8).  stats_json
+ * assign_out[n] = the assignment (smallest-index tie-break, A8); assign_out
+ * NULL = value-only solve (no value phase; allowed with "retain":"none").  stats_json
  * (NULL ok) receives per-bucket timings when the plan has "timing":true. */
 gbe_status gbe_solve_be(gbe_plan *plan, void *stream, gbe_value *opt, int32_t *assign_out,
                         char *stats_json, size_t cap);
@@ -166,8 +167,11 @@ gbe_status gbe_solve_mbe(gbe_plan *plan, void *stream, gbe_value *lower, gbe_val
                          int32_t *assign_out, char *stats_json, size_t cap);
 
 /* DPOP UTIL phase on the plan's pseudo-tree: UTIL messages are the
- * bucket functions (Thm 1); siblings run concurrently.  The run
- * keeps the argmin tables for the VALUE phase.  root_util = optimum. */
+ * bucket functions (Thm 1).  The run keeps the argmin tables for
+ * the VALUE phase.  root_util = optimum.  With an MBE plan (ibound >= 0) this
+ * is ADPOP: the messages are the mini-bucket functions, root_util
+ * is the lower bound, and the VALUE phase minimises over all mini-bucket
+ * functions of each variable (A7). */
 gbe_status gbe_dpop_util(gbe_plan *plan, void *stream, gbe_run **run_out,
                          gbe_value *root_util);
 /* DPOP VALUE phase: assign_out[n]. */

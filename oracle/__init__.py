@@ -211,7 +211,9 @@ class Run:
     """Result of or_solve: tables in creation order, optimum / bounds,
     assignment."""
 
-    def __init__(self, inst, order, ibound=-1, keep_tables=True, nthreads=0):
+    def __init__(self, inst, order, ibound=-1, keep_tables=True, nthreads=0, table_fn=None):
+        """table_fn(t, table, out, arg), if given, receives each kept table
+        instead of the Run storing a copy (bounded memory for big runs)."""
         self.inst = inst
         self._P = Problem(inst)
         self.order = np.ascontiguousarray(order, dtype=np.int32)
@@ -245,7 +247,11 @@ class Run:
                                                 _p(out, ctypes.c_double) if inst.is_f64 else None,
                                                 _p(arg, ctypes.c_uint8))
                         if ok:
-                            T.out, T.arg = out, arg
+                            if table_fn is not None:
+                                table_fn(t, T, out, arg)
+                            else:
+                                T.out, T.arg = out, arg
+                        del out, arg
                     self.tables.append(T)
                 if inst.is_f64:
                     self.value = float(L.or_run_value_f(h))

@@ -48,6 +48,11 @@ struct SrF;
 template <>
 struct SrF<int32_t> {
   using Acc = uint32_t;
+  static constexpr bool kInt = true;
+  // sums of <= 3 clamped partials (each <= 2^30) fit uint32 without clamping
+  __device__ __forceinline__ static Acc add_nc(Acc a, Acc b) { return a + b; }
+  __device__ __forceinline__ static Acc add3_nc(Acc a, Acc b, Acc c) { return a + b + c; }
+  __device__ __forceinline__ static Acc inf() { return kInf; }
   __device__ __forceinline__ static Acc zero() { return 0u; }
   __device__ __forceinline__ static Acc add(Acc a, Acc b) {
     uint32_t s = a + b;
@@ -62,6 +67,10 @@ struct SrF<int32_t> {
 template <>
 struct SrF<double> {
   using Acc = double;
+  static constexpr bool kInt = false;
+  __device__ __forceinline__ static Acc add_nc(Acc a, Acc b) { return __dadd_rn(a, b); }
+  __device__ __forceinline__ static Acc add3_nc(Acc a, Acc b, Acc c) { return __dadd_rn(__dadd_rn(a, b), c); }
+  __device__ __forceinline__ static Acc inf() { return __longlong_as_double(0x7ff0000000000000LL); }
   __device__ __forceinline__ static Acc zero() { return 0.0; }
   __device__ __forceinline__ static Acc add(Acc a, Acc b) { return __dadd_rn(a, b); }
   __device__ __forceinline__ static Acc add3(Acc a, Acc b, Acc c) { return __dadd_rn(__dadd_rn(a, b), c); }
@@ -133,14 +142,14 @@ struct SliceRange {
   int64_t rowstart;  // lane 0 only
 };
 __device__ __forceinline__ SliceRange tile_slice(const FastDesc *__restrict__ Fg, const FastHot &f,
-                                                 const InPtrs &in, int64_t t) {
+                                                 const InPtrs &in, int64_t t, const int64_t *hstr_s) {
   const int lane = threadIdx.x & 31;
   int dig = 0;
   if (lane < f.nH) dig = (int)(((uint32_t)t / (uint32_t)Fg->hdiv[lane]) % (uint32_t)Fg->hrad[lane]);
   int64_t base = 0, rs = 0;
   for (int e = 0; e < f.nH; e++) {
     int de = __shfl_sync(0xffffffffu, dig, e);
-    if (lane < f.k) base += (int64_t)de * Fg->hstr[e][lane];
+    if (lane < f.k) base += (int64_t)de * hstr_s[e * 32 + lane];
     if (lane == 0) rs += (int64_t)de * Fg->hrow[e];
   }
   SliceRange r{0, 0, 0, rs};
@@ -160,9 +169,10 @@ __device__ __forceinline__ SliceRange tile_slice(const FastDesc *__restrict__ Fg
 // bulk copy per input) and publishes the slice bases for the consumers.
 __device__ __forceinline__ void issue_tile(const FastDesc *__restrict__ Fg, const FastHot &f,
                                            const InPtrs &in, int64_t t, int s, unsigned char *sm,
-                                           uint64_t *full, int32_t *sbase, int64_t *rowstart) {
+                                           uint64_t *full, int32_t *sbase, int64_t *rowstart,
+                                           const int64_t *hstr_s) {
   const int lane = threadIdx.x & 31;
-  SliceRange r = tile_slice(Fg, f, in, t);
+  SliceRange r = tile_slice(Fg, f, in, t, hstr_s);
   if (lane < f.k) sbase[s * 32 + lane] = s * f.stage_bytes + f.soff[lane] + (int32_t)r.skew;
   uint32_t total = r.bytes;
   for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
@@ -179,8 +189,8 @@ __device__ __forceinline__ void issue_tile(const FastDesc *__restrict__ Fg, cons
 // L2 prefetch of the large slices of a future tile: the DRAM latency is paid
 // off the critical path, the TMA load of that tile then hits L2.
 __device__ __forceinline__ void prefetch_tile(const FastDesc *__restrict__ Fg, const FastHot &f,
-                                              const InPtrs &in, int64_t t) {
-  SliceRange r = tile_slice(Fg, f, in, t);
+                                              const InPtrs &in, int64_t t, const int64_t *hstr_s) {
+  SliceRange r = tile_slice(Fg, f, in, t, hstr_s);
   const int lane = threadIdx.x & 31;
   if (lane < f.k && r.bytes >= 2048) prefetch_l2((const void *)r.a16, r.bytes);
 }
@@ -192,25 +202,28 @@ __device__ __forceinline__ void combine(const typename SrF<T>::Acc (&P0)[DV],
                                         const typename SrF<T>::Acc (&P1)[R][DV],
                                         const typename SrF<T>::Acc (&P2)[R][DV],
                                         const typename SrF<T>::Acc (&P3)[R][R][DV], T *outs,
-                                        uint8_t *args, int row0, int rs1, int rs2) {
+                                        uint8_t *args, const int (&loff)[R][R]) {
   using S = SrF<T>;
   using Acc = typename S::Acc;
 #pragma unroll
   for (int a = 0; a < R; a++) {
-    Acc Q[DV];
+    Acc Q[DV];  // clamped: P0 + P1 can reach 2^31
 #pragma unroll
     for (int v = 0; v < DV; v++) Q[v] = H1 ? S::add(P0[v], P1[a][v]) : P0[v];
 #pragma unroll
     for (int b = 0; b < R; b++) {
+      // unclamped cell sums (int: <= 3 * 2^30 < 2^32); min over v, then one
+      // clamp per row.  If the row minimum is infinite every value clamps to
+      // INF and the first index wins (A8).
       Acc c[DV];
 #pragma unroll
       for (int v = 0; v < DV; v++) {
         if (H2 && H3)
-          c[v] = S::add3(Q[v], P2[b][v], P3[a][b][v]);
+          c[v] = S::add3_nc(Q[v], P2[b][v], P3[a][b][v]);
         else if (H2)
-          c[v] = S::add(Q[v], P2[b][v]);
+          c[v] = S::add_nc(Q[v], P2[b][v]);
         else if (H3)
-          c[v] = S::add(Q[v], P3[a][b][v]);
+          c[v] = S::add_nc(Q[v], P3[a][b][v]);
         else
           c[v] = Q[v];
       }
@@ -222,7 +235,11 @@ __device__ __forceinline__ void combine(const typename SrF<T>::Acc (&P0)[DV],
           best = c[v];
           bv = v;
         }
-      const int l = row0 + a * rs1 + b * rs2;
+      if (S::kInt && best >= S::inf()) {
+        best = S::inf();
+        bv = 0;
+      }
+      const int l = loff[a][b];
       outs[l] = S::out(best);
       args[l] = (uint8_t)bv;
     }
@@ -241,6 +258,8 @@ __global__ void __launch_bounds__(kThreads) bk_fast_kernel(const FastDesc *__res
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ int32_t sbase[kMaxStages * 32];
   __shared__ int64_t rowstart[kMaxStages];
+  __shared__ int64_t hstr_s[32 * 32];  // producer's per-digit input strides
+  for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) hstr_s[i] = Fg->hstr[i / 32][i % 32];
   {
     const int *src = (const int *)&Fg->hot;
     int *dst = (int *)&f;
@@ -277,15 +296,15 @@ __global__ void __launch_bounds__(kThreads) bk_fast_kernel(const FastDesc *__res
   if (warp == kConsumerWarps) {  // ---- producer warp: TMA ring ----
     for (int i = 1; i < kPrefetch; i++)  // warm the prefetch window
       if (t_begin + blockIdx.x + (int64_t)i * gridDim.x < t_end)
-        prefetch_tile(Fg, f, in, t_begin + blockIdx.x + (int64_t)i * gridDim.x);
+        prefetch_tile(Fg, f, in, t_begin + blockIdx.x + (int64_t)i * gridDim.x, hstr_s);
     int s = 0;
     uint32_t ph = 0;
     for (int64_t t = t_begin + blockIdx.x; t < t_end; t += gridDim.x) {
       mbar_wait(&empty[s], ph ^ 1u);
-      issue_tile(Fg, f, in, t, s, sm, full, sbase, rowstart);
+      issue_tile(Fg, f, in, t, s, sm, full, sbase, rowstart, hstr_s);
       if (kPrefetch > 0) {
         const int64_t tp = t + (int64_t)kPrefetch * gridDim.x;
-        if (tp < t_end) prefetch_tile(Fg, f, in, tp);
+        if (tp < t_end) prefetch_tile(Fg, f, in, tp, hstr_s);
       }
       if (++s == f.nstages) {
         s = 0;
@@ -311,6 +330,11 @@ __global__ void __launch_bounds__(kThreads) bk_fast_kernel(const FastDesc *__res
     T *outs = (T *)(sm + f.off_out + b * f.out_bytes) + sh;
     uint8_t *args = sm + f.off_arg + b * f.arg_bytes + sha;
     const int c0 = f.cls_off[0], c1 = f.cls_off[1], c2 = f.cls_off[2], c3 = f.cls_off[3], c4 = f.cls_off[4];
+    int loff[R][R];  // in-tile row offsets of the group digits (tile-invariant)
+#pragma unroll
+    for (int a = 0; a < R; a++)
+#pragma unroll
+      for (int bb = 0; bb < R; bb++) loff[a][bb] = a * f.rs1 + bb * f.rs2;
     const int sel = (c2 > c1 ? 1 : 0) | (c3 > c2 ? 2 : 0) | (c4 > c3 ? 4 : 0);
     for (int q = ctid; q < Pmid; q += 32 * kConsumerWarps) {
       Acc P0[DV], P1[R][DV], P2[R][DV], P3[R][R][DV];
@@ -385,15 +409,17 @@ __global__ void __launch_bounds__(kThreads) bk_fast_kernel(const FastDesc *__res
         }
       }
       const int row0 = mrowoff[q];
+      T *outq = outs + row0;
+      uint8_t *argq = args + row0;
       switch (sel) {
-        case 0: combine<T, R, DV, false, false, false>(P0, P1, P2, P3, outs, args, row0, f.rs1, f.rs2); break;
-        case 1: combine<T, R, DV, true, false, false>(P0, P1, P2, P3, outs, args, row0, f.rs1, f.rs2); break;
-        case 2: combine<T, R, DV, false, true, false>(P0, P1, P2, P3, outs, args, row0, f.rs1, f.rs2); break;
-        case 3: combine<T, R, DV, true, true, false>(P0, P1, P2, P3, outs, args, row0, f.rs1, f.rs2); break;
-        case 4: combine<T, R, DV, false, false, true>(P0, P1, P2, P3, outs, args, row0, f.rs1, f.rs2); break;
-        case 5: combine<T, R, DV, true, false, true>(P0, P1, P2, P3, outs, args, row0, f.rs1, f.rs2); break;
-        case 6: combine<T, R, DV, false, true, true>(P0, P1, P2, P3, outs, args, row0, f.rs1, f.rs2); break;
-        default: combine<T, R, DV, true, true, true>(P0, P1, P2, P3, outs, args, row0, f.rs1, f.rs2); break;
+        case 0: combine<T, R, DV, false, false, false>(P0, P1, P2, P3, outq, argq, loff); break;
+        case 1: combine<T, R, DV, true, false, false>(P0, P1, P2, P3, outq, argq, loff); break;
+        case 2: combine<T, R, DV, false, true, false>(P0, P1, P2, P3, outq, argq, loff); break;
+        case 3: combine<T, R, DV, true, true, false>(P0, P1, P2, P3, outq, argq, loff); break;
+        case 4: combine<T, R, DV, false, false, true>(P0, P1, P2, P3, outq, argq, loff); break;
+        case 5: combine<T, R, DV, true, false, true>(P0, P1, P2, P3, outq, argq, loff); break;
+        case 6: combine<T, R, DV, false, true, true>(P0, P1, P2, P3, outq, argq, loff); break;
+        default: combine<T, R, DV, true, true, true>(P0, P1, P2, P3, outq, argq, loff); break;
       }
     }
     __syncwarp();

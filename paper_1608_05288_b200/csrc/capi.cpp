@@ -192,10 +192,10 @@ gbe_status gbe_solve_mbe(gbe_plan *plan, void *stream, gbe_value *lower, gbe_val
 gbe_status gbe_dpop_util(gbe_plan *plan, void *stream, gbe_run **run_out, gbe_value *root_util) {
   return guard([&] {
     if (!plan || !run_out) GBE_FAIL(GBE_E_INVALID, "null argument");
-    if (plan->plan->ibound >= 0) GBE_FAIL(GBE_E_INVALID, "DPOP needs an exact plan (i-bound < 0)");
     auto *r = new gbe_run();
     try {
-      r->impl = run_create(plan, stream, false);
+      // an MBE plan gives ADPOP: UTIL messages = mini-bucket functions
+      r->impl = run_create(plan, stream, plan->plan->ibound >= 0);
     } catch (...) {
       delete r;
       throw;

@@ -164,7 +164,7 @@ static void plan_arena(const Plan &P, DevPlan *D, bool mbe_mode) {
   A.off_raw = fl.alloc(raw);
   A.off_sorted = fl.alloc(raw);
   fl.release(A.off_raw, raw);  // raw tables are dead after the relayout
-  const bool want_arg = !mbe_mode || P.ex.retain >= 2;
+  const bool want_arg = (!mbe_mode && P.ex.retain >= 1) || P.ex.retain >= 2;
   std::vector<size_t> out_b(nt, 0), full_b(nt, 0);
   for (size_t ti = 0; ti < nt; ti++) {
     const Task &t = P.tasks[ti];
@@ -410,7 +410,7 @@ static void run_util(RunImpl &R) {
   R.d_sorted = R.base + R.A->off_sorted;
   CK(relayout_launch(R.d_raw, R.d_sorted, (int)el, p.nf, D->d_off, D->d_poff, D->d_prad,
                      D->d_pstride, s));
-  const bool want_arg = !R.mbe || P.ex.retain >= 2;
+  const bool want_arg = (!R.mbe && P.ex.retain >= 1) || P.ex.retain >= 2;
   for (size_t ti = 0; ti < nt; ti++) {
     const Task &t = P.tasks[ti];
     const Shard &sh = t.shard;
@@ -636,10 +636,16 @@ void solve(gbe_plan *gp, void *stream, bool mbe, gbe_value *opt, gbe_value *uppe
   RunImpl *R = run_create(gp, stream, mbe);
   try {
     if (opt) *opt = R->optimum;
-    std::vector<int32_t> a(std::max(gp->plan->prob->n, 1));
-    run_value(*R, a.data());
-    if (assign_out) std::memcpy(assign_out, a.data(), sizeof(int32_t) * gp->plan->prob->n);
-    if (upper) *upper = problem_evaluate(*gp->plan->prob, a.data());
+    // value-only solves (no assignment requested, e.g. "retain":"none" on the
+    // exact 20x20 grid whose argmins would need 1.27 TB) skip the value phase
+    if (assign_out || upper) {
+      if (!mbe && gp->plan->ex.retain < 1)
+        GBE_FAIL(GBE_E_INVALID, "an assignment needs the argmin tables (plan has \"retain\":\"none\")");
+      std::vector<int32_t> a(std::max(gp->plan->prob->n, 1));
+      run_value(*R, a.data());
+      if (assign_out) std::memcpy(assign_out, a.data(), sizeof(int32_t) * gp->plan->prob->n);
+      if (upper) *upper = problem_evaluate(*gp->plan->prob, a.data());
+    }
     copy_stats(*R, stats, cap);
   } catch (...) {
     delete R;

@@ -356,12 +356,12 @@ std::unique_ptr<Plan> make_plan(std::shared_ptr<const Problem> pp, const int32_t
     int64_t local = t.shard.on ? (t.shard.hi - t.shard.lo) : t.rows;
     int64_t full = t.shard.on && t.shard.gather ? t.shard.per * t.shard.block_rows * W : 0;
     msg_bytes[ti] = el * (local + full);
-    live += msg_bytes[ti] + local;  // message + argmin
+    const bool want_arg = (ibound < 0 && plan->ex.retain >= 1) || plan->ex.retain >= 2;
+    live += msg_bytes[ti] + (want_arg ? local : 0);  // message + argmin
     peak = std::max(peak, live);
     if (plan->ex.retain < 2 && ibound < 0)
       for (auto &m : t.members)
         if (m.kind == 1) live -= msg_bytes[m.index];
-    if (plan->ex.retain == 0) live -= local;
   }
   plan->peak_bytes = peak;
   if (ex.budget_bytes > 0 && peak > ex.budget_bytes) {

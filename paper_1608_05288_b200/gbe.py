@@ -236,13 +236,16 @@ class Plan:
                 _check(st)
             cap *= 4
 
-    def solve_be(self, stream=None, stats=False):
+    def solve_be(self, stream=None, stats=False, assignment=True):
+        """(optimum, assignment[, stats]); assignment=False runs a value-only
+        solve (no value phase; works with retain="none")."""
         v = Value()
         a = np.zeros(max(self.problem.n, 1), dtype=np.int32)
         cap = (1 << 22) if stats else 0
         buf = ctypes.create_string_buffer(cap) if stats else None
-        _check(lib().gbe_solve_be(self._h, _stream_ptr(stream), ctypes.byref(v), _ptr(a), buf, cap))
-        out = (_val(v, self.problem.is_f64), a[:self.problem.n])
+        _check(lib().gbe_solve_be(self._h, _stream_ptr(stream), ctypes.byref(v),
+                                  _ptr(a) if assignment else None, buf, cap))
+        out = (_val(v, self.problem.is_f64), a[:self.problem.n] if assignment else None)
         return out + (json.loads(buf.value.decode()),) if stats else out
 
     def solve_mbe(self, stream=None, stats=False):
