@@ -197,12 +197,12 @@ __device__ __forceinline__ void prefetch_tile(const FastDesc *__restrict__ Fg, c
 
 // cell (a, b, v) = P0[v] (+ P1[a][v]) (+ P2[b][v]) (+ P3[a][b][v]) with the
 // saturating adds of A9; min over v, first minimiser (A8); staged in smem.
-template <typename T, int R, int DV, bool H1, bool H2, bool H3>
+template <typename T, int R, int R2, int DV, bool H1, bool H2, bool H3>
 __device__ __forceinline__ void combine(const typename SrF<T>::Acc (&P0)[DV],
                                         const typename SrF<T>::Acc (&P1)[R][DV],
-                                        const typename SrF<T>::Acc (&P2)[R][DV],
-                                        const typename SrF<T>::Acc (&P3)[R][R][DV], T *outs,
-                                        uint8_t *args, const int (&loff)[R][R]) {
+                                        const typename SrF<T>::Acc (&P2)[R2][DV],
+                                        const typename SrF<T>::Acc (&P3)[R][R2][DV], T *outs,
+                                        uint8_t *args, const int (&loff)[R][R2]) {
   using S = SrF<T>;
   using Acc = typename S::Acc;
 #pragma unroll
@@ -211,7 +211,7 @@ __device__ __forceinline__ void combine(const typename SrF<T>::Acc (&P0)[DV],
 #pragma unroll
     for (int v = 0; v < DV; v++) Q[v] = H1 ? S::add(P0[v], P1[a][v]) : P0[v];
 #pragma unroll
-    for (int b = 0; b < R; b++) {
+    for (int b = 0; b < R2; b++) {
       // unclamped cell sums (int: <= 3 * 2^30 < 2^32); min over v, then one
       // clamp per row.  If the row minimum is infinite every value clamps to
       // INF and the first index wins (A8).
@@ -246,7 +246,7 @@ __device__ __forceinline__ void combine(const typename SrF<T>::Acc (&P0)[DV],
   }
 }
 
-template <typename T, int R, int DV>
+template <typename T, int R, int R2, int DV>
 __global__ void __launch_bounds__(kThreads) bk_fast_kernel(const FastDesc *__restrict__ Fg, InPtrs in,
                                                            T *__restrict__ out, uint8_t *__restrict__ arg,
                                                            int64_t row_begin, int64_t t_begin,
@@ -330,14 +330,14 @@ __global__ void __launch_bounds__(kThreads) bk_fast_kernel(const FastDesc *__res
     T *outs = (T *)(sm + f.off_out + b * f.out_bytes) + sh;
     uint8_t *args = sm + f.off_arg + b * f.arg_bytes + sha;
     const int c0 = f.cls_off[0], c1 = f.cls_off[1], c2 = f.cls_off[2], c3 = f.cls_off[3], c4 = f.cls_off[4];
-    int loff[R][R];  // in-tile row offsets of the group digits (tile-invariant)
+    int loff[R][R2];  // in-tile row offsets of the group digits (tile-invariant)
 #pragma unroll
     for (int a = 0; a < R; a++)
 #pragma unroll
-      for (int bb = 0; bb < R; bb++) loff[a][bb] = a * f.rs1 + bb * f.rs2;
+      for (int bb = 0; bb < R2; bb++) loff[a][bb] = a * f.rs1 + bb * f.rs2;
     const int sel = (c2 > c1 ? 1 : 0) | (c3 > c2 ? 2 : 0) | (c4 > c3 ? 4 : 0);
     for (int q = ctid; q < Pmid; q += 32 * kConsumerWarps) {
-      Acc P0[DV], P1[R][DV], P2[R][DV], P3[R][R][DV];
+      Acc P0[DV], P1[R][DV], P2[R2][DV], P3[R][R2][DV];
       // class 0 (no group digit): P0[v]
       if (c1 > c0) {
         const unsigned char *p = sm + sbase[s * 32 + c0] + offtab[c0 * Pmid + q];
@@ -374,14 +374,14 @@ __global__ void __launch_bounds__(kThreads) bk_fast_kernel(const FastDesc *__res
         const unsigned char *p = sm + sbase[s * 32 + c2] + offtab[c2 * Pmid + q];
         const int s2 = f.sg2[c2];
 #pragma unroll
-        for (int bb = 0; bb < R; bb++)
+        for (int bb = 0; bb < R2; bb++)
 #pragma unroll
           for (int v = 0; v < DV; v++) P2[bb][v] = (Acc)((const T *)(p + bb * s2))[v];
         for (int jj = c2 + 1; jj < c3; jj++) {
           const unsigned char *pj = sm + sbase[s * 32 + jj] + offtab[jj * Pmid + q];
           const int t2 = f.sg2[jj];
 #pragma unroll
-          for (int bb = 0; bb < R; bb++)
+          for (int bb = 0; bb < R2; bb++)
 #pragma unroll
             for (int v = 0; v < DV; v++) P2[bb][v] = S::add(P2[bb][v], (Acc)((const T *)(pj + bb * t2))[v]);
         }
@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(kThreads) bk_fast_kernel(const FastDesc *__res
 #pragma unroll
         for (int a = 0; a < R; a++)
 #pragma unroll
-          for (int bb = 0; bb < R; bb++)
+          for (int bb = 0; bb < R2; bb++)
 #pragma unroll
             for (int v = 0; v < DV; v++) P3[a][bb][v] = (Acc)((const T *)(p + a * s1 + bb * s2))[v];
         for (int jj = c3 + 1; jj < c4; jj++) {
@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(kThreads) bk_fast_kernel(const FastDesc *__res
 #pragma unroll
           for (int a = 0; a < R; a++)
 #pragma unroll
-            for (int bb = 0; bb < R; bb++)
+            for (int bb = 0; bb < R2; bb++)
 #pragma unroll
               for (int v = 0; v < DV; v++)
                 P3[a][bb][v] = S::add(P3[a][bb][v], (Acc)((const T *)(pj + a * t1 + bb * t2))[v]);
@@ -412,14 +412,14 @@ __global__ void __launch_bounds__(kThreads) bk_fast_kernel(const FastDesc *__res
       T *outq = outs + row0;
       uint8_t *argq = args + row0;
       switch (sel) {
-        case 0: combine<T, R, DV, false, false, false>(P0, P1, P2, P3, outq, argq, loff); break;
-        case 1: combine<T, R, DV, true, false, false>(P0, P1, P2, P3, outq, argq, loff); break;
-        case 2: combine<T, R, DV, false, true, false>(P0, P1, P2, P3, outq, argq, loff); break;
-        case 3: combine<T, R, DV, true, true, false>(P0, P1, P2, P3, outq, argq, loff); break;
-        case 4: combine<T, R, DV, false, false, true>(P0, P1, P2, P3, outq, argq, loff); break;
-        case 5: combine<T, R, DV, true, false, true>(P0, P1, P2, P3, outq, argq, loff); break;
-        case 6: combine<T, R, DV, false, true, true>(P0, P1, P2, P3, outq, argq, loff); break;
-        default: combine<T, R, DV, true, true, true>(P0, P1, P2, P3, outq, argq, loff); break;
+        case 0: combine<T, R, R2, DV, false, false, false>(P0, P1, P2, P3, outq, argq, loff); break;
+        case 1: combine<T, R, R2, DV, true, false, false>(P0, P1, P2, P3, outq, argq, loff); break;
+        case 2: combine<T, R, R2, DV, false, true, false>(P0, P1, P2, P3, outq, argq, loff); break;
+        case 3: combine<T, R, R2, DV, true, true, false>(P0, P1, P2, P3, outq, argq, loff); break;
+        case 4: combine<T, R, R2, DV, false, false, true>(P0, P1, P2, P3, outq, argq, loff); break;
+        case 5: combine<T, R, R2, DV, true, false, true>(P0, P1, P2, P3, outq, argq, loff); break;
+        case 6: combine<T, R, R2, DV, false, true, true>(P0, P1, P2, P3, outq, argq, loff); break;
+        default: combine<T, R, R2, DV, true, true, true>(P0, P1, P2, P3, outq, argq, loff); break;
       }
     }
     __syncwarp();
@@ -464,10 +464,10 @@ __global__ void __launch_bounds__(kThreads) bk_fast_kernel(const FastDesc *__res
 // ---------------------------------------------------------------------------
 // dispatch table over (semiring, R, DV)
 
-template <typename T, int R, int DV>
+template <typename T, int R, int R2, int DV>
 cudaError_t launch_one(const FastDesc *d, const InPtrs &in, void *out, uint8_t *arg, int64_t rb,
                        int64_t t0, int64_t t1, int grid, int block, int smem, cudaStream_t s) {
-  auto kern = bk_fast_kernel<T, R, DV>;
+  auto kern = bk_fast_kernel<T, R, R2, DV>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -478,22 +478,33 @@ cudaError_t launch_one(const FastDesc *d, const InPtrs &in, void *out, uint8_t *
 }
 
 template <typename T>
-cudaError_t dispatch(int R, int DV, const FastDesc *d, const InPtrs &in, void *out, uint8_t *arg,
-                     int64_t rb, int64_t t0, int64_t t1, int grid, int block, int smem,
-                     cudaStream_t s) {
-#define GBE_CASE(r, dv) \
-  if (R == r && DV == dv) return launch_one<T, r, dv>(d, in, out, arg, rb, t0, t1, grid, block, smem, s);
-  GBE_CASE(2, 2) GBE_CASE(2, 3) GBE_CASE(2, 4) GBE_CASE(2, 5) GBE_CASE(3, 2) GBE_CASE(3, 3)
-  if constexpr (sizeof(T) == 4) {  // f64 keeps R*R*DV <= 27 (register budget)
-    GBE_CASE(3, 4) GBE_CASE(3, 5) GBE_CASE(4, 2) GBE_CASE(4, 3)
+cudaError_t dispatch(int R, int R2, int DV, const FastDesc *d, const InPtrs &in, void *out,
+                     uint8_t *arg, int64_t rb, int64_t t0, int64_t t1, int grid, int block,
+                     int smem, cudaStream_t s) {
+#define GBE_CASE(r, r2, dv) \
+  if (R == r && R2 == r2 && DV == dv) return launch_one<T, r, r2, dv>(d, in, out, arg, rb, t0, t1, grid, block, smem, s);
+  GBE_CASE(2, 2, 2) GBE_CASE(2, 2, 3) GBE_CASE(2, 2, 4) GBE_CASE(2, 2, 5) GBE_CASE(3, 3, 2) GBE_CASE(3, 3, 3)
+  GBE_CASE(3, 1, 2) GBE_CASE(3, 1, 3) GBE_CASE(3, 1, 4) GBE_CASE(3, 1, 5)
+  GBE_CASE(4, 1, 2) GBE_CASE(4, 1, 3) GBE_CASE(4, 1, 4) GBE_CASE(4, 1, 5)
+  GBE_CASE(5, 1, 2) GBE_CASE(5, 1, 3) GBE_CASE(5, 1, 4)
+  if constexpr (sizeof(T) == 4) {  // f64 keeps R*R2*DV <= 27 (register budget)
+    GBE_CASE(3, 3, 4) GBE_CASE(3, 3, 5) GBE_CASE(4, 4, 2) GBE_CASE(4, 4, 3) GBE_CASE(5, 1, 5)
   }
 #undef GBE_CASE
   return cudaErrorInvalidValue;
 }
 
-bool supported(int R, int DV) {
-  if (R == 2 || R == 3) return DV >= 2 && DV <= 5;
-  if (R == 4) return DV == 2 || DV == 3;
+bool supported(int R, int R2, int DV, int es) {
+  if (DV < 2 || DV > 5) return false;
+  if (R2 == R) {
+    if (R == 2) return true;
+    if (R == 3) return DV <= 3 || es == 4;
+    if (R == 4) return DV <= 3 && es == 4;
+    return false;
+  }
+  if (R2 != 1) return false;
+  if (R >= 3 && R <= 4) return true;
+  if (R == 5) return DV <= 4 || es == 4;
   return false;
 }
 
@@ -525,14 +536,15 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     int64_t PL = 1;
     for (int p = m - nl; p < m; p++) PL *= h.radix[p];
     if (PL > kPLMax) continue;
-    // group digits: best pair with equal supported radix
+    // group digits: the pair (equal radix) or single digit with a supported
+    // register-blocking shape that minimises the per-cell shared-memory
+    // loads sum_j R^-|G \ S_j|; pairs win ties (more reuse per group)
     double bestc = 1e30;
     int g1 = -1, g2 = -1;
     for (int a = m - nl; a < m; a++)
       for (int b = a + 1; b < m; b++) {
         int R = h.radix[a];
-        if (h.radix[b] != R || !supported(R, DV)) continue;
-        if (es == 8 && R * R * DV > 27) continue;  // f64 register budget
+        if (h.radix[b] != R || !supported(R, R, DV, es)) continue;
         double c = 0;
         for (int j = 0; j < k; j++) c += 1.0 / ((has(j, a) ? 1 : R) * (has(j, b) ? 1 : R));
         if (c < bestc - 1e-12 || (c < bestc + 1e-12 && b > g2)) {
@@ -541,9 +553,21 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
           g2 = b;
         }
       }
+    if (g1 < 0)
+      for (int a = m - nl; a < m; a++) {
+        int R = h.radix[a];
+        if (!supported(R, 1, DV, es)) continue;
+        double c = 0;
+        for (int j = 0; j < k; j++) c += 1.0 / (has(j, a) ? 1 : R);
+        if (c < bestc - 1e-12 || (c < bestc + 1e-12 && a > g1)) {
+          bestc = c;
+          g1 = a;
+        }
+      }
     if (g1 < 0) continue;
     const int R = h.radix[g1];
-    const int64_t Pmid = PL / (R * R);
+    const int R2 = g2 >= 0 ? R : 1;
+    const int64_t Pmid = PL / (R * R2);
     if (row_begin % PL || row_end % PL) continue;
     // classes
     std::memset(&F, 0, sizeof(F));
@@ -558,11 +582,11 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     for (int c = 0; c < 4; c++) {
       f.cls_off[c] = jj;
       for (int j = 0; j < k; j++) {
-        int cls = (has(j, g1) ? 1 : 0) + (has(j, g2) ? 2 : 0);
+        int cls = (has(j, g1) ? 1 : 0) + (g2 >= 0 && has(j, g2) ? 2 : 0);
         if (cls != c) continue;
         f.in_idx[jj] = j;
         f.sg1[jj] = (int32_t)(h.stride[j][g1] * es);  // bytes
-        f.sg2[jj] = (int32_t)(h.stride[j][g2] * es);
+        f.sg2[jj] = g2 >= 0 ? (int32_t)(h.stride[j][g2] * es) : 0;
         int64_t sl = DV;
         for (int p = m - nl; p < m; p++)
           if (has(j, p)) sl *= h.radix[p];
@@ -588,7 +612,7 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
       for (int q = 0; q < k; q++) f.mstr[e][q] = (int32_t)h.stride[f.in_idx[q]][p];
     }
     f.rs1 = (int32_t)rowstride[g1];
-    f.rs2 = (int32_t)rowstride[g2];
+    f.rs2 = g2 >= 0 ? (int32_t)rowstride[g2] : 0;
     // H digits: natural order; for a full-range launch, digits absent from
     // the largest input go last (fastest) so their re-reads hit L2
     std::vector<int> hd;
@@ -644,6 +668,7 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     int64_t tiles = L.t_end - L.t_begin;
     L.grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms * per_sm));
     L.R = R;
+    L.R2 = R2;
     L.DV = DV;
     L.es = es;
     return true;
@@ -654,9 +679,9 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
 cudaError_t bkf_launch(const FastDesc *dev_f, const BkfLaunch &L, const InPtrs &in, void *out,
                        uint8_t *arg, int64_t row_begin, cudaStream_t s) {
   if (L.es == 8)
-    return dispatch<double>(L.R, L.DV, dev_f, in, out, arg, row_begin, L.t_begin, L.t_end, L.grid,
+    return dispatch<double>(L.R, L.R2, L.DV, dev_f, in, out, arg, row_begin, L.t_begin, L.t_end, L.grid,
                             L.block, L.smem, s);
-  return dispatch<int32_t>(L.R, L.DV, dev_f, in, out, arg, row_begin, L.t_begin, L.t_end, L.grid,
+  return dispatch<int32_t>(L.R, L.R2, L.DV, dev_f, in, out, arg, row_begin, L.t_begin, L.t_end, L.grid,
                            L.block, L.smem, s);
 }
 

@@ -10,7 +10,7 @@ namespace gbe {
 
 // Fields every CTA copies into shared memory (all int32).
 struct FastHot {
-  int32_t k, es, PL, Pmid, R, DV, nmid, nH;
+  int32_t k, es, PL, Pmid, R, DV, nmid, nH;  // R: radix of g1 (g2 has R or is absent)
   int32_t cls_off[5];    // input class ranges: none / g1 / g2 / both
   int32_t in_idx[32];    // class-ordered input -> original input
   int32_t sg1[32], sg2[32];  // byte strides of the group digits (0 if absent)
@@ -35,7 +35,7 @@ struct FastDesc {
 };
 
 struct BkfLaunch {
-  int R = 0, DV = 0, es = 4;
+  int R = 0, R2 = 0, DV = 0, es = 4;
   int grid = 1, block = 256, smem = 0;
   int64_t t_begin = 0, t_end = 0;
 };

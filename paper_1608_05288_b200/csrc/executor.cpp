@@ -95,8 +95,15 @@ struct DevPlan {
     std::vector<size_t> off_out, off_full, off_arg;
     void *mem = nullptr;
     bool busy = false, hook = false;
+    void *vprog = nullptr;  // cached value-phase program (device)
+    int vsteps = 0;
+    size_t b_steps = 0, b_mems = 0;
+    std::vector<char> vsharded;
   } arena[2];
   ~DevPlan() {
+    for (auto &a : arena) {
+      if (a.vprog) cudaFree(a.vprog);
+    }
     for (auto &a : arena)
       if (a.mem) {
         if (a.hook && g_free) g_free(a.mem, g_alloc_u);
@@ -345,7 +352,8 @@ static void run_util(RunImpl &R) {
   const size_t nt = P.tasks.size();
 
   // pre-flight memory budget: plan estimate vs what the device has
-  {
+  // (once: later runs reuse the plan's arena)
+  if (!D->arena[R.mbe ? 1 : 0].mem) {
     size_t fr = 0, tot = 0;
     CK(cudaMemGetInfo(&fr, &tot));
     uint64_t reserved = 0, used = 0;
@@ -461,12 +469,59 @@ static void run_util(RunImpl &R) {
   R.util_done = true;
 }
 
+struct VProg {
+  VStep *steps;
+  VMember *mems;
+  VTerm *terms;
+};
+
+// launch the value kernel over the program, exchanging sharded lookups
+static void run_value_steps(RunImpl &R, const VProg &pg, int nsteps, const std::vector<char> &sharded,
+                            int32_t *assign_out) {
+  const Plan &P = *R.gp->plan;
+  const Problem &p = *P.prob;
+  cudaStream_t s = R.stream;
+  const int W = P.ex.world_size;
+  if (W > 1 && !R.d_gbuf) R.d_gbuf = (int32_t *)dalloc(sizeof(int32_t) * W, s);
+  // segments end at row-sharded steps: the owner's lookup is exchanged
+  int s0 = 0, gvar = -1;
+  for (int i = 0; i < nsteps; i++) {
+    if (!(W > 1 && sharded[i])) continue;
+    CK(value_launch(p.is_f64(), pg.steps, s0, i + 1, pg.mems, pg.terms, R.d_assign, R.d_gbuf, gvar,
+                    W, nullptr, -1, nullptr, s));
+    if (!g_ag) GBE_FAIL(GBE_E_COMM, "sharded value phase needs the all-gather hook");
+    int var = P.order[i];
+    if (g_ag(R.d_assign + var, R.d_gbuf, sizeof(int32_t), (void *)s, g_ag_u) != 0)
+      GBE_FAIL(GBE_E_COMM, "all-gather of the value of x%d failed", var);
+    gvar = var;
+    s0 = i + 1;
+  }
+  CK(value_launch(p.is_f64(), pg.steps, s0, nsteps, pg.mems, pg.terms, R.d_assign, R.d_gbuf, gvar, W,
+                  nullptr, -1, nullptr, s));
+  CK(cudaMemcpyAsync(assign_out, R.d_assign, sizeof(int32_t) * p.n, cudaMemcpyDeviceToHost, s));
+}
+
+static void run_value_program(RunImpl &R, void *buf, int nsteps, const std::vector<char> &sharded,
+                              int32_t *assign_out) {
+  DevPlan::Arena *A = R.A;
+  VProg pg{(VStep *)buf, (VMember *)((char *)buf + A->b_steps),
+           (VTerm *)((char *)buf + A->b_steps + A->b_mems)};
+  run_value_steps(R, pg, nsteps, sharded, assign_out);
+  CK(cudaStreamSynchronize(R.stream));
+}
+
 // VALUE / assignment phase (Alg. 1 lines 6-7)
 static void run_value(RunImpl &R, int32_t *assign_out) {
   const Plan &P = *R.gp->plan;
   const Problem &p = *P.prob;
   cudaStream_t s = R.stream;
-  const int W = P.ex.world_size;
+  // the program depends only on the plan and the arena addresses: a run on
+  // the plan's cached arena reuses the device copy built by the first run
+  DevPlan::Arena *A = R.arena_own ? nullptr : R.A;
+  if (A && A->vprog) {
+    run_value_program(R, A->vprog, A->vsteps, A->vsharded, assign_out);
+    return;
+  }
   std::vector<VStep> steps;
   std::vector<VMember> mems;
   std::vector<VTerm> terms;
@@ -527,30 +582,28 @@ static void run_value(RunImpl &R, int32_t *assign_out) {
   size_t b_steps = sizeof(VStep) * std::max<size_t>(steps.size(), 1);
   size_t b_mems = sizeof(VMember) * std::max<size_t>(mems.size(), 1);
   size_t b_terms = sizeof(VTerm) * std::max<size_t>(terms.size(), 1);
-  char *buf = (char *)dalloc(b_steps + b_mems + b_terms, s);
+  char *buf = nullptr;
+  if (A) {
+    CK(cudaMalloc(&buf, b_steps + b_mems + b_terms));
+  } else {
+    buf = (char *)dalloc(b_steps + b_mems + b_terms, s);
+  }
   VStep *d_steps = (VStep *)buf;
   VMember *d_mems = (VMember *)(buf + b_steps);
   VTerm *d_terms = (VTerm *)(buf + b_steps + b_mems);
   if (!steps.empty()) CK(cudaMemcpyAsync(d_steps, steps.data(), sizeof(VStep) * steps.size(), cudaMemcpyHostToDevice, s));
   if (!mems.empty()) CK(cudaMemcpyAsync(d_mems, mems.data(), sizeof(VMember) * mems.size(), cudaMemcpyHostToDevice, s));
   if (!terms.empty()) CK(cudaMemcpyAsync(d_terms, terms.data(), sizeof(VTerm) * terms.size(), cudaMemcpyHostToDevice, s));
-  if (W > 1 && !R.d_gbuf) R.d_gbuf = (int32_t *)dalloc(sizeof(int32_t) * W, s);
-  // segments end at row-sharded steps: the owner's lookup is exchanged
-  int s0 = 0, gvar = -1;
-  for (int i = 0; i < (int)steps.size(); i++) {
-    if (!(W > 1 && sharded[i])) continue;
-    CK(value_launch(p.is_f64(), d_steps, s0, i + 1, d_mems, d_terms, R.d_assign, R.d_gbuf, gvar,
-                    W, nullptr, -1, nullptr, s));
-    if (!g_ag) GBE_FAIL(GBE_E_COMM, "sharded value phase needs the all-gather hook");
-    if (g_ag(R.d_assign + steps[i].var, R.d_gbuf, sizeof(int32_t), (void *)s, g_ag_u) != 0)
-      GBE_FAIL(GBE_E_COMM, "all-gather of the value of x%d failed", steps[i].var);
-    gvar = steps[i].var;
-    s0 = i + 1;
+  if (A) {
+    A->vprog = buf;
+    A->vsteps = (int)steps.size();
+    A->vsharded = sharded;
+    A->b_steps = b_steps;
+    A->b_mems = b_mems;
   }
-  CK(value_launch(p.is_f64(), d_steps, s0, (int)steps.size(), d_mems, d_terms, R.d_assign,
-                  R.d_gbuf, gvar, W, nullptr, -1, nullptr, s));
-  CK(cudaMemcpyAsync(assign_out, R.d_assign, sizeof(int32_t) * p.n, cudaMemcpyDeviceToHost, s));
-  dfree(buf, s);
+  VProg prog{d_steps, d_mems, d_terms};
+  run_value_steps(R, prog, (int)steps.size(), sharded, assign_out);
+  if (!A) dfree(buf, s);
   CK(cudaStreamSynchronize(s));
 }
 

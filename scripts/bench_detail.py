@@ -6,13 +6,15 @@ import paper_1608_05288_b200 as G
 from gen import configs
 
 wl = sys.argv[1] if len(sys.argv) > 1 else "c4"
-inst = {"c4": configs.c4, "c2": configs.c2, "c4alt": lambda: configs.c4(seed=configs.C4_ALT_SEED)}[wl]()
+ib = int(sys.argv[2]) if len(sys.argv) > 2 else -1
+inst = {"c4": configs.c4, "c2": configs.c2, "c5": configs.c5, "c3": configs.c3,
+        "c4alt": lambda: configs.c4(seed=configs.C4_ALT_SEED)}[wl]()
 P = G.Problem.from_instance(inst)
-order, w = P.order()
-info = G.Plan(P, order).info()
+order = configs.c3_order() if wl == "c3" else P.order()[0]
+info = G.Plan(P, order, ib).info()
 for label, opts in [("resident", dict(resident_inputs=True, timing=True)), ("e2e", dict(timing=True)),
                     ("e2e-notiming", dict())]:
-    plan = G.Plan(P, order, **opts)
+    plan = G.Plan(P, order, ib, **opts)
     for _ in range(3):
         run, root = plan.dpop_util(); run.value(); run.close()
     s = torch.cuda.current_stream()

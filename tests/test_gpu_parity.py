@@ -278,7 +278,8 @@ def test_mpe_bn_small_against_brute_force(torch_cuda):
 
 # ---------------------------------------------------------------- tiled TMA kernel
 
-FAST_SHAPES = [(2, 2), (2, 3), (2, 4), (2, 5), (3, 2), (3, 3), (3, 4), (3, 5), (4, 2), (4, 3)]
+FAST_SHAPES = [(2, 2), (2, 3), (2, 4), (2, 5), (3, 2), (3, 3), (3, 4), (3, 5), (4, 2), (4, 3), (4, 4),
+               (4, 5), (5, 2), (5, 3), (5, 4), (5, 5)]
 
 
 def uniform_bucket(rng, R, DV, m, k, f64):
@@ -303,12 +304,12 @@ def uniform_bucket(rng, R, DV, m, k, f64):
 @pytest.mark.parametrize("f64", [False, True])
 def test_fast_kernel_shapes(torch_cuda, R, DV, f64):
     rng = np.random.default_rng(R * 100 + DV * 10 + int(f64))
-    m = {2: 13, 3: 9, 4: 7}[R]
+    m = {2: 13, 3: 9, 4: 7, 5: 6}[R]
     for trial in range(3):
         k = int(rng.integers(1, 12))
         dom, sep, x, members = uniform_bucket(rng, R, DV, m, k, f64)
         D, rows = desc_for(dom, sep, x, members, f64)
-        if f64 and R * R * DV > 27:
+        if f64 and R == 5 and DV == 5:  # no f64 shape fits the register budget
             assert G.bucket_kernel_variant(D, 0, rows) == 0
             continue
         assert G.bucket_kernel_variant(D, 0, rows) == 1
