@@ -162,7 +162,10 @@ gbe_status gbe_solve_be(gbe_plan *plan, void *stream, gbe_value *opt, int32_t *a
                         char *stats_json, size_t cap);
 
 /* MBE(i) (Alg. 2): lower = sum of constants; upper = evaluate(assignment);
- * the value phase minimises the sum of all mini-bucket functions (A7). */
+ * the value phase minimises the sum of all mini-bucket functions (A7), so the
+ * messages are retained until it runs.  upper = assign_out = NULL gives the
+ * lower bound only; with "retain":"none" messages are then freed once
+ * consumed (e.g. the 20x20 grid at i = 18, whose messages total ~0.5 TB). */
 gbe_status gbe_solve_mbe(gbe_plan *plan, void *stream, gbe_value *lower, gbe_value *upper,
                          int32_t *assign_out, char *stats_json, size_t cap);
 

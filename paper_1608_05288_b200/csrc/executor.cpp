@@ -187,7 +187,7 @@ static void plan_arena(const Plan &P, DevPlan *D, bool mbe_mode) {
       fl.release(A.off_out[ti], out_b[ti]);
       out_b[ti] = 0;
     }
-    if (!mbe_mode && P.ex.retain < 2)
+    if ((!mbe_mode || P.ex.retain == 0) && P.ex.retain < 2)
       for (auto &m : t.members)
         if (m.kind == 1) {
           if (out_b[m.index]) fl.release(A.off_out[m.index], out_b[m.index]);
@@ -446,7 +446,7 @@ static void run_util(RunImpl &R) {
       R.out[ti] = nullptr;
     }
     // consumed messages are dead (BE/DPOP; MBE keeps them for its value phase, A7)
-    if (!R.mbe && P.ex.retain < 2)
+    if ((!R.mbe || P.ex.retain == 0) && P.ex.retain < 2)
       for (auto &m : t.members)
         if (m.kind == 1) R.out[m.index] = R.full[m.index] = nullptr;
   }
@@ -692,8 +692,8 @@ void solve(gbe_plan *gp, void *stream, bool mbe, gbe_value *opt, gbe_value *uppe
     // value-only solves (no assignment requested, e.g. "retain":"none" on the
     // exact 20x20 grid whose argmins would need 1.27 TB) skip the value phase
     if (assign_out || upper) {
-      if (!mbe && gp->plan->ex.retain < 1)
-        GBE_FAIL(GBE_E_INVALID, "an assignment needs the argmin tables (plan has \"retain\":\"none\")");
+      if (gp->plan->ex.retain < 1)
+        GBE_FAIL(GBE_E_INVALID, "an assignment needs the argmin tables / retained messages (plan has \"retain\":\"none\")");
       std::vector<int32_t> a(std::max(gp->plan->prob->n, 1));
       run_value(*R, a.data());
       if (assign_out) std::memcpy(assign_out, a.data(), sizeof(int32_t) * gp->plan->prob->n);

@@ -359,7 +359,7 @@ std::unique_ptr<Plan> make_plan(std::shared_ptr<const Problem> pp, const int32_t
     const bool want_arg = (ibound < 0 && plan->ex.retain >= 1) || plan->ex.retain >= 2;
     live += msg_bytes[ti] + (want_arg ? local : 0);  // message + argmin
     peak = std::max(peak, live);
-    if (plan->ex.retain < 2 && ibound < 0)
+    if (plan->ex.retain < 2 && (ibound < 0 || plan->ex.retain == 0))
       for (auto &m : t.members)
         if (m.kind == 1) live -= msg_bytes[m.index];
   }

@@ -248,15 +248,18 @@ class Plan:
         out = (_val(v, self.problem.is_f64), a[:self.problem.n] if assignment else None)
         return out + (json.loads(buf.value.decode()),) if stats else out
 
-    def solve_mbe(self, stream=None, stats=False):
+    def solve_mbe(self, stream=None, stats=False, assignment=True):
+        """(lower, upper, assignment[, stats]); assignment=False: lower bound
+        only (no value phase; messages freed once consumed with retain="none")."""
         lo, up = Value(), Value()
         a = np.zeros(max(self.problem.n, 1), dtype=np.int32)
         cap = (1 << 22) if stats else 0
         buf = ctypes.create_string_buffer(cap) if stats else None
-        _check(lib().gbe_solve_mbe(self._h, _stream_ptr(stream), ctypes.byref(lo), ctypes.byref(up),
-                                   _ptr(a), buf, cap))
+        _check(lib().gbe_solve_mbe(self._h, _stream_ptr(stream), ctypes.byref(lo),
+                                   ctypes.byref(up) if assignment else None,
+                                   _ptr(a) if assignment else None, buf, cap))
         f = self.problem.is_f64
-        out = (_val(lo, f), _val(up, f), a[:self.problem.n])
+        out = (_val(lo, f), _val(up, f) if assignment else None, a[:self.problem.n] if assignment else None)
         return out + (json.loads(buf.value.decode()),) if stats else out
 
     def dpop_util(self, stream=None):

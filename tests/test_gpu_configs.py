@@ -6,8 +6,9 @@ oracle/ and gen/) and against properties that hold at any size (-m gpu).
   (out, argmin) equals the oracle's; optimum equal; evaluate(assignment) =
   optimum (C2: assignment equal).
 * C3 (20x20 grid, row-major): MBE i = 8..16 lower bounds and table digests
-  equal (i <= 14: upper bound and assignment equal); i = 18 and the exact
-  value (value-only solve, argmins would need 1.27 TB) satisfy
+  equal (i <= 14: upper bound and assignment equal); the i = 18 lower bound
+  (value-only: its retained messages would total ~0.5 TB) and the exact value
+  (value-only: its argmins would need 1.27 TB) satisfy
   lower(i) <= exact <= upper(i) (P:308-316).
 * C5 (BN MPE, f64): exact and MBE i=16 optima within 1e-9 relative, per-table
   sum / min / max of finite entries within 1e-9, infinite counts equal.
@@ -100,12 +101,14 @@ def test_c3_grid_mbe_sweep_and_exact():
         lo2, up2, a2 = G.Plan(P, order, ib).solve_mbe()
         assert (lo2, up2) == (lo, up) and list(a2) == list(a)
         bounds[ib] = (lo, up)
-    lo18, up18, _ = G.Plan(P, order, 18).solve_mbe()
-    bounds[18] = (lo18, up18)
+    # i = 18: its retained messages would total ~0.5 TB, so lower bound only
+    # (value-only MBE frees each message once consumed)
+    lo18, _, _ = G.Plan(P, order, 18, retain="none").solve_mbe(assignment=False)
     exact, _ = G.Plan(P, order, retain="none").solve_be(assignment=False)
+    assert lo18 <= exact
     for ib, (lo, up) in bounds.items():
         assert lo <= exact <= up, (ib, lo, exact, up)
-    assert bounds[18][0] >= bounds[8][0]
+    assert lo18 >= bounds[8][0]
 
 
 def test_c5_bn_mpe_exact_and_mbe16():
