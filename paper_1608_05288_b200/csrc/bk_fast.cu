@@ -39,6 +39,7 @@ namespace {
 constexpr uint32_t kInf = GBE_INF_I32;
 constexpr int kMaxStages = 4;
 constexpr int kOutBufs = 3;
+constexpr int64_t kMinCells = 1 << 10;  // measured: the tiled kernel beats bk_generic from ~1e3 cells
 constexpr int kPrefetch = 0;  // tiles ahead (per CTA) prefetched into L2 (0 = off: measured slower)
 constexpr int kConsumerWarps = 8;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
@@ -520,6 +521,9 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
   const int es = h.semiring == GBE_MINSUM_F64 ? 8 : 4;
   if (m < 2 || k < 1 || k > 32 || DV < 2 || DV > 5) return false;
   if (row_end <= row_begin) return false;
+  // tiny buckets: the tiled kernel's per-CTA setup (descriptor copy, offset
+  // tables, mbarrier ring) costs more than the bucket; bk_generic is faster
+  if ((row_end - row_begin) * DV < kMinCells) return false;
   const int64_t kPLMax = 16384;
   const size_t kSmemMax = 112 * 1024;
   // inputs' sizes (cells) to find the largest

@@ -46,6 +46,7 @@ ExecOptions parse_exec(const char *json) {
   ex.timing = j.b("timing", false);
   ex.kernel = (int)j.i("kernel", -1);
   ex.resident_inputs = j.b("resident_inputs", false);
+  ex.graph = j.b("graph", true);
   return ex;
 }
 
