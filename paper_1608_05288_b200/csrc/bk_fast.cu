@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -525,7 +526,16 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
   // tables, mbarrier ring) costs more than the bucket; bk_generic is faster
   if ((row_end - row_begin) * DV < kMinCells) return false;
   const int64_t kPLMax = 16384;
-  const size_t kSmemMax = 112 * 1024;
+  // shared-memory budget per CTA (2 CTAs/SM by default); GBE_FAST_SMEM_KB
+  // overrides it for tuning experiments
+  static const size_t kSmemMax = [] {
+    const char *e = std::getenv("GBE_FAST_SMEM_KB");
+    return (size_t)(e ? std::atoi(e) : 112) * 1024;
+  }();
+  static const int kStagesMax = [] {
+    const char *e = std::getenv("GBE_FAST_STAGES");
+    return e ? std::max(2, std::min(kMaxStages, std::atoi(e))) : kMaxStages;
+  }();
   // inputs' sizes (cells) to find the largest
   auto has = [&](int j, int p) { return h.stride[j][p] != 0; };
   std::vector<int64_t> cells(k, DV);
@@ -649,8 +659,8 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     f.arg_bytes = (int32_t)(((size_t)PL + 16 + 127) & ~size_t(127));
     size_t fixed = kOutBufs * ((size_t)f.out_bytes + f.arg_bytes) + (size_t)(k + 1) * Pmid * 4 + 256;
     // 2 CTAs per SM when possible (~110 KB each), 2..4 input stages
-    int nst = kMaxStages;
-    while (nst > 2 && fixed + nst * off > 112 * 1024) nst--;
+    int nst = kStagesMax;
+    while (nst > 2 && fixed + nst * off > kSmemMax) nst--;
     f.nstages = nst;
     off = nst * off;
     f.off_out = (int32_t)off;

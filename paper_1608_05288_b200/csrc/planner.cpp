@@ -308,20 +308,50 @@ std::unique_ptr<Plan> make_plan(std::shared_ptr<const Problem> pp, const int32_t
     plan->total_bytes += el * t.in_cells + el * t.rows + t.rows;
   }
 
-  // row-shard plan: only tasks with >= shard_min_rows rows
+  // row-shard plan: only tasks with >= shard_min_rows rows.
+  // Key = the leading output digits; the default key is the shortest prefix
+  // with >= 8*W blocks (>= ~90 % balance).  Then, walking from the root side,
+  // a producer adopts its consumer's key whenever the consumer's key variables
+  // are also the leading variables of the producer's separator (same blocks),
+  // so messages along a chain of big buckets never need an all-gather.
   const int W = ex.world_size;
-  for (auto &t : plan->tasks) {
+  const int nt = (int)plan->tasks.size();
+  std::vector<int> kd(nt, 0);
+  auto blocks_of = [&](const Task &t, int k) {
+    int64_t b = 1;
+    for (int q = 0; q < k; q++) b *= p.dom[t.sep[q]];
+    return b;
+  };
+  for (int ti = 0; ti < nt; ti++) {
+    Task &t = plan->tasks[ti];
+    if (W <= 1 || t.rows < ex.shard_min_rows || t.sep.empty()) continue;
+    int k = 0;
+    while (k < (int)t.sep.size() && blocks_of(t, k) < 8LL * W) k++;  // >= ~90 % balance
+    if (blocks_of(t, k) < W) continue;
+    kd[ti] = k;
+  }
+  for (int ti = nt - 1; ti >= 0; ti--) {
+    const Task &t = plan->tasks[ti];
+    if (!kd[ti]) continue;
+    for (auto &m : t.members) {
+      if (m.kind != 1 || !kd[m.index]) continue;
+      const Task &pr = plan->tasks[m.index];
+      if (kd[ti] > (int)pr.sep.size()) continue;
+      bool same = true;
+      for (int q = 0; same && q < kd[ti]; q++) same = pr.sep[q] == t.sep[q];
+      if (same) kd[m.index] = kd[ti];
+    }
+  }
+  for (int ti = 0; ti < nt; ti++) {
+    Task &t = plan->tasks[ti];
     Shard &s = t.shard;
     s = Shard{};
     s.lo = 0;
     s.hi = t.rows;
-    if (W <= 1 || t.rows < ex.shard_min_rows || t.sep.empty()) continue;
-    int64_t blocks = 1;
-    int kd = 0;
-    while (kd < (int)t.sep.size() && blocks < 16LL * W) blocks *= p.dom[t.sep[kd++]];
-    if (blocks < W) continue;
+    if (!kd[ti]) continue;
+    int64_t blocks = blocks_of(t, kd[ti]);
     s.on = true;
-    s.key_digits = kd;
+    s.key_digits = kd[ti];
     s.blocks = blocks;
     s.block_rows = t.rows / blocks;
     s.per = (blocks + W - 1) / W;
