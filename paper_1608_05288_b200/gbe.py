@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgbe.so")
+LIB_PATH = os.environ.get("GBE_LIB") or os.path.join(_HERE, "libgbe.so")  # GBE_LIB: A/B builds
 
 INF_I32 = 1 << 30
 MAX_SEP = 40
