@@ -138,3 +138,15 @@ def test_sharded_dpop_two_ranks_one_gpu(tmp_path):
             np.testing.assert_array_equal(z[f"o{t}"], full[t][0][lo:hi], err_msg=f"rank {r} table {t}")
             np.testing.assert_array_equal(z[f"a{t}"], full[t][1][lo:hi], err_msg=f"rank {r} argmin {t}")
     assert sharded >= 4
+
+
+@pytest.mark.gpu
+def test_builtin_nccl_communicator_single_rank():
+    """The built-in NCCL transport loads (dlopen libnccl.so.2), creates a
+    communicator and tears it down (1 rank; the multi-GPU data path runs in
+    the driver's scaling step)."""
+    import paper_1608_05288_b200 as G
+    uid = G.comm_nccl_id()
+    assert len(uid) == 128
+    G.comm_nccl_init(uid, 1, 0, 0)
+    G.comm_finalize()
