@@ -568,7 +568,8 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     // loads sum_j R^-|G \ S_j|; pairs win ties (more reuse per group)
     double bestc = 1e30;
     int g1 = -1, g2 = -1;
-    for (int a = m - nl; a < m; a++)
+    static const bool single_only = std::getenv("GBE_FAST_SINGLE") != nullptr;  // tuning knob
+    for (int a = m - nl; a < m && !single_only; a++)
       for (int b = a + 1; b < m; b++) {
         int R = h.radix[a];
         if (h.radix[b] != R || !supported(R, R, DV, es)) continue;
