@@ -247,7 +247,7 @@ __device__ __forceinline__ void combine(const typename SrF<T>::Acc (&P0)[DV],
 }
 
 template <typename T, int R, int R2, int DV>
-__global__ void __launch_bounds__(kThreads) bk_fast_kernel(const FastDesc *__restrict__ Fg, InPtrs in,
+__global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && R * R2 * DV <= 27) ? 2 : 1) bk_fast_kernel(const FastDesc *__restrict__ Fg, InPtrs in,
                                                            T *__restrict__ out, uint8_t *__restrict__ arg,
                                                            int64_t row_begin, int64_t t_begin,
                                                            int64_t t_end) {
@@ -502,8 +502,9 @@ cudaError_t dispatch(int R, int R2, int DV, const FastDesc *d, const InPtrs &in,
   GBE_CASE(3, 1, 2) GBE_CASE(3, 1, 3) GBE_CASE(3, 1, 4) GBE_CASE(3, 1, 5)
   GBE_CASE(4, 1, 2) GBE_CASE(4, 1, 3) GBE_CASE(4, 1, 4) GBE_CASE(4, 1, 5)
   GBE_CASE(5, 1, 2) GBE_CASE(5, 1, 3) GBE_CASE(5, 1, 4)
-  if constexpr (sizeof(T) == 4) {  // f64 keeps R*R2*DV <= 27 (register budget)
-    GBE_CASE(3, 3, 4) GBE_CASE(3, 3, 5) GBE_CASE(4, 4, 2) GBE_CASE(4, 4, 3) GBE_CASE(5, 1, 5)
+  GBE_CASE(4, 4, 2)
+  if constexpr (sizeof(T) == 4) {  // f64 register budget (ptxas caps it at 168)
+    GBE_CASE(3, 3, 4) GBE_CASE(3, 3, 5) GBE_CASE(4, 4, 3) GBE_CASE(5, 1, 5)
   }
 #undef GBE_CASE
   return cudaErrorInvalidValue;
@@ -514,13 +515,12 @@ bool supported(int R, int R2, int DV, int es) {
   if (R2 == R) {
     if (R == 2) return true;
     if (R == 3) return DV <= 3 || es == 4;
-    if (R == 4) return DV <= 3 && es == 4;
+    if (R == 4) return DV == 2 || (DV == 3 && es == 4);
     return false;
   }
   if (R2 != 1) return false;
-  if (R >= 3 && R <= 4) return true;
-  if (R == 5) return DV <= 4 || es == 4;
-  return false;
+  if (R == 3 || R == 4) return true;
+  return R == 5 && (DV <= 4 || es == 4);
 }
 
 }  // namespace
