@@ -150,3 +150,52 @@ def test_builtin_nccl_communicator_single_rank():
     assert len(uid) == 128
     G.comm_nccl_init(uid, 1, 0, 0)
     G.comm_finalize()
+
+
+def _c4_worker(rank, world, port, out_dir):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+
+    import paper_1608_05288_b200 as G
+    from gen import configs
+    from paper_1608_05288_b200 import dist as gdist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    gdist.install(0, "gloo")
+    P = G.Problem.from_instance(configs.c4())
+    order, _ = P.order()
+    plan = G.Plan(P, order, world_size=world, rank=rank)  # bench.py's launch configuration
+    info = plan.info()
+    run, root = plan.dpop_util()
+    assign = run.value()
+    run.close()
+    np.savez(os.path.join(out_dir, f"c4rank{rank}.npz"), root=root, assign=assign,
+             nshard=sum(1 for t in info["tables"] if t["shard"]["on"]))
+    del plan
+    gdist.uninstall()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_c4_sharded_two_ranks_one_gpu(tmp_path):
+    """The bench workload (C4, largest UTIL table 3^20 rows) row-sharded over 2
+    ranks (sharing one GPU, host-staged all-gather): optimum and assignment
+    equal the oracle's golden optimum and the 1-GPU assignment."""
+    import json
+
+    import paper_1608_05288_b200 as G
+    from gen import configs
+    port = _free_port()
+    mp.start_processes(_c4_worker, args=(2, port, str(tmp_path)), nprocs=2, start_method="spawn")
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "c4.json")))
+    P = G.Problem.from_instance(configs.c4())
+    order, _ = P.order()
+    opt, assign = G.Plan(P, order).solve_be()
+    for r in range(2):
+        z = np.load(tmp_path / f"c4rank{r}.npz")
+        assert int(z["root"]) == g["value"] == opt
+        assert list(z["assign"]) == list(assign)
+        assert int(z["nshard"]) >= 5
