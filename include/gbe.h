@@ -139,8 +139,16 @@ gbe_status gbe_pseudotree(const gbe_problem *p, const int32_t *order,
  * generated function, |mini-bucket scope union| <= ibound + 1, reading A5;
  * greedy first-fit partition, reading A6).  json_exec (NULL ok):
  *   {"device":0, "budget_bytes":N, "world_size":W, "rank":r,
- *    "shard_min_rows":N, "retain":"none"|"args"|"all", "timing":true}
+ *    "shard_min_rows":N, "retain":"none"|"args"|"all", "timing":true,
+ *    "kernel":-1|0|1, "resident_inputs":false, "graph":true, "concurrent":true}
  * "retain":"all" keeps every table on the device for gbe_run_table().
+ * "kernel" forces the generic (0) or tiled (1) bucket kernel (-1 = auto).
+ * "resident_inputs" keeps the uploaded tables on the device between solves.
+ * "graph" replays the UTIL phase as a CUDA graph from the second solve on
+ * (1 GPU); "concurrent" makes that graph the task DAG (a bucket waits only on
+ * its producers and on earlier users of the arena ranges it reuses), so
+ * sibling subtrees run concurrently.  "timing" serialises the
+ * buckets (per-launch events).
  * Errors: GBE_E_INVALID (bad order, i-bound < member arity - 1),
  * GBE_E_BUDGET (names the bucket and its rows). */
 gbe_status gbe_plan_create(const gbe_problem *p, const int32_t *order, int32_t ibound,

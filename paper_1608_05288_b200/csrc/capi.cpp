@@ -47,6 +47,7 @@ ExecOptions parse_exec(const char *json) {
   ex.kernel = (int)j.i("kernel", -1);
   ex.resident_inputs = j.b("resident_inputs", false);
   ex.graph = j.b("graph", true);
+  ex.concurrent = j.b("concurrent", true);
   return ex;
 }
 

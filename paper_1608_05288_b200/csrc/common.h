@@ -111,6 +111,7 @@ struct ExecOptions {
   int kernel = -1;             // -1 auto, else force a kernel variant
   bool resident_inputs = false; // keep the uploaded originals on the device between solves
   bool graph = true;            // replay the UTIL phase as a CUDA graph (1 GPU, cached arena)
+  bool concurrent = true;       // the graph is the task DAG: sibling subtrees overlap
 };
 
 struct Plan {

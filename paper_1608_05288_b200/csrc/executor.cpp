@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 
@@ -88,12 +89,17 @@ struct DevPlan {
   void *d_resident = nullptr;  // resident raw tables (resident_inputs)
   bool resident = false;
   cudaStream_t cap_stream = nullptr;  // CUDA-graph capture
+  std::vector<cudaStream_t> side;     // capture branches (concurrent subtrees)
+  std::vector<cudaEvent_t> tev;       // capture-internal task completion events
   // static memory plans (exact / MBE mode): every large buffer of a run at a
   // fixed offset of one arena allocation, reused by consecutive runs
   struct Arena {
     bool planned = false;
     size_t bytes = 0, off_raw = 0, off_sorted = 0;
     std::vector<size_t> off_out, off_full, off_arg;
+    // UTIL-phase DAG: deps[t] = tasks that must finish before task t starts
+    // (its producers and the last users of arena ranges it overwrites)
+    std::vector<std::vector<int32_t>> deps;
     void *mem = nullptr;
     bool busy = false, hook = false;
     void *vprog = nullptr;  // cached value-phase program (device)
@@ -117,6 +123,8 @@ struct DevPlan {
       for (auto e : a.ev) cudaEventDestroy(e);
     }
     if (cap_stream) cudaStreamDestroy(cap_stream);
+    for (auto st : side) cudaStreamDestroy(st);
+    for (auto e : tev) cudaEventDestroy(e);
     for (auto &a : arena)
       if (a.mem) {
         if (a.hook && g_free) g_free(a.mem, g_alloc_u);
@@ -186,6 +194,12 @@ static void plan_arena(const Plan &P, DevPlan *D, bool mbe_mode) {
   fl.release(A.off_raw, raw);  // raw tables are dead after the relayout
   const bool want_arg = (!mbe_mode && P.ex.retain >= 1) || P.ex.retain >= 2;
   std::vector<size_t> out_b(nt, 0), full_b(nt, 0);
+  // ranges[t]: the arena ranges task t writes; a later task overwriting any of
+  // them must wait for t and for t's consumer (the only reader of t's output)
+  std::vector<std::vector<std::pair<size_t, size_t>>> ranges(nt);
+  auto put = [&](size_t ti, size_t o, size_t b) {
+    ranges[ti].push_back({o, o + std::max<size_t>((b + 255) & ~size_t(255), 256)});
+  };
   for (size_t ti = 0; ti < nt; ti++) {
     const Task &t = P.tasks[ti];
     const Shard &sh = t.shard;
@@ -193,10 +207,15 @@ static void plan_arena(const Plan &P, DevPlan *D, bool mbe_mode) {
     int64_t cap = sh.on ? sh.per * sh.block_rows : t.rows;
     out_b[ti] = el * (size_t)cap;
     A.off_out[ti] = fl.alloc(out_b[ti]);
-    if (want_arg) A.off_arg[ti] = fl.alloc((size_t)std::max<int64_t>(local, 1));
+    put(ti, A.off_out[ti], out_b[ti]);
+    if (want_arg) {
+      A.off_arg[ti] = fl.alloc((size_t)std::max<int64_t>(local, 1));
+      put(ti, A.off_arg[ti], (size_t)std::max<int64_t>(local, 1));
+    }
     if (sh.on && sh.gather) {
       full_b[ti] = out_b[ti] * W;
       A.off_full[ti] = fl.alloc(full_b[ti]);
+      put(ti, A.off_full[ti], full_b[ti]);
       fl.release(A.off_out[ti], out_b[ti]);
       out_b[ti] = 0;
     }
@@ -209,6 +228,47 @@ static void plan_arena(const Plan &P, DevPlan *D, bool mbe_mode) {
         }
   }
   A.bytes = std::max<size_t>(fl.top, 256);
+  // the DAG of the UTIL phase (sibling subtrees are independent)
+  A.deps.assign(nt, {});
+  for (size_t ti = 0; ti < nt; ti++) {
+    std::vector<int32_t> &dp = A.deps[ti];
+    for (auto &m : P.tasks[ti].members)
+      if (m.kind == 1) dp.push_back(m.index);
+    for (size_t k = 0; k < ti; k++) {
+      bool hit = false;
+      for (auto &a : ranges[ti])
+        for (auto &b : ranges[k])
+          if (a.first < b.second && b.first < a.second) hit = true;
+      if (!hit) continue;
+      dp.push_back((int32_t)k);
+      int32_t c = P.tasks[k].consumer;
+      if (c >= 0 && (size_t)c < ti) dp.push_back(c);
+    }
+    std::sort(dp.begin(), dp.end());
+    dp.erase(std::unique(dp.begin(), dp.end()), dp.end());
+  }
+  // transitive reduction: drop an edge k -> t when another predecessor of t
+  // already descends from k (fewer cross-branch waits in the graph)
+  {
+    const size_t words = (nt + 63) / 64;
+    std::vector<uint64_t> anc(nt * words, 0);  // anc[t] = all ancestors of t
+    for (size_t ti = 0; ti < nt; ti++) {
+      uint64_t *a = &anc[ti * words];
+      for (int32_t k : A.deps[ti]) {
+        a[k >> 6] |= 1ull << (k & 63);
+        const uint64_t *b = &anc[(size_t)k * words];
+        for (size_t w = 0; w < words; w++) a[w] |= b[w];
+      }
+      std::vector<int32_t> keep;
+      for (int32_t k : A.deps[ti]) {
+        bool implied = false;
+        for (int32_t k2 : A.deps[ti])
+          if (k2 != k && (anc[(size_t)k2 * words + (k >> 6)] >> (k & 63) & 1)) implied = true;
+        if (!implied) keep.push_back(k);
+      }
+      A.deps[ti].swap(keep);
+    }
+  }
   A.planned = true;
 }
 
@@ -490,9 +550,48 @@ static void run_util(RunImpl &R) {
       CK(cudaMemcpyAsync(R.d_raw, D->h_raw, D->raw_bytes, cudaMemcpyHostToDevice, st));
     CK(relayout_launch(R.d_raw, R.d_sorted, (int)el, p.nf, D->d_off, D->d_poff, D->d_prad,
                        D->d_pstride, st));
+    // concurrent subtrees: inside a capture (and without per-launch timing)
+    // each task runs on a branch that waits only on its DAG predecessors;
+    // otherwise the tasks run in creation order on `st`
+    const bool dag = capturing && P.ex.concurrent && !P.ex.timing && nt > 1;
+    std::vector<int> last_on;   // last task enqueued on each branch
+    std::vector<int> branch_of(nt, -1);
+    if (dag) {
+      static const size_t kBranches = [] {
+        const char *e = std::getenv("GBE_BRANCHES");
+        return (size_t)std::max(1, e ? std::atoi(e) : 16);
+      }();
+      while (D->side.size() < kBranches) {
+        cudaStream_t b;
+        CK(cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking));
+        D->side.push_back(b);
+      }
+      while (D->tev.size() < nt + 1) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        D->tev.push_back(e);
+      }
+      CK(cudaEventRecord(D->tev[nt], st));  // fork after the relayout
+      last_on.assign(D->side.size(), -2);   // -2: branch not forked yet
+    }
+    size_t rr = 0;
     for (size_t ti = 0; ti < nt; ti++) {
       const Task &t = P.tasks[ti];
       const Shard &sh = t.shard;
+      cudaStream_t st0 = st;
+      if (dag) {
+        const std::vector<int32_t> &dp = A.deps[ti];
+        int b = -1;  // continue the branch whose last task is a predecessor
+        for (size_t q = 0; q < last_on.size() && b < 0; q++)
+          if (last_on[q] >= 0 && std::binary_search(dp.begin(), dp.end(), last_on[q])) b = (int)q;
+        if (b < 0) b = (int)(rr++ % last_on.size());
+        st = D->side[b];
+        if (last_on[b] == -2) CK(cudaStreamWaitEvent(st, D->tev[nt], 0));
+        for (int32_t k : dp)
+          if (branch_of[k] != b) CK(cudaStreamWaitEvent(st, D->tev[k], 0));
+        last_on[b] = (int)ti;
+        branch_of[ti] = b;
+      }
       void *out = gathered_src[ti] ? gathered_src[ti] : R.base + R.A->off_out[ti];
       uint8_t *argp = want_arg ? (uint8_t *)(R.base + R.A->off_arg[ti]) : nullptr;
       if (P.ex.timing) rec(ev[2 * ti]);
@@ -507,7 +606,14 @@ static void run_util(RunImpl &R) {
         if (g_ag(gathered_src[ti], R.base + R.A->off_full[ti], bytes, (void *)st, g_ag_u) != 0)
           GBE_FAIL(GBE_E_COMM, "all-gather of the message of x%d failed", t.var);
       }
+      if (dag) {
+        CK(cudaEventRecord(D->tev[ti], st));
+        st = st0;
+      }
     }
+    if (dag)  // join every branch before the constants
+      for (size_t q = 0; q < last_on.size(); q++)
+        if (last_on[q] >= 0) CK(cudaStreamWaitEvent(st, D->tev[last_on[q]], 0));
     // optimum / lower bound = sum of the constants
     void *cp = d_cp;
     if (!graph) {

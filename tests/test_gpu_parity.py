@@ -360,3 +360,58 @@ def test_fast_and_generic_kernels_agree_on_c4alt_buckets(torch_cuda):
         np.testing.assert_array_equal(oa, og)
         np.testing.assert_array_equal(aa, ag)
     assert list(ra.value()) == list(rg.value())
+
+
+@pytest.mark.parametrize("concurrent", [True, False])
+@pytest.mark.parametrize("name", ["scalefree", "grid6", "random_graph_p2", "bn", "c2"])
+def test_graph_replay_matches_oracle(torch_cuda, name, concurrent):
+    """From the second solve on the UTIL phase replays as a CUDA graph; with
+    "concurrent" that graph is the task DAG (sibling subtrees overlap, arena
+    ranges reused under DAG edges).  Every replay must equal the oracle: all
+    tables and argmins (retain all), optimum + assignment (retain args) and the
+    value-only optimum (retain none, maximum arena reuse)."""
+    inst = configs.c2() if name == "c2" else INSTANCES[name]()
+    P = G.Problem.from_instance(inst)
+    order, _ = P.order()
+    orun = oracle.solve_be(inst, order)
+
+    def same(v):
+        return math.isclose(v, orun.value, rel_tol=1e-9) if inst.is_f64 else v == orun.value
+
+    plan = G.Plan(P, order, retain="all", concurrent=concurrent)
+    info = plan.info()
+    for rep in range(3):
+        run, root = plan.dpop_util()
+        assert same(root), rep
+        if rep == 2:
+            _check_tables(run, info, orun, inst.is_f64)
+        run.close()
+    plan = G.Plan(P, order, concurrent=concurrent)
+    for rep in range(4):
+        opt, a = plan.solve_be()
+        assert same(opt), rep
+        if not inst.is_f64:
+            assert list(a) == list(orun.assignment), rep
+    plan = G.Plan(P, order, retain="none", concurrent=concurrent)
+    for rep in range(4):
+        opt, _ = plan.solve_be(assignment=False)
+        assert same(opt), rep
+
+
+@pytest.mark.parametrize("ib", [2, 4])
+def test_graph_replay_mbe(torch_cuda, ib):
+    """MBE plans replay too: lower/upper bounds and assignment stay equal to the
+    oracle's on every replay (messages retained for the value phase, A7)."""
+    inst = INSTANCES["grid6"]()
+    P = G.Problem.from_instance(inst)
+    order, _ = P.order()
+    orun = oracle.solve_mbe(inst, order, ib)
+    plan = G.Plan(P, order, ib)
+    for rep in range(4):
+        lo, up, a = plan.solve_mbe()
+        assert (lo, up) == (orun.value, orun.upper), rep
+        assert list(a) == list(orun.assignment), rep
+    plan = G.Plan(P, order, ib, retain="none")
+    for rep in range(4):
+        lo, _, _ = plan.solve_mbe(assignment=False)
+        assert lo == orun.value, rep
