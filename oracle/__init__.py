@@ -55,6 +55,11 @@ def lib():
                                      I32P, F64P, U8P, ctypes.c_int32]
         L.or_solve.argtypes = [PP, I32P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
         L.or_solve.restype = ctypes.c_void_p
+        L.or_bucket_rows_sp.argtypes = [I32P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                        I32P, I64P, I32P, ctypes.POINTER(F64P), ctypes.c_int32,
+                                        I32P, ctypes.c_int64, ctypes.c_int64, F64P, ctypes.c_int32]
+        L.or_solve_sumprod.argtypes = [PP, I32P, ctypes.c_int32, ctypes.c_int32]
+        L.or_solve_sumprod.restype = ctypes.c_void_p
         L.or_run_status.argtypes = [ctypes.c_void_p]
         L.or_run_status.restype = ctypes.c_int32
         L.or_run_ntables.argtypes = [ctypes.c_void_p]
@@ -203,6 +208,32 @@ def bucket_eval(dom, is_f64, x, members, sep, row_begin=0, row_end=None, nthread
     return out[:nrows], arg[:nrows]
 
 
+def bucket_eval_sp(dom, x, members, sep, row_begin=0, row_end=None, nthreads=0):
+    """Sum-product bucket (or_bucket_rows_sp): rows [row_begin, row_end) of
+    -log sum_x exp(-sum members); f64 members [(scope, table)]."""
+    dom = np.ascontiguousarray(dom, dtype=np.int32)
+    sep = [int(v) for v in sep]
+    if row_end is None:
+        row_end = int(np.prod([dom[v] for v in sep], dtype=np.int64)) if sep else 1
+    nm = len(members)
+    mar = np.array([len(s) for s, _ in members] + [0], dtype=np.int32)
+    moff = np.zeros(nm + 1, dtype=np.int64)
+    moff[1:] = np.cumsum(mar[:nm]) if nm else []
+    msc = np.array([int(v) for s, _ in members for v in s] + [0], dtype=np.int32)
+    tabs = [np.ascontiguousarray(t, dtype=np.float64) for _, t in members]
+    ft = (F64P * (nm + 1))()
+    for k, t in enumerate(tabs):
+        ft[k] = _p(t, ctypes.c_double)
+    sepa = np.array(sep + [0], dtype=np.int32)
+    nrows = row_end - row_begin
+    out = np.zeros(max(nrows, 1), dtype=np.float64)
+    lib().or_bucket_rows_sp(_p(dom, ctypes.c_int32), len(dom), int(x), nm, _p(mar, ctypes.c_int32),
+                            _p(moff, ctypes.c_int64), _p(msc, ctypes.c_int32), ft, len(sep),
+                            _p(sepa, ctypes.c_int32), row_begin, row_end, _p(out, ctypes.c_double),
+                            nthreads)
+    return out[:nrows]
+
+
 class Table:
     __slots__ = ("var", "mb", "sep", "rows", "dest", "members", "out", "arg", "digest")
 
@@ -211,15 +242,23 @@ class Run:
     """Result of or_solve: tables in creation order, optimum / bounds,
     assignment."""
 
-    def __init__(self, inst, order, ibound=-1, keep_tables=True, nthreads=0, table_fn=None):
+    def __init__(self, inst, order, ibound=-1, keep_tables=True, nthreads=0, table_fn=None,
+                 sumprod=False):
         """table_fn(t, table, out, arg), if given, receives each kept table
-        instead of the Run storing a copy (bounded memory for big runs)."""
+        instead of the Run storing a copy (bounded memory for big runs).
+        sumprod: exact BE in the sum-product semiring (f64; value = -log Z)."""
         self.inst = inst
         self._P = Problem(inst)
         self.order = np.ascontiguousarray(order, dtype=np.int32)
         L = lib()
-        h = L.or_solve(self._P.ref, _p(self.order, ctypes.c_int32), int(ibound),
-                       int(bool(keep_tables)), int(nthreads))
+        if sumprod:
+            if not inst.is_f64 or ibound >= 0:
+                raise ValueError("sum-product oracle: f64 problems, exact BE only")
+            h = L.or_solve_sumprod(self._P.ref, _p(self.order, ctypes.c_int32),
+                                   int(bool(keep_tables)), int(nthreads))
+        else:
+            h = L.or_solve(self._P.ref, _p(self.order, ctypes.c_int32), int(ibound),
+                           int(bool(keep_tables)), int(nthreads))
         try:
             self.status = int(L.or_run_status(h))
             self.tables = []
@@ -273,3 +312,8 @@ def solve_be(inst, order, keep_tables=True, nthreads=0) -> Run:
 
 def solve_mbe(inst, order, ibound, keep_tables=True, nthreads=0) -> Run:
     return Run(inst, order, ibound, keep_tables, nthreads)
+
+
+def solve_sumprod(inst, order, keep_tables=True, nthreads=0) -> Run:
+    """Exact BE in the sum-product semiring: .value = -log Z."""
+    return Run(inst, order, -1, keep_tables, nthreads, sumprod=True)

@@ -110,3 +110,25 @@ def brute_force_np(inst, order=None, limit=50_000_000):
             total = np.minimum(total + t.astype(np.int64), INF_I32)
     best = int(np.argmin(total))  # first occurrence = lexicographically smallest
     return (float(total[best]) if inst.is_f64 else int(total[best])), [int(vals[v][best]) for v in range(n)]
+
+
+def neg_log_z(inst, limit=2_000_000):
+    """-log Z by enumeration, Z = sum over the whole state space of
+    exp(-cost(assignment)) (the partition function; cost = Eq. (1) summed
+    in f64).  Accumulated with math.fsum over exp(m - cost), m = min cost."""
+    import math
+    n = inst.n
+    space = 1
+    for v in range(n):
+        space *= int(inst.dom[v])
+    if space > limit:
+        raise ValueError(f"state space {space} exceeds brute-force limit {limit}")
+    costs = []
+    assign = [0] * n
+    for vals in itertools.product(*[range(int(inst.dom[v])) for v in range(n)]):
+        assign[:] = vals
+        costs.append(_cost(inst, assign))
+    m = min(costs)
+    if math.isinf(m):
+        return math.inf
+    return m - math.log(math.fsum(math.exp(m - c) for c in costs))

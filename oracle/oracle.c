@@ -207,6 +207,59 @@ void or_bucket_rows(const int32_t *dom, int32_t n, int32_t is_f64, int32_t x,
   }
 }
 
+/* Sum-product bucket (the paper's future work):
+ * the same aggregation as or_bucket_rows (the members' -log
+ * values are added, i.e. the factors multiplied), but the elimination sums x
+ * out instead of minimising (the sum/product semiring P:210 names):
+ *     out[theta] = -log sum_v exp(-s_v),   s_v = sum_k f_k(theta.v).
+ * Written as the textbook log-sum-exp: with m = min_v s_v (if m = +inf the
+ * row is +inf), out = m - log sum_v exp(m - s_v).  f64 only; no argmin. */
+void or_bucket_rows_sp(const int32_t *dom, int32_t n, int32_t x, int32_t nmem,
+                       const int32_t *mar, const int64_t *moff, const int32_t *mscope,
+                       const double *const *ftab, int32_t nsep, const int32_t *sep,
+                       int64_t row_begin, int64_t row_end, double *out_f, int32_t nthreads) {
+#ifdef _OPENMP
+  if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel num_threads(nthreads)
+#endif
+  {
+    int32_t *a = (int32_t *)calloc(n ? n : 1, sizeof(int32_t));
+    double *s = (double *)malloc(sizeof(double) * (dom[x] ? dom[x] : 1));
+#ifdef _OPENMP
+#pragma omp for schedule(static)
+#endif
+    for (int64_t row = row_begin; row < row_end; row++) {
+      int64_t r = row;
+      for (int q = nsep - 1; q >= 0; q--) {
+        a[sep[q]] = (int32_t)(r % dom[sep[q]]);
+        r /= dom[sep[q]];
+      }
+      for (int v = 0; v < dom[x]; v++) {
+        a[x] = v;
+        s[v] = 0.0;
+        for (int k = 0; k < nmem; k++) {
+          const int32_t *sc = mscope + moff[k];
+          int64_t idx = 0;
+          for (int q = 0; q < mar[k]; q++) idx = idx * dom[sc[q]] + a[sc[q]];
+          s[v] = s[v] + ftab[k][idx];
+        }
+      }
+      double m = INFINITY;
+      for (int v = 0; v < dom[x]; v++)
+        if (s[v] < m) m = s[v];
+      double o = INFINITY;
+      if (m < INFINITY) {
+        double z = 0.0;
+        for (int v = 0; v < dom[x]; v++) z += exp(m - s[v]);
+        o = m - log(z);
+      }
+      out_f[row - row_begin] = o;
+    }
+    free(s);
+    free(a);
+  }
+}
+
 /* ------------------------------------------------------------------ */
 /* whole solve: Alg. 1 (BE) / Alg. 2 (MBE)                              */
 
@@ -272,8 +325,8 @@ static int cmp_by_pos(const void *a, const void *b) {
   return (x > y) - (x < y);
 }
 
-or_run *or_solve(const or_problem *p, const int32_t *order, int32_t ibound,
-                 int32_t keep_tables, int32_t nthreads) {
+static or_run *or_solve_impl(const or_problem *p, const int32_t *order, int32_t ibound,
+                             int32_t keep_tables, int32_t nthreads, int32_t sumprod) {
   int n = p->n;
   or_run *r = (or_run *)calloc(1, sizeof(or_run));
   r->is_f64 = p->is_f64;
@@ -427,8 +480,14 @@ or_run *or_solve(const or_problem *p, const int32_t *order, int32_t ibound,
         it[k] = p->is_f64 ? NULL : mem_itab(p, r, t.mem[k]);
         ft[k] = p->is_f64 ? mem_ftab(p, r, t.mem[k]) : NULL;
       }
-      or_bucket_rows(p->dom, n, p->is_f64, x, t.nmem, mar, moff, msc, it, ft, t.nsep,
-                     t.sep, 0, t.rows, t.out_i, t.out_f, t.arg, nthreads);
+      if (sumprod) {
+        or_bucket_rows_sp(p->dom, n, x, t.nmem, mar, moff, msc, ft, t.nsep, t.sep, 0, t.rows,
+                          t.out_f, nthreads);
+        memset(t.arg, 0, t.rows); /* no argmin in the sum-product semiring */
+      } else {
+        or_bucket_rows(p->dom, n, p->is_f64, x, t.nmem, mar, moff, msc, it, ft, t.nsep,
+                       t.sep, 0, t.rows, t.out_i, t.out_f, t.arg, nthreads);
+      }
       free(mar);
       free(moff);
       free(msc);
@@ -487,7 +546,7 @@ or_run *or_solve(const or_problem *p, const int32_t *order, int32_t ibound,
     /* Value assignment phase (Alg. 1 lines 6-7; MBE: Example 4,
      * P:341, reading A7): for x = first..last pick the value minimising the
      * sum of ALL functions of B_x (canonical order) given earlier values. */
-    if (keep_tables) {
+    if (keep_tables && !sumprod) {
       int32_t *a = r->assign;
       for (int i = 0; i < n; i++) {
         int x = order[i];
@@ -642,4 +701,15 @@ double or_evaluate_f(const or_problem *p, const int32_t *assign) {
     s = s + p->fcost[p->table_off[f] + idx];
   }
   return s;
+}
+
+or_run *or_solve(const or_problem *p, const int32_t *order, int32_t ibound,
+                 int32_t keep_tables, int32_t nthreads) {
+  return or_solve_impl(p, order, ibound, keep_tables, nthreads, 0);
+}
+
+or_run *or_solve_sumprod(const or_problem *p, const int32_t *order, int32_t keep_tables,
+                         int32_t nthreads) {
+  if (!p->is_f64) return NULL;
+  return or_solve_impl(p, order, -1, keep_tables, nthreads, 1);
 }

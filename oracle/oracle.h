@@ -76,6 +76,14 @@ void or_bucket_rows(const int32_t *dom, int32_t n, int32_t is_f64, int32_t x,
                     int64_t row_begin, int64_t row_end, int32_t *out_i,
                     double *out_f, uint8_t *arg, int32_t nthreads);
 
+/* Sum-product variant of the bucket (the
+ * sum/product semiring of P:210): out = -log sum_v exp(-sum_k f_k), written
+ * as m - log sum_v exp(m - s_v) with m = min_v s_v; f64 only, no argmin. */
+void or_bucket_rows_sp(const int32_t *dom, int32_t n, int32_t x, int32_t nmem,
+                       const int32_t *mar, const int64_t *moff, const int32_t *mscope,
+                       const double *const *ftab, int32_t nsep, const int32_t *sep,
+                       int64_t row_begin, int64_t row_end, double *out_f, int32_t nthreads);
+
 /* ---- whole solve: BE (ibound < 0) or MBE(ibound) (Alg. 1, Alg. 2) ----- */
 typedef struct or_run or_run;
 /* keep_tables: 1 keeps every (mini-)bucket table and argmin for inspection
@@ -83,6 +91,13 @@ typedef struct or_run or_run;
  * consumed (digests are still recorded) and skips the forward pass. */
 or_run *or_solve(const or_problem *p, const int32_t *order, int32_t ibound,
                  int32_t keep_tables, int32_t nthreads);
+/* Exact BE in the sum-product semiring (f64 problems; NULL otherwise): the
+ * value is -log Z, Z = sum over all assignments of prod exp(-f) (the
+ * partition function; a belief network with evidence as 0/INF unary
+ * functions gives -log P(E)).  No forward pass (no assignment); argmin
+ * tables are all zero. */
+or_run *or_solve_sumprod(const or_problem *p, const int32_t *order, int32_t keep_tables,
+                         int32_t nthreads);
 /* 0 ok; 1 invalid i-bound (a member cannot fit, A5/A6); 2 out of memory */
 int32_t or_run_status(const or_run *r);
 int32_t or_run_ntables(const or_run *r);

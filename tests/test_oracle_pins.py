@@ -397,3 +397,111 @@ def test_pinned_config_widths():
     c5 = configs.c5()
     assert oracle.induced_width(c5, oracle.minfill_order(c5)) == 18
     assert oracle.induced_width(configs.c3(), configs.c3_order()) == 20
+
+
+# ------------------------------------------------ sum-product (§8(f) row 3)
+# The sum/product semiring (partition function = the paper's future
+# work): -log Z with Z = sum over all assignments of prod exp(-f).
+
+def _close(a, b, tol=1e-12):
+    return (math.isinf(a) and math.isinf(b)) or abs(a - b) <= tol * (1 + abs(b))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_sumprod_against_brute_force(seed):
+    """-log Z of the oracle's sum-product BE equals enumeration of the whole
+    state space (with forbidden cells for seeds >= 3)."""
+    from oracle.brute import neg_log_z
+    inst = gen.random_network_f64(8, 2, 3, 12, 1, 3, 4.0, 0.3 if seed >= 3 else 0.0, seed)
+    for order in (oracle.minfill_order(inst), np.arange(inst.n, dtype=np.int32)):
+        r = oracle.solve_sumprod(inst, order)
+        assert r.assignment is None
+        assert _close(r.value, neg_log_z(inst)), (r.value, neg_log_z(inst))
+
+
+@pytest.mark.parametrize("n,seed", [(30, 1), (80, 2), (150, 3)])
+def test_sumprod_belief_net_is_normalised(n, seed):
+    """A belief network without evidence is a normalised distribution
+    (CPTs sum to 1 over the child), so Z = 1 exactly and
+    -log Z = 0 up to rounding, at any size."""
+    bn = gen.belief_net(n, 2, 4, 3, 8, seed)
+    r = oracle.solve_sumprod(bn, oracle.minfill_order(bn))
+    assert abs(r.value) < 1e-12 * n
+
+
+def _with_evidence(bn, ev):
+    """Evidence as 0 / +inf unary functions."""
+    funcs = [(list(bn.scope(f)), bn.table(f)) for f in range(bn.nf)]
+    for v, e in ev.items():
+        t = np.full(int(bn.dom[v]), np.inf)
+        t[e] = 0.0
+        funcs.append(([v], t))
+    return gen.Instance.from_functions(bn.dom, funcs, is_f64=True)
+
+
+def test_sumprod_root_evidence_is_the_prior():
+    """Evidence on the parentless x0 and on a child x1 whose only parent is
+    x0: Z = P(E) = p(x0 = e0) * p(x1 = e1 | x0 = e0), two CPT entries (the
+    generator's CPT tables are -log p with the child last)."""
+    bn = gen.belief_net(40, 2, 4, 3, 8, 5)
+    f0 = [f for f in range(bn.nf) if list(bn.scope(f)) == [0]]
+    f1 = [f for f in range(bn.nf) if list(bn.scope(f)) == [0, 1]]
+    assert len(f0) == 1 and len(f1) == 1
+    t1 = bn.table(f1[0]).reshape(int(bn.dom[0]), int(bn.dom[1]))
+    assert np.allclose(np.exp(-t1).sum(axis=1), 1.0)  # child last: rows normalised
+    e0, e1 = int(bn.dom[0]) - 1, 1
+    inst = _with_evidence(bn, {0: e0})
+    r = oracle.solve_sumprod(inst, oracle.minfill_order(inst))
+    assert _close(r.value, float(bn.table(f0[0])[e0]), 1e-11)
+    inst = _with_evidence(bn, {0: e0, 1: e1})
+    r = oracle.solve_sumprod(inst, oracle.minfill_order(inst))
+    expect = float(bn.table(f0[0])[e0]) + float(t1[e0, e1])
+    assert _close(r.value, expect, 1e-11), (r.value, expect)
+
+
+def test_sumprod_evidence_against_brute_force():
+    """P(E) for evidence on non-root variables, against enumeration."""
+    from oracle.brute import neg_log_z
+    bn = gen.belief_net(9, 2, 3, 2, 4, 11)
+    inst = _with_evidence(bn, {8: 1, 5: 0})
+    r = oracle.solve_sumprod(inst, oracle.minfill_order(inst))
+    assert _close(r.value, neg_log_z(inst))
+    assert r.value > 0  # P(E) < 1
+
+
+def test_sumprod_independent_factors_closed_form():
+    """Unary factors only: Z = prod_i sum_v exp(-f_i(v)); all-zero costs give
+    Z = prod d_i, i.e. negative messages (-log d) — pins the sign."""
+    rng = np.random.default_rng(3)
+    dom = [2, 3, 5, 4, 1]
+    tabs = [rng.uniform(0, 6, d) for d in dom]
+    inst = gen.Instance.from_functions(dom, [([i], t) for i, t in enumerate(tabs)], is_f64=True)
+    expect = math.fsum(-math.log(math.fsum(math.exp(-c) for c in t)) for t in tabs)
+    assert _close(oracle.solve_sumprod(inst, oracle.minfill_order(inst)).value, expect)
+    zero = gen.Instance.from_functions(dom, [([i], np.zeros(d)) for i, d in enumerate(dom)],
+                                       is_f64=True)
+    assert _close(oracle.solve_sumprod(zero, np.arange(5, dtype=np.int32)).value,
+                  -math.log(2 * 3 * 5 * 4 * 1))
+
+
+def test_sumprod_bucket_rows_special_cases():
+    """One member: each row is scipy's logsumexp of the negated slice
+    (library routine); an all-infinite row stays +inf; d = 1 is the identity."""
+    from scipy.special import logsumexp
+    rng = np.random.default_rng(9)
+    dom = [3, 4, 6]
+    t = rng.uniform(-5, 20, 3 * 4 * 6)
+    t[:6] = np.inf  # row (0, 0) all infinite
+    t[7] = np.inf
+    out = oracle.bucket_eval_sp(dom, 2, [([0, 1, 2], t)], [0, 1])
+    ref = [-logsumexp(-t[r * 6:(r + 1) * 6]) for r in range(12)]
+    assert math.isinf(out[0]) and out[0] > 0
+    np.testing.assert_allclose(out[1:], ref[1:], rtol=1e-13)
+    # two members: sum inside the exponent (aggregation P:204-205)
+    u = rng.uniform(0, 3, 4 * 6)
+    out2 = oracle.bucket_eval_sp(dom, 2, [([0, 1, 2], t), ([1, 2], u)], [0, 1])
+    for r in range(1, 12):
+        b = r % 4
+        assert _close(out2[r], -logsumexp(-(t[r * 6:(r + 1) * 6] + u[b * 6:(b + 1) * 6])), 1e-13)
+    one = oracle.bucket_eval_sp([3, 1], 1, [([0, 1], np.array([1.5, 2.0, 7.0]))], [0])
+    np.testing.assert_array_equal(one, [1.5, 2.0, 7.0])
