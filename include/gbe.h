@@ -52,8 +52,12 @@ typedef enum {
 } gbe_status;
 
 /* Semiring of the aggregate/eliminate operators.
- * MPE is solved as min-sum over -log p in float64 (A10). */
-typedef enum { GBE_MINSUM_I32 = 0, GBE_MINSUM_F64 = 1 } gbe_semiring;
+ * MPE is solved as min-sum over -log p in float64 (A10).  GBE_SUMPROD_F64
+ * (buckets and plans only; problems hold GBE_MINSUM_F64 costs): the same
+ * aggregation of -log values, eliminated by -log sum_v exp(-s_v) — the
+ * sum/product semiring of P:210, giving -log Z (partition function, P(E);
+ * SURVEY §8(f) row 3, the paper's future work P:1631).  No argmin. */
+typedef enum { GBE_MINSUM_I32 = 0, GBE_MINSUM_F64 = 1, GBE_SUMPROD_F64 = 2 } gbe_semiring;
 
 typedef enum {
   GBE_ORDER_MINFILL = 0,      /* greedy min-fill, ties (fill, degree, id) (A3) */
@@ -140,7 +144,8 @@ gbe_status gbe_pseudotree(const gbe_problem *p, const int32_t *order,
  * greedy first-fit partition, reading A6).  json_exec (NULL ok):
  *   {"device":0, "budget_bytes":N, "world_size":W, "rank":r,
  *    "shard_min_rows":N, "retain":"none"|"args"|"all", "timing":true,
- *    "kernel":-1|0|1, "resident_inputs":false, "graph":true, "concurrent":true}
+ *    "kernel":-1|0|1, "resident_inputs":false, "graph":true, "concurrent":true,
+ *    "semiring":"minsum"|"sumprod"}
  * "retain":"all" keeps every table on the device for gbe_run_table().
  * "kernel" forces the generic (0) or tiled (1) bucket kernel (-1 = auto).
  * "resident_inputs" keeps the uploaded tables on the device between solves.
@@ -149,6 +154,10 @@ gbe_status gbe_pseudotree(const gbe_problem *p, const int32_t *order,
  * its producers and on earlier users of the arena ranges it reuses), so
  * sibling subtrees run concurrently.  "timing" serialises the
  * buckets (per-launch events).
+ * "semiring":"sumprod" (float64 problems, ibound < 0 only, else
+ * GBE_E_INVALID): every bucket eliminates by -log sum exp(-.), so
+ * gbe_solve_be's opt is -log Z; there is no assignment (assign_out must be
+ * NULL, gbe_dpop_value fails) and argmin tables read back as zeros.
  * Errors: GBE_E_INVALID (bad order, i-bound < member arity - 1),
  * GBE_E_BUDGET (names the bucket and its rows). */
 gbe_status gbe_plan_create(const gbe_problem *p, const int32_t *order, int32_t ibound,
@@ -219,7 +228,9 @@ typedef struct gbe_bucket_desc {
                                     sharded inputs: first local element)           */
 } gbe_bucket_desc;
 
-/* desc: HOST pointer; dev_inputs[k]: device pointers to int32 or double tables;
+/* With semiring GBE_SUMPROD_F64: out = -log sum_v exp(-s_v) (m - log sum_v
+ * exp(m - s_v), m = min_v s_v; +inf rows stay +inf) and arg = 0.
+ * desc: HOST pointer; dev_inputs[k]: device pointers to int32 or double tables;
  * dev_out: device array of (row_end - row_begin) int32/double; dev_arg: device
  * uint8 array of the same length or NULL.  Asynchronous on `stream`.
  * Errors: GBE_E_INVALID (sizes, d > 256, k > GBE_MAX_INPUTS), GBE_E_CUDA. */

@@ -199,7 +199,7 @@ __device__ __forceinline__ void prefetch_tile(const FastDesc *__restrict__ Fg, c
 
 // cell (a, b, v) = P0[v] (+ P1[a][v]) (+ P2[b][v]) (+ P3[a][b][v]) with the
 // saturating adds of A9; min over v, first minimiser (A8); staged in smem.
-template <typename T, int R, int R2, int DV, bool H1, bool H2, bool H3>
+template <typename T, int R, int R2, int DV, bool H1, bool H2, bool H3, bool SP>
 __device__ __forceinline__ void combine(const typename SrF<T>::Acc (&P0)[DV],
                                         const typename SrF<T>::Acc (&P1)[R][DV],
                                         const typename SrF<T>::Acc (&P2)[R2][DV],
@@ -230,23 +230,37 @@ __device__ __forceinline__ void combine(const typename SrF<T>::Acc (&P0)[DV],
         else
           c[v] = Q[v];
       }
-      Acc best = c[0];
-      int bv = 0;
-#pragma unroll
-      for (int v = 1; v < DV; v++)
-        if (c[v] < best) {
-          best = c[v];
-          bv = v;
-        }
-      if (S::kInt) gmax = gmax > best ? gmax : best;  // infinite rows fixed per group
       const int l = loff[a][b];
-      outs[l] = S::out(best);
-      args[l] = (uint8_t)bv;
+      if constexpr (SP) {  // -log sum_v exp(-c_v) = m - log sum_v exp(m - c_v)
+        Acc m = c[0];
+#pragma unroll
+        for (int v = 1; v < DV; v++) m = fmin(m, c[v]);
+        if (m < S::inf()) {
+          double z = 0.0;
+#pragma unroll
+          for (int v = 0; v < DV; v++) z += exp(m - c[v]);
+          m -= log(z);
+        }
+        outs[l] = S::out(m);
+        args[l] = 0;
+      } else {
+        Acc best = c[0];
+        int bv = 0;
+#pragma unroll
+        for (int v = 1; v < DV; v++)
+          if (c[v] < best) {
+            best = c[v];
+            bv = v;
+          }
+        if (S::kInt) gmax = gmax > best ? gmax : best;  // infinite rows fixed per group
+        outs[l] = S::out(best);
+        args[l] = (uint8_t)bv;
+      }
     }
   }
 }
 
-template <typename T, int R, int R2, int DV>
+template <typename T, int R, int R2, int DV, bool SP>
 __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && R * R2 * DV <= 27) ? 2 : 1) bk_fast_kernel(const FastDesc *__restrict__ Fg, InPtrs in,
                                                            T *__restrict__ out, uint8_t *__restrict__ arg,
                                                            int64_t row_begin, int64_t t_begin,
@@ -413,14 +427,14 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && R * R2 * DV <= 27
       uint8_t *argq = args + row0;
       Acc gmax = S::zero();
       switch (sel) {
-        case 0: combine<T, R, R2, DV, false, false, false>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
-        case 1: combine<T, R, R2, DV, true, false, false>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
-        case 2: combine<T, R, R2, DV, false, true, false>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
-        case 3: combine<T, R, R2, DV, true, true, false>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
-        case 4: combine<T, R, R2, DV, false, false, true>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
-        case 5: combine<T, R, R2, DV, true, false, true>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
-        case 6: combine<T, R, R2, DV, false, true, true>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
-        default: combine<T, R, R2, DV, true, true, true>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
+        case 0: combine<T, R, R2, DV, false, false, false, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
+        case 1: combine<T, R, R2, DV, true, false, false, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
+        case 2: combine<T, R, R2, DV, false, true, false, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
+        case 3: combine<T, R, R2, DV, true, true, false, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
+        case 4: combine<T, R, R2, DV, false, false, true, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
+        case 5: combine<T, R, R2, DV, true, false, true, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
+        case 6: combine<T, R, R2, DV, false, true, true, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
+        default: combine<T, R, R2, DV, true, true, true, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
       }
       // a row whose minimum is infinite clamps every value to INF, so its
       // first index wins (A8); rare, so handled once per group
@@ -479,10 +493,10 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && R * R2 * DV <= 27
 // ---------------------------------------------------------------------------
 // dispatch table over (semiring, R, DV)
 
-template <typename T, int R, int R2, int DV>
+template <typename T, int R, int R2, int DV, bool SP>
 cudaError_t launch_one(const FastDesc *d, const InPtrs &in, void *out, uint8_t *arg, int64_t rb,
                        int64_t t0, int64_t t1, int grid, int block, int smem, cudaStream_t s) {
-  auto kern = bk_fast_kernel<T, R, R2, DV>;
+  auto kern = bk_fast_kernel<T, R, R2, DV, SP>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -492,12 +506,12 @@ cudaError_t launch_one(const FastDesc *d, const InPtrs &in, void *out, uint8_t *
   return cudaGetLastError();
 }
 
-template <typename T>
+template <typename T, bool SP>
 cudaError_t dispatch(int R, int R2, int DV, const FastDesc *d, const InPtrs &in, void *out,
                      uint8_t *arg, int64_t rb, int64_t t0, int64_t t1, int grid, int block,
                      int smem, cudaStream_t s) {
 #define GBE_CASE(r, r2, dv) \
-  if (R == r && R2 == r2 && DV == dv) return launch_one<T, r, r2, dv>(d, in, out, arg, rb, t0, t1, grid, block, smem, s);
+  if (R == r && R2 == r2 && DV == dv) return launch_one<T, r, r2, dv, SP>(d, in, out, arg, rb, t0, t1, grid, block, smem, s);
   GBE_CASE(2, 2, 2) GBE_CASE(2, 2, 3) GBE_CASE(2, 2, 4) GBE_CASE(2, 2, 5) GBE_CASE(3, 3, 2) GBE_CASE(3, 3, 3)
   GBE_CASE(3, 1, 2) GBE_CASE(3, 1, 3) GBE_CASE(3, 1, 4) GBE_CASE(3, 1, 5)
   GBE_CASE(4, 1, 2) GBE_CASE(4, 1, 3) GBE_CASE(4, 1, 4) GBE_CASE(4, 1, 5)
@@ -532,7 +546,7 @@ bool supported(int R, int R2, int DV, int es) {
 bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int num_sms,
                FastDesc &F, BkfLaunch &L) {
   const int m = h.nsep, k = h.ninputs, DV = h.d;
-  const int es = h.semiring == GBE_MINSUM_F64 ? 8 : 4;
+  const int es = h.semiring == GBE_MINSUM_I32 ? 4 : 8;
   if (m < 2 || k < 1 || k > 32 || DV < 2 || DV > 5) return false;
   if (row_end <= row_begin) return false;
   // tiny buckets: the tiled kernel's per-CTA setup (descriptor copy, offset
@@ -699,6 +713,7 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     L.R2 = R2;
     L.DV = DV;
     L.es = es;
+    L.sp = h.semiring == GBE_SUMPROD_F64;
     return true;
   }
   return false;
@@ -706,10 +721,13 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
 
 cudaError_t bkf_launch(const FastDesc *dev_f, const BkfLaunch &L, const InPtrs &in, void *out,
                        uint8_t *arg, int64_t row_begin, cudaStream_t s) {
+  if (L.sp)
+    return dispatch<double, true>(L.R, L.R2, L.DV, dev_f, in, out, arg, row_begin, L.t_begin, L.t_end,
+                                  L.grid, L.block, L.smem, s);
   if (L.es == 8)
-    return dispatch<double>(L.R, L.R2, L.DV, dev_f, in, out, arg, row_begin, L.t_begin, L.t_end, L.grid,
+    return dispatch<double, false>(L.R, L.R2, L.DV, dev_f, in, out, arg, row_begin, L.t_begin, L.t_end, L.grid,
                             L.block, L.smem, s);
-  return dispatch<int32_t>(L.R, L.R2, L.DV, dev_f, in, out, arg, row_begin, L.t_begin, L.t_end, L.grid,
+  return dispatch<int32_t, false>(L.R, L.R2, L.DV, dev_f, in, out, arg, row_begin, L.t_begin, L.t_end, L.grid,
                            L.block, L.smem, s);
 }
 

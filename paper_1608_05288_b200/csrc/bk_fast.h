@@ -36,6 +36,7 @@ struct FastDesc {
 
 struct BkfLaunch {
   int R = 0, R2 = 0, DV = 0, es = 4;
+  bool sp = false;  // sum-product elimination (GBE_SUMPROD_F64)
   int grid = 1, block = 256, smem = 0;
   int64_t t_begin = 0, t_end = 0;
 };

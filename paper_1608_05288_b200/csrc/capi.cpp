@@ -48,6 +48,9 @@ ExecOptions parse_exec(const char *json) {
   ex.resident_inputs = j.b("resident_inputs", false);
   ex.graph = j.b("graph", true);
   ex.concurrent = j.b("concurrent", true);
+  std::string sr = j.s("semiring", "minsum");
+  if (sr == "sumprod") ex.sumprod = true;
+  else if (sr != "minsum") GBE_FAIL(GBE_E_INVALID, "semiring must be minsum|sumprod");
   return ex;
 }
 
@@ -179,6 +182,8 @@ gbe_status gbe_solve_be(gbe_plan *plan, void *stream, gbe_value *opt, int32_t *a
   return guard([&] {
     if (!plan) GBE_FAIL(GBE_E_INVALID, "null plan");
     if (plan->plan->ibound >= 0) GBE_FAIL(GBE_E_INVALID, "plan was built for MBE (i-bound %d)", plan->plan->ibound);
+    if (plan->plan->ex.sumprod && assign_out)
+      GBE_FAIL(GBE_E_INVALID, "a sum-product plan has no assignment (pass assign_out = NULL)");
     solve(plan, stream, false, opt, nullptr, assign_out, stats_json, cap);
   });
 }

@@ -112,6 +112,7 @@ struct ExecOptions {
   bool resident_inputs = false; // keep the uploaded originals on the device between solves
   bool graph = true;            // replay the UTIL phase as a CUDA graph (1 GPU, cached arena)
   bool concurrent = true;       // the graph is the task DAG: sibling subtrees overlap
+  bool sumprod = false;         // sum-product semiring (-log Z), f64 exact BE only
 };
 
 struct Plan {

@@ -846,6 +846,7 @@ void run_destroy(RunImpl *R) { delete R; }
 gbe_value run_optimum(const RunImpl *R) { return R->optimum; }
 
 void run_value_phase(RunImpl *R, int32_t *assign_out) {
+  if (R->gp->plan->ex.sumprod) GBE_FAIL(GBE_E_INVALID, "a sum-product run has no VALUE phase");
   CK(cudaSetDevice(R->D->device));
   run_value(*R, assign_out);
 }
@@ -907,7 +908,8 @@ int bucket_kernel_variant(const gbe_bucket_desc *h, int64_t row_begin, int64_t r
 void bucket_kernel(const gbe_bucket_desc *h, const void *const *dev_inputs, void *dev_out,
                    uint8_t *dev_arg, int64_t row_begin, int64_t row_end, void *stream) {
   if (!h) GBE_FAIL(GBE_E_INVALID, "null descriptor");
-  if (h->semiring != GBE_MINSUM_I32 && h->semiring != GBE_MINSUM_F64) GBE_FAIL(GBE_E_INVALID, "bad semiring");
+  if (h->semiring != GBE_MINSUM_I32 && h->semiring != GBE_MINSUM_F64 && h->semiring != GBE_SUMPROD_F64)
+    GBE_FAIL(GBE_E_INVALID, "bad semiring");
   if (h->nsep < 0 || h->nsep > GBE_MAX_SEP || h->ninputs < 0 || h->ninputs > GBE_MAX_INPUTS)
     GBE_FAIL(GBE_E_INVALID, "nsep/ninputs out of range");
   if (h->d < 1 || h->d > GBE_MAX_DOMAIN) GBE_FAIL(GBE_E_INVALID, "d=%d outside [1,%d]", h->d, GBE_MAX_DOMAIN);

@@ -8,7 +8,9 @@
 // as precomputed per-input strides ("mul/div/mod").
 //
 // Semirings: int32 min-sum with INF = 2^30 and clamp after every add (A9);
-// float64 min-sum (MPE on -log p, A10), inputs added in canonical order.
+// float64 min-sum (MPE on -log p, A10), inputs added in canonical order;
+// float64 sum-product: the same sums, eliminated by
+// -log sum_v exp(-s_v) (online log-sum-exp over v), arg = 0.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -47,6 +49,7 @@ struct Sr<double> {
   __device__ __forceinline__ static Acc load(const double *p, int64_t i) { return __ldg(p + i); }
   __device__ __forceinline__ static Acc add(Acc a, Acc b) { return __dadd_rn(a, b); }
   __device__ __forceinline__ static double out(Acc a) { return a; }
+  __device__ __forceinline__ static double inf() { return __longlong_as_double(0x7ff0000000000000LL); }
 };
 
 // ---------------------------------------------------------------------------
@@ -55,7 +58,7 @@ struct Sr<double> {
 // input are built once in shared memory; per tile: one base offset per input
 // from the high digits.  Per row: k shared-memory offsets + k*d loads.
 
-template <typename T>
+template <typename T, bool SP>
 __global__ void __launch_bounds__(256) bk_generic(const gbe_bucket_desc *__restrict__ D,
                                                   InPtrs in, T *__restrict__ out,
                                                   uint8_t *__restrict__ arg, int64_t row_begin,
@@ -94,14 +97,25 @@ __global__ void __launch_bounds__(256) bk_generic(const gbe_bucket_desc *__restr
       if (r < row_begin || r >= row_end) continue;
       Acc best = S::zero();
       int bv = 0;
+      double z = 0.0;  // SP: sum_v exp(best - s_v), rescaled whenever best drops
       for (int v = 0; v < d; v++) {
         Acc s = S::zero();
         for (int j = 0; j < k; j++)
           s = S::add(s, S::load((const T *)in.p[j], base[j] + loff[j * plow + l] + v));
-        if (v == 0 || s < best) {
+        if constexpr (SP) {
+          if (v == 0 || s < best) {
+            z = (v == 0 || best == Sr<double>::inf()) ? 1.0 : z * exp((double)s - (double)best) + 1.0;
+            best = s;
+          } else if (s < Sr<double>::inf()) {
+            z += exp((double)best - (double)s);
+          }
+        } else if (v == 0 || s < best) {
           best = s;
           bv = v;
         }
+      }
+      if constexpr (SP) {
+        if ((double)best < Sr<double>::inf()) best = (Acc)((double)best - log(z));
       }
       out[r - row_begin] = S::out(best);
       if (arg) arg[r - row_begin] = (uint8_t)bv;
@@ -226,12 +240,15 @@ cudaError_t bk_launch(const gbe_bucket_desc &h, const gbe_bucket_desc *dev_desc,
                       const InPtrs &in, void *out, uint8_t *arg, int64_t row_begin,
                       int64_t row_end, const BkLaunchInfo &li, cudaStream_t stream) {
   if (row_end <= row_begin) return cudaSuccess;
-  if (h.semiring == GBE_MINSUM_F64)
-    bk_generic<double><<<li.grid, li.block, li.smem, stream>>>(dev_desc, in, (double *)out, arg,
-                                                                row_begin, row_end, li.nlow, li.plow);
+  if (h.semiring == GBE_SUMPROD_F64)
+    bk_generic<double, true><<<li.grid, li.block, li.smem, stream>>>(
+        dev_desc, in, (double *)out, arg, row_begin, row_end, li.nlow, li.plow);
+  else if (h.semiring == GBE_MINSUM_F64)
+    bk_generic<double, false><<<li.grid, li.block, li.smem, stream>>>(
+        dev_desc, in, (double *)out, arg, row_begin, row_end, li.nlow, li.plow);
   else
-    bk_generic<int32_t><<<li.grid, li.block, li.smem, stream>>>(dev_desc, in, (int32_t *)out, arg,
-                                                                 row_begin, row_end, li.nlow, li.plow);
+    bk_generic<int32_t, false><<<li.grid, li.block, li.smem, stream>>>(
+        dev_desc, in, (int32_t *)out, arg, row_begin, row_end, li.nlow, li.plow);
   return cudaGetLastError();
 }
 

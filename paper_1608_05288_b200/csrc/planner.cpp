@@ -138,6 +138,11 @@ std::unique_ptr<Plan> make_plan(std::shared_ptr<const Problem> pp, const int32_t
   plan->prob = pp;
   plan->ibound = ibound;
   plan->ex = ex;
+  if (ex.sumprod) {
+    if (!p.is_f64()) GBE_FAIL(GBE_E_INVALID, "semiring sumprod needs a float64 (-log) problem");
+    if (ibound >= 0) GBE_FAIL(GBE_E_INVALID, "semiring sumprod: exact BE only (ibound < 0)");
+    if (plan->ex.retain == 1) plan->ex.retain = 0;  // no value phase: argmins are never read
+  }
   int n = p.n;
   if (ex.world_size < 1 || ex.rank < 0 || ex.rank >= ex.world_size)
     GBE_FAIL(GBE_E_INVALID, "bad world_size/rank (%d/%d)", ex.world_size, ex.rank);
@@ -263,7 +268,7 @@ std::unique_ptr<Plan> make_plan(std::shared_ptr<const Problem> pp, const int32_t
       t.dest = t.sep.empty() ? -1 : t.sep.back();
       // descriptor: radices + stride maps (Eq. P:673-697 as per-input strides)
       gbe_bucket_desc &D = t.desc;
-      D.semiring = p.sr;
+      D.semiring = ex.sumprod ? GBE_SUMPROD_F64 : p.sr;
       D.nsep = (int32_t)t.sep.size();
       D.d = t.d;
       D.ninputs = (int32_t)t.members.size();

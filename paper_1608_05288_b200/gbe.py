@@ -19,7 +19,7 @@ INF_I32 = 1 << 30
 MAX_SEP = 40
 MAX_INPUTS = 32
 
-MINSUM_I32, MINSUM_F64 = 0, 1
+MINSUM_I32, MINSUM_F64, SUMPROD_F64 = 0, 1, 2
 ORDER_MINFILL, ORDER_PAPER_DEGREE, ORDER_GIVEN = 0, 1, 2
 
 STATUS = {0: "OK", 1: "INVALID", 2: "PARSE", 3: "BUDGET", 4: "CUDA", 5: "COMM", 6: "INTERNAL"}
@@ -247,6 +247,12 @@ class Plan:
                                   _ptr(a) if assignment else None, buf, cap))
         out = (_val(v, self.problem.is_f64), a[:self.problem.n] if assignment else None)
         return out + (json.loads(buf.value.decode()),) if stats else out
+
+    def log_z(self, stream=None):
+        """log Z of a plan made with semiring="sumprod" (natural log of the
+        partition function; -log P(E) for a belief network with evidence is
+        -log_z()).  One value-only solve: -(gbe_solve_be's optimum)."""
+        return -self.solve_be(stream, assignment=False)[0]
 
     def solve_mbe(self, stream=None, stats=False, assignment=True):
         """(lower, upper, assignment[, stats]); assignment=False: lower bound

@@ -184,3 +184,20 @@ def test_c4_plan_shape():
     info = G.Plan(P, o).info()
     assert max(t["rows"] for t in info["tables"]) == 3 ** 20
     assert info["total_cells"] == sum(t["rows"] * t["d"] for t in info["tables"])
+
+
+def test_sumprod_plan_validation_host():
+    """"semiring":"sumprod" is validated at plan time (host only): float64
+    problems, exact BE; unknown semirings are rejected."""
+    fi = gen.random_network_f64(12, 2, 3, 18, 1, 3, 4.0, 0.0, 1)
+    P = G.Problem.from_instance(fi)
+    order, _ = P.order()
+    G.Plan(P, order, semiring="sumprod").info()
+    with pytest.raises(G.GbeError):
+        G.Plan(P, order, 2, semiring="sumprod")
+    with pytest.raises(G.GbeError):
+        G.Plan(P, order, semiring="logsum")
+    Pi = G.Problem.from_instance(gen.random_graph(10, 3, 20, 0, 0.0, 1))
+    oi, _ = Pi.order()
+    with pytest.raises(G.GbeError):
+        G.Plan(Pi, oi, semiring="sumprod")
