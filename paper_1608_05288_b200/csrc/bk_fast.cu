@@ -79,6 +79,37 @@ struct SrF<double> {
   __device__ __forceinline__ static double out(Acc a) { return a; }
 };
 
+// exp(x) for x <= 0 (x = m - c_v of the sum-product elimination, m the row
+// minimum), branch-free so the R*R2*DV independent evaluations of a thread
+// interleave (the library exp's special-case branch serialises them).
+// x is clamped at -708 (e^-708 ~ 3e-308 vanishes next to the row's own
+// term 1); x = n ln2 + r, |r| <= ln2/2 (magic-number rounding, two-part
+// ln2); e^r by its degree-12 Taylor polynomial (truncation r^13/13! < 2e-16
+// relative); 2^n from the exponent bits (n >= -1021, a normal double).
+// Constants live in a constant bank: DFMA takes c[][] operands directly,
+// whereas 64-bit literals are rematerialised (UMOV/IMAD pairs) per use under
+// the kernel's register pressure.
+__constant__ double kExpC[16] = {
+    1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0, 1.0 / 362880.0, 1.0 / 40320.0,
+    1.0 / 5040.0, 1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5, 1.0, 1.0,
+    1.4426950408889634,        // [13] log2(e)
+    -0.6931471805599453,       // [14] -ln2 (high part)
+    -2.3190468138462996e-17};  // [15] -ln2 (low part)
+
+__device__ __forceinline__ double exp_nonpos(double x) {
+  x = fmax(x, -708.0);
+  const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+  const double kn = fma(x, kExpC[13], kMagic);
+  const double n = kn - kMagic;
+  double r = fma(n, kExpC[14], x);
+  r = fma(n, kExpC[15], r);
+  double p = kExpC[0];
+#pragma unroll
+  for (int i = 1; i <= 12; i++) p = fma(p, r, kExpC[i]);
+  const int ni = __double2loint(kn);  // n in the low word (two's complement)
+  return p * __hiloint2double((ni + 1023) << 20, 0);
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -238,7 +269,7 @@ __device__ __forceinline__ void combine(const typename SrF<T>::Acc (&P0)[DV],
         if (m < S::inf()) {
           double z = 0.0;
 #pragma unroll
-          for (int v = 0; v < DV; v++) z += exp(m - c[v]);
+          for (int v = 0; v < DV; v++) z += exp_nonpos(m - c[v]);
           m -= log(z);
         }
         outs[l] = S::out(m);

@@ -17,13 +17,15 @@ ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--which-fast", action="store_true")
 ap.add_argument("--var", type=int, default=-1)
 a = ap.parse_args()
-inst = {"c4": configs.c4, "c2": configs.c2}[a.workload]()
+inst = {"c4": configs.c4, "c2": configs.c2, "c5": configs.c5, "c5sp": configs.c5}[a.workload]()
+sp = a.workload == "c5sp"
 P = G.Problem.from_instance(inst)
 order, w = P.order()
-plan = G.Plan(P, order, timing=True)
+plan = G.Plan(P, order, timing=True, **({"semiring": "sumprod"} if sp else {}))
 for _ in range(a.steps):
     run, root = plan.dpop_util()
-    assign = run.value()
+    if not sp:
+        assign = run.value()
     st = run.stats()
     run.close()
 fast = [t for t in st["tasks"] if t["variant"] == 1]
