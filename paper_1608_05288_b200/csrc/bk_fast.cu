@@ -38,12 +38,11 @@ namespace gbe {
 namespace {
 
 constexpr uint32_t kInf = GBE_INF_I32;
-constexpr int kMaxStages = 4;
-constexpr int kOutBufs = 3;
+constexpr int kMaxStages = 8;
+constexpr int kOutBufs = 2;
 constexpr int64_t kMinCells = 1 << 10;  // measured: the tiled kernel beats bk_generic from ~1e3 cells
-constexpr int kPrefetch = 0;  // tiles ahead (per CTA) prefetched into L2 (0 = off: measured slower)
-constexpr int kConsumerWarps = 8;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;
+constexpr int kGroupWarps = 8;  // warps per consumer group
+constexpr int kSmemCap = 200 * 1024;  // dynamic shared memory cap per CTA
 
 template <typename T>
 struct SrF;
@@ -141,9 +140,6 @@ __device__ __forceinline__ void tma_load_1d(void *smem_dst, const void *gsrc, ui
       : "memory");
 }
 
-__device__ __forceinline__ void prefetch_l2(const void *gsrc, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(gsrc), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ void tma_store_1d(void *gdst, const void *smem_src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst),
                "r"(smem_u32(smem_src)), "r"(bytes)
@@ -158,8 +154,8 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
-__device__ __forceinline__ void consumer_sync() {  // named barrier 1 over the consumer warps
-  asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumerWarps * 32) : "memory");
+__device__ __forceinline__ void group_sync(uint32_t id) {  // named barrier over one consumer group
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "n"(kGroupWarps * 32) : "memory");
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -167,65 +163,80 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 }
 
 
-// Slice of input `lane` (< k) for tile t: 16-byte aligned source range and the
-// byte offset of the slice start inside it.  Lane e also decodes digit e of t.
-struct SliceRange {
-  uintptr_t a16;
-  uint32_t bytes, skew;
-  int64_t rowstart;  // lane 0 only
+// Producer-side tile decode, batched: lane L decodes the CTA's tile
+// t + L*G (G = gridDim.x) — its mixed-radix high digits (one division chain
+// per lane, all lanes in parallel) — into the element offset of every input
+// slice, tb[L][j], and its first output row, trow[L].  One batch serves the
+// next 32 tiles, so the per-tile issue path is a few shared-memory reads.
+constexpr int kMaxH = 32;
+struct ProdSmem {
+  int64_t tb[32][32];    // [tile in batch][class-ordered input] element offset (shift applied)
+  int64_t trow[32];      // first output row of the tile
+  int64_t hstr[kMaxH][32];
+  int64_t hrow[kMaxH];
+  int64_t shift[32];
+  uint32_t hrad[kMaxH];
 };
-__device__ __forceinline__ SliceRange tile_slice(const FastDesc *__restrict__ Fg, const FastHot &f,
-                                                 const InPtrs &in, int64_t t, const int64_t *hstr_s) {
+
+__device__ __forceinline__ void decode_batch(ProdSmem &ps, const FastHot &f, int64_t t, int64_t step,
+                                             int64_t t_end) {
   const int lane = threadIdx.x & 31;
-  int dig = 0;
-  if (lane < f.nH) dig = (int)(((uint32_t)t / (uint32_t)Fg->hdiv[lane]) % (uint32_t)Fg->hrad[lane]);
-  int64_t base = 0, rs = 0;
-  for (int e = 0; e < f.nH; e++) {
-    int de = __shfl_sync(0xffffffffu, dig, e);
-    if (lane < f.k) base += (int64_t)de * hstr_s[e * 32 + lane];
-    if (lane == 0) rs += (int64_t)de * Fg->hrow[e];
+  const int64_t tl = t + (int64_t)lane * step;
+  if (tl < t_end) {
+    uint32_t x = (uint32_t)tl;
+    int dg[kMaxH];
+#pragma unroll
+    for (int e = kMaxH - 1; e >= 0; e--) {
+      dg[e] = 0;
+      if (e < f.nH) {
+        const uint32_t r = ps.hrad[e];
+        const uint32_t qt = x / r;
+        dg[e] = (int)(x - qt * r);
+        x = qt;
+      }
+    }
+    int64_t rs = 0;
+#pragma unroll
+    for (int e = 0; e < kMaxH; e++)
+      if (e < f.nH) rs += (int64_t)dg[e] * ps.hrow[e];
+    ps.trow[lane] = rs;
+    for (int j = 0; j < f.k; j++) {
+      int64_t acc = -ps.shift[j];
+#pragma unroll
+      for (int e = 0; e < kMaxH; e++)
+        if (e < f.nH) acc += (int64_t)dg[e] * ps.hstr[e][j];
+      ps.tb[lane][j] = acc;
+    }
   }
-  SliceRange r{0, 0, 0, rs};
-  if (lane < f.k) {
-    base -= Fg->shift[lane];
-    const char *p = (const char *)in.p[f.in_idx[lane]] + base * f.es;
-    uintptr_t a16 = (uintptr_t)p & ~(uintptr_t)15;
-    uintptr_t e16 = ((uintptr_t)p + (uintptr_t)f.slen[lane] * f.es + 15) & ~(uintptr_t)15;
-    r.a16 = a16;
-    r.bytes = (uint32_t)(e16 - a16);
-    r.skew = (uint32_t)((uintptr_t)p - a16);
-  }
-  return r;
+  __syncwarp();
 }
 
-// The producer warp issues the TMA copies of tile t into stage s (one 1-D
-// bulk copy per input) and publishes the slice bases for the consumers.
-__device__ __forceinline__ void issue_tile(const FastDesc *__restrict__ Fg, const FastHot &f,
-                                           const InPtrs &in, int64_t t, int s, unsigned char *sm,
-                                           uint64_t *full, int32_t *sbase, int64_t *rowstart,
-                                           const int64_t *hstr_s) {
+// The producer warp issues the TMA copies of batch slot L into stage s (one
+// 1-D bulk copy per input: the 16-byte aligned range covering the slice) and
+// publishes the slice bases for the consumers.
+__device__ __forceinline__ void issue_tile(const ProdSmem &ps, const FastHot &f, const char *my_in, int L,
+                                           int s, unsigned char *sm, uint64_t *full, int32_t *sbase,
+                                           int64_t *rowstart) {
   const int lane = threadIdx.x & 31;
-  SliceRange r = tile_slice(Fg, f, in, t, hstr_s);
-  if (lane < f.k) sbase[s * 32 + lane] = s * f.stage_bytes + f.soff[lane] + (int32_t)r.skew;
-  uint32_t total = r.bytes;
-  for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
-  if (lane == 0) rowstart[s] = r.rowstart;
-  __syncwarp();
+  uintptr_t a16 = 0;
+  uint32_t bytes = 0, skew = 0;
+  if (lane < f.k) {
+    const char *p = my_in + ps.tb[L][lane] * f.es;
+    a16 = (uintptr_t)p & ~(uintptr_t)15;
+    const uintptr_t e16 = ((uintptr_t)p + (uintptr_t)f.slen[lane] * f.es + 15) & ~(uintptr_t)15;
+    bytes = (uint32_t)(e16 - a16);
+    skew = (uint32_t)((uintptr_t)p - a16);
+    sbase[s * 32 + lane] = s * f.stage_bytes + f.soff[lane] + (int32_t)skew;
+  }
+  const uint32_t total = __reduce_add_sync(0xffffffffu, bytes);
+  __syncwarp();  // every lane's sbase store before lane 0's release (redux.sync does not order memory)
   if (lane == 0) {
+    rowstart[s] = ps.trow[L];
     __threadfence_block();
     mbar_arrive_expect_tx(&full[s], total);
   }
   __syncwarp();
-  if (lane < f.k && r.bytes) tma_load_1d(sm + s * f.stage_bytes + f.soff[lane], (const void *)r.a16, r.bytes, &full[s]);
-}
-
-// L2 prefetch of the large slices of a future tile: the DRAM latency is paid
-// off the critical path, the TMA load of that tile then hits L2.
-__device__ __forceinline__ void prefetch_tile(const FastDesc *__restrict__ Fg, const FastHot &f,
-                                              const InPtrs &in, int64_t t, const int64_t *hstr_s) {
-  SliceRange r = tile_slice(Fg, f, in, t, hstr_s);
-  const int lane = threadIdx.x & 31;
-  if (lane < f.k && r.bytes >= 2048) prefetch_l2((const void *)r.a16, r.bytes);
+  if (bytes) tma_load_1d(sm + s * f.stage_bytes + f.soff[lane], (const void *)a16, bytes, &full[s]);
 }
 
 // cell (a, b, v) = P0[v] (+ P1[a][v]) (+ P2[b][v]) (+ P3[a][b][v]) with the
@@ -291,20 +302,94 @@ __device__ __forceinline__ void combine(const typename SrF<T>::Acc (&P0)[DV],
   }
 }
 
-template <typename T, int R, int R2, int DV, bool SP>
-__global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && R * R2 * DV <= 27) ? 2 : 1) bk_fast_kernel(const FastDesc *__restrict__ Fg, InPtrs in,
-                                                           T *__restrict__ out, uint8_t *__restrict__ arg,
-                                                           int64_t row_begin, int64_t t_begin,
-                                                           int64_t t_end) {
+// Infinity-free int32 tables (the plan proved every entry finite and
+// (sum of the largest entries) << SH < 2^32): every cell sum is exact in
+// uint32 without clamping, and the first minimiser comes out of ONE unsigned
+// min over packed keys (sum << SH) | v — ties on the sum resolve to the
+// smaller v, i.e. A8.  The shift is folded into the per-cell add (IMAD/LEA)
+// and into group-amortised partial sums.
+template <int R, int R2, int DV, bool H1, bool H2, bool H3>
+__device__ __forceinline__ void combine_nf(const uint32_t (&P0)[DV], const uint32_t (&P1)[R][DV],
+                                           const uint32_t (&P2)[R2][DV], const uint32_t (&P3)[R][R2][DV],
+                                           int32_t *outs, uint8_t *args, const int (&loff)[R][R2]) {
+  constexpr int SH = DV <= 4 ? 2 : 3;
+  constexpr uint32_t MASK = (1u << SH) - 1u;
+  auto emit = [&](const uint32_t (&key)[DV], int l) {
+    uint32_t m = key[0];
+#pragma unroll
+    for (int v = 1; v < DV; v++) m = min(m, key[v]);
+    outs[l] = (int32_t)(m >> SH);
+    args[l] = (uint8_t)(m & MASK);
+  };
+  if constexpr (!H1) {
+    uint32_t B[R2][DV];  // ((P0 + P2[b]) << SH) + v, shared by every a
+#pragma unroll
+    for (int b = 0; b < R2; b++)
+#pragma unroll
+      for (int v = 0; v < DV; v++) B[b][v] = ((H2 ? P0[v] + P2[b][v] : P0[v]) << SH) + (uint32_t)v;
+#pragma unroll
+    for (int a = 0; a < R; a++)
+#pragma unroll
+      for (int b = 0; b < R2; b++) {
+        uint32_t key[DV];
+#pragma unroll
+        for (int v = 0; v < DV; v++) key[v] = H3 ? B[b][v] + (P3[a][b][v] << SH) : B[b][v];
+        emit(key, loff[a][b]);
+      }
+  } else {
+    uint32_t P2s[R2][DV];
+    if constexpr (H2) {
+#pragma unroll
+      for (int b = 0; b < R2; b++)
+#pragma unroll
+        for (int v = 0; v < DV; v++) P2s[b][v] = P2[b][v] << SH;
+    }
+#pragma unroll
+    for (int a = 0; a < R; a++) {
+      uint32_t A[DV];  // ((P0 + P1[a]) << SH) + v, shared by every b
+#pragma unroll
+      for (int v = 0; v < DV; v++) A[v] = ((P0[v] + P1[a][v]) << SH) + (uint32_t)v;
+#pragma unroll
+      for (int b = 0; b < R2; b++) {
+        uint32_t key[DV];
+#pragma unroll
+        for (int v = 0; v < DV; v++) {
+          uint32_t x = H2 ? A[v] + P2s[b][v] : A[v];
+          key[v] = H3 ? x + (P3[a][b][v] << SH) : x;
+        }
+        emit(key, loff[a][b]);
+      }
+    }
+  }
+}
+
+// One CTA = NG consumer groups of kGroupWarps warps + one producer warp.  The
+// producer fills ONE ring of f.nstages input stages; tile i of this CTA goes
+// to stage i mod nstages and to consumer group i mod NG, so a group computing
+// one tile never holds back the loads of the next ones (NG = 2: up to
+// nstages - 2 tiles in flight per SM).  Each group stages its rows in its own
+// output buffers and stores them with TMA bulk copies.
+template <typename T, int R, int R2, int DV, bool SP, bool NF, int NG>
+// (registers: 17 warps put 5 on one SM sub-partition, so NG = 2 gets 96 per
+// thread; NG = 1 gets 168)
+__global__ void __launch_bounds__((NG * kGroupWarps + 1) * 32, 1)
+    bk_fast_kernel(const FastDesc *__restrict__ Fg, InPtrs in, T *__restrict__ out,
+                   uint8_t *__restrict__ arg, int64_t row_begin, int64_t t_begin, int64_t t_end) {
   using S = SrF<T>;
   using Acc = typename S::Acc;
+  constexpr int kGT = kGroupWarps * 32;  // threads per consumer group
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ FastHot f;
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ int32_t sbase[kMaxStages * 32];
   __shared__ int64_t rowstart[kMaxStages];
-  __shared__ int64_t hstr_s[32 * 32];  // producer's per-digit input strides
-  for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) hstr_s[i] = Fg->hstr[i / 32][i % 32];
+  __shared__ ProdSmem ps;  // producer's decode tables
+  for (int i = threadIdx.x; i < kMaxH * 32; i += blockDim.x) ps.hstr[i / 32][i % 32] = Fg->hstr[i / 32][i % 32];
+  if (threadIdx.x < kMaxH) {
+    ps.hrow[threadIdx.x] = Fg->hrow[threadIdx.x];
+    ps.hrad[threadIdx.x] = (uint32_t)Fg->hrad[threadIdx.x];
+    ps.shift[threadIdx.x] = Fg->shift[threadIdx.x];
+  }
   {
     const int *src = (const int *)&Fg->hot;
     int *dst = (int *)&f;
@@ -313,12 +398,12 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && R * R2 * DV <= 27
   if (threadIdx.x == 0) {
     for (int s = 0; s < kMaxStages; s++) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
+      mbar_init(&empty[s], kGroupWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  const int k = f.k, Pmid = f.Pmid;
+  const int k = f.k, Pmid = f.Pmid, nst = f.nstages;
   int32_t *offtab = (int32_t *)(sm + f.off_tab);
   int32_t *mrowoff = (int32_t *)(sm + f.off_mrow);
   // per-CTA tables: slice offset of every thread group, per input; row offset
@@ -338,60 +423,62 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && R * R2 * DV <= 27
   __syncthreads();
   const int warp = threadIdx.x >> 5;
 
-  if (warp == kConsumerWarps) {  // ---- producer warp: TMA ring ----
-    for (int i = 1; i < kPrefetch; i++)  // warm the prefetch window
-      if (t_begin + blockIdx.x + (int64_t)i * gridDim.x < t_end)
-        prefetch_tile(Fg, f, in, t_begin + blockIdx.x + (int64_t)i * gridDim.x, hstr_s);
-    int s = 0;
+  if (warp == NG * kGroupWarps) {  // ---- producer warp: TMA ring ----
+    const int lane = threadIdx.x & 31;
+    const char *my_in = lane < k ? (const char *)in.p[f.in_idx[lane]] : nullptr;
+    int s = 0, L = 0;
     uint32_t ph = 0;
     for (int64_t t = t_begin + blockIdx.x; t < t_end; t += gridDim.x) {
+      if (L == 0) decode_batch(ps, f, t, gridDim.x, t_end);
       mbar_wait(&empty[s], ph ^ 1u);
-      issue_tile(Fg, f, in, t, s, sm, full, sbase, rowstart, hstr_s);
-      if (kPrefetch > 0) {
-        const int64_t tp = t + (int64_t)kPrefetch * gridDim.x;
-        if (tp < t_end) prefetch_tile(Fg, f, in, tp, hstr_s);
-      }
-      if (++s == f.nstages) {
+      issue_tile(ps, f, my_in, L, s, sm, full, sbase, rowstart);
+      if (++s == nst) {
         s = 0;
         ph ^= 1u;
       }
+      L = (L + 1) & 31;
     }
     return;
   }
 
-  // ---- consumer warps ----
-  const int ctid = threadIdx.x;  // 0 .. 32*kConsumerWarps-1
+  // ---- consumer groups ----
+  const int g = warp / kGroupWarps;
+  const int ctid = threadIdx.x - g * kGT;  // 0 .. kGT-1 inside the group
   const int PL = f.PL, es = (int)sizeof(T);
-  int s = 0, b = 0;
-  uint32_t ph = 0;
-  for (int64_t t = t_begin + blockIdx.x; t < t_end; t += gridDim.x) {
+  const int c0 = f.cls_off[0], c1 = f.cls_off[1], c2 = f.cls_off[2], c3 = f.cls_off[3], c4 = f.cls_off[4];
+  const int sel = (c2 > c1 ? 1 : 0) | (c3 > c2 ? 2 : 0) | (c4 > c3 ? 4 : 0);
+  int loff[R][R2];  // in-tile row offsets of the group digits (tile-invariant)
+#pragma unroll
+  for (int a = 0; a < R; a++)
+#pragma unroll
+    for (int bb = 0; bb < R2; bb++) loff[a][bb] = a * f.rs1 + bb * f.rs2;
+  unsigned char *const obase = sm + f.off_out + g * kOutBufs * f.out_bytes;
+  unsigned char *const abase = sm + f.off_arg + g * kOutBufs * f.arg_bytes;
+  const uint32_t bar_id = 1 + g;
+  int s = g % nst, b = 0;
+  uint32_t ph = (uint32_t)((g / nst) & 1);
+  for (int64_t t = t_begin + blockIdx.x + (int64_t)g * gridDim.x; t < t_end; t += (int64_t)NG * gridDim.x) {
     mbar_wait(&full[s], ph);
-    const unsigned char *stage = sm + s * f.stage_bytes;
+    const int32_t *sb = sbase + s * 32;
     const int64_t o0 = rowstart[s] - row_begin;
     // staging: element l of this tile lives at index l + sh (16-byte phase of
     // its global address), so the aligned interior is one TMA bulk store
     const int sh = (int)((((uintptr_t)(out + o0)) & 15) / es);
     const int sha = (int)(((uintptr_t)(arg + o0)) & 15);
-    T *outs = (T *)(sm + f.off_out + b * f.out_bytes) + sh;
-    uint8_t *args = sm + f.off_arg + b * f.arg_bytes + sha;
-    const int c0 = f.cls_off[0], c1 = f.cls_off[1], c2 = f.cls_off[2], c3 = f.cls_off[3], c4 = f.cls_off[4];
-    int loff[R][R2];  // in-tile row offsets of the group digits (tile-invariant)
-#pragma unroll
-    for (int a = 0; a < R; a++)
-#pragma unroll
-      for (int bb = 0; bb < R2; bb++) loff[a][bb] = a * f.rs1 + bb * f.rs2;
-    const int sel = (c2 > c1 ? 1 : 0) | (c3 > c2 ? 2 : 0) | (c4 > c3 ? 4 : 0);
-    for (int q = ctid; q < Pmid; q += 32 * kConsumerWarps) {
+    T *outs = (T *)(obase + b * f.out_bytes) + sh;
+    uint8_t *args = abase + b * f.arg_bytes + sha;
+    for (int q = ctid; q < Pmid; q += kGT) {
       Acc P0[DV], P1[R][DV], P2[R2][DV], P3[R][R2][DV];
       // class 0 (no group digit): P0[v]
       if (c1 > c0) {
-        const unsigned char *p = sm + sbase[s * 32 + c0] + offtab[c0 * Pmid + q];
+        const unsigned char *p = sm + sb[c0] + offtab[c0 * Pmid + q];
 #pragma unroll
         for (int v = 0; v < DV; v++) P0[v] = (Acc)((const T *)p)[v];
+#pragma unroll 1
         for (int jj = c0 + 1; jj < c1; jj++) {
-          const unsigned char *pj = sm + sbase[s * 32 + jj] + offtab[jj * Pmid + q];
+          const unsigned char *pj = sm + sb[jj] + offtab[jj * Pmid + q];
 #pragma unroll
-          for (int v = 0; v < DV; v++) P0[v] = S::add(P0[v], (Acc)((const T *)pj)[v]);
+          for (int v = 0; v < DV; v++) P0[v] = NF ? S::add_nc(P0[v], (Acc)((const T *)pj)[v]) : S::add(P0[v], (Acc)((const T *)pj)[v]);
         }
       } else {
 #pragma unroll
@@ -399,41 +486,49 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && R * R2 * DV <= 27
       }
       // class 1 (g1 only): P1[a][v]
       if (sel & 1) {
-        const unsigned char *p = sm + sbase[s * 32 + c1] + offtab[c1 * Pmid + q];
+        const unsigned char *p = sm + sb[c1] + offtab[c1 * Pmid + q];
         const int s1 = f.sg1[c1];
 #pragma unroll
         for (int a = 0; a < R; a++)
 #pragma unroll
           for (int v = 0; v < DV; v++) P1[a][v] = (Acc)((const T *)(p + a * s1))[v];
+#pragma unroll 1
         for (int jj = c1 + 1; jj < c2; jj++) {
-          const unsigned char *pj = sm + sbase[s * 32 + jj] + offtab[jj * Pmid + q];
+          const unsigned char *pj = sm + sb[jj] + offtab[jj * Pmid + q];
           const int t1 = f.sg1[jj];
 #pragma unroll
           for (int a = 0; a < R; a++)
 #pragma unroll
-            for (int v = 0; v < DV; v++) P1[a][v] = S::add(P1[a][v], (Acc)((const T *)(pj + a * t1))[v]);
+            for (int v = 0; v < DV; v++) {
+              const Acc x = (Acc)((const T *)(pj + a * t1))[v];
+              P1[a][v] = NF ? S::add_nc(P1[a][v], x) : S::add(P1[a][v], x);
+            }
         }
       }
       // class 2 (g2 only): P2[b][v]
       if (sel & 2) {
-        const unsigned char *p = sm + sbase[s * 32 + c2] + offtab[c2 * Pmid + q];
+        const unsigned char *p = sm + sb[c2] + offtab[c2 * Pmid + q];
         const int s2 = f.sg2[c2];
 #pragma unroll
         for (int bb = 0; bb < R2; bb++)
 #pragma unroll
           for (int v = 0; v < DV; v++) P2[bb][v] = (Acc)((const T *)(p + bb * s2))[v];
+#pragma unroll 1
         for (int jj = c2 + 1; jj < c3; jj++) {
-          const unsigned char *pj = sm + sbase[s * 32 + jj] + offtab[jj * Pmid + q];
+          const unsigned char *pj = sm + sb[jj] + offtab[jj * Pmid + q];
           const int t2 = f.sg2[jj];
 #pragma unroll
           for (int bb = 0; bb < R2; bb++)
 #pragma unroll
-            for (int v = 0; v < DV; v++) P2[bb][v] = S::add(P2[bb][v], (Acc)((const T *)(pj + bb * t2))[v]);
+            for (int v = 0; v < DV; v++) {
+              const Acc x = (Acc)((const T *)(pj + bb * t2))[v];
+              P2[bb][v] = NF ? S::add_nc(P2[bb][v], x) : S::add(P2[bb][v], x);
+            }
         }
       }
       // class 3 (both): P3[a][b][v]
       if (sel & 4) {
-        const unsigned char *p = sm + sbase[s * 32 + c3] + offtab[c3 * Pmid + q];
+        const unsigned char *p = sm + sb[c3] + offtab[c3 * Pmid + q];
         const int s1 = f.sg1[c3], s2 = f.sg2[c3];
 #pragma unroll
         for (int a = 0; a < R; a++)
@@ -441,52 +536,72 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && R * R2 * DV <= 27
           for (int bb = 0; bb < R2; bb++)
 #pragma unroll
             for (int v = 0; v < DV; v++) P3[a][bb][v] = (Acc)((const T *)(p + a * s1 + bb * s2))[v];
+#pragma unroll 1
         for (int jj = c3 + 1; jj < c4; jj++) {
-          const unsigned char *pj = sm + sbase[s * 32 + jj] + offtab[jj * Pmid + q];
+          const unsigned char *pj = sm + sb[jj] + offtab[jj * Pmid + q];
           const int t1 = f.sg1[jj], t2 = f.sg2[jj];
 #pragma unroll
           for (int a = 0; a < R; a++)
 #pragma unroll
             for (int bb = 0; bb < R2; bb++)
 #pragma unroll
-              for (int v = 0; v < DV; v++)
-                P3[a][bb][v] = S::add(P3[a][bb][v], (Acc)((const T *)(pj + a * t1 + bb * t2))[v]);
+              for (int v = 0; v < DV; v++) {
+                const Acc x = (Acc)((const T *)(pj + a * t1 + bb * t2))[v];
+                P3[a][bb][v] = NF ? S::add_nc(P3[a][bb][v], x) : S::add(P3[a][bb][v], x);
+              }
         }
       }
       const int row0 = mrowoff[q];
       T *outq = outs + row0;
       uint8_t *argq = args + row0;
-      Acc gmax = S::zero();
-      switch (sel) {
-        case 0: combine<T, R, R2, DV, false, false, false, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
-        case 1: combine<T, R, R2, DV, true, false, false, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
-        case 2: combine<T, R, R2, DV, false, true, false, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
-        case 3: combine<T, R, R2, DV, true, true, false, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
-        case 4: combine<T, R, R2, DV, false, false, true, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
-        case 5: combine<T, R, R2, DV, true, false, true, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
-        case 6: combine<T, R, R2, DV, false, true, true, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
-        default: combine<T, R, R2, DV, true, true, true, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
-      }
-      // a row whose minimum is infinite clamps every value to INF, so its
-      // first index wins (A8); rare, so handled once per group
-      if (S::kInt && gmax >= S::inf()) {
+      if constexpr (NF) {
+        // (T = int32: Acc = uint32)
+#define GBE_NF(h1, h2, h3) \
+  combine_nf<R, R2, DV, h1, h2, h3>(P0, P1, P2, P3, (int32_t *)outq, argq, loff)
+        switch (sel) {
+          case 0: GBE_NF(false, false, false); break;
+          case 1: GBE_NF(true, false, false); break;
+          case 2: GBE_NF(false, true, false); break;
+          case 3: GBE_NF(true, true, false); break;
+          case 4: GBE_NF(false, false, true); break;
+          case 5: GBE_NF(true, false, true); break;
+          case 6: GBE_NF(false, true, true); break;
+          default: GBE_NF(true, true, true); break;
+        }
+#undef GBE_NF
+      } else {
+        Acc gmax = S::zero();
+        switch (sel) {
+          case 0: combine<T, R, R2, DV, false, false, false, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
+          case 1: combine<T, R, R2, DV, true, false, false, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
+          case 2: combine<T, R, R2, DV, false, true, false, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
+          case 3: combine<T, R, R2, DV, true, true, false, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
+          case 4: combine<T, R, R2, DV, false, false, true, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
+          case 5: combine<T, R, R2, DV, true, false, true, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
+          case 6: combine<T, R, R2, DV, false, true, true, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
+          default: combine<T, R, R2, DV, true, true, true, SP>(P0, P1, P2, P3, outq, argq, loff, gmax); break;
+        }
+        // a row whose minimum is infinite clamps every value to INF, so its
+        // first index wins (A8); rare, so handled once per group
+        if (S::kInt && gmax >= S::inf()) {
 #pragma unroll
-        for (int a = 0; a < R; a++)
+          for (int a = 0; a < R; a++)
 #pragma unroll
-          for (int bb = 0; bb < R2; bb++) {
-            const int l = loff[a][bb];
-            if ((uint32_t)outq[l] >= kInf) {
-              outq[l] = (T)kInf;
-              argq[l] = 0;
+            for (int bb = 0; bb < R2; bb++) {
+              const int l = loff[a][bb];
+              if ((uint32_t)outq[l] >= kInf) {
+                outq[l] = (T)kInf;
+                argq[l] = 0;
+              }
             }
-          }
+        }
       }
     }
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);  // input stage free
     fence_proxy_async_smem();                             // staged rows -> async proxy
-    consumer_sync();
-    if (ctid < 32) {  // warp 0: aligned interior by TMA bulk stores, ragged ends plainly
+    group_sync(bar_id);
+    if (ctid < 32) {  // first warp of the group: aligned interior by TMA bulk stores, ragged ends plainly
       T *gout = out + o0;
       const int h = (int)(((16 - (((uintptr_t)gout) & 15)) & 15) / es);
       const int hh = min(h, PL);
@@ -506,14 +621,15 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && R * R2 * DV <= 27
       }
       if (ctid == 0) {
         bulk_commit();
-        // staging buffer of tile (i - kOutBufs + 1) is free once its store has
-        // read it; ordered before that buffer's next writers by the next
-        // consumer_sync
+        // staging buffer of this group's tile (i - kOutBufs + 1) is free once
+        // its store has read it; ordered before that buffer's next writers by
+        // the next group_sync
         bulk_wait_read<kOutBufs - 1>();
       }
     }
-    if (++s == f.nstages) {
-      s = 0;
+    s += NG;
+    if (s >= nst) {
+      s -= nst;
       ph ^= 1u;
     }
     if (++b == kOutBufs) b = 0;
@@ -524,25 +640,34 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && R * R2 * DV <= 27
 // ---------------------------------------------------------------------------
 // dispatch table over (semiring, R, DV)
 
-template <typename T, int R, int R2, int DV, bool SP>
+template <typename T, int R, int R2, int DV, bool SP, bool NF, int NG>
 cudaError_t launch_one(const FastDesc *d, const InPtrs &in, void *out, uint8_t *arg, int64_t rb,
                        int64_t t0, int64_t t1, int grid, int block, int smem, cudaStream_t s) {
-  auto kern = bk_fast_kernel<T, R, R2, DV, SP>;
+  auto kern = bk_fast_kernel<T, R, R2, DV, SP, NF, NG>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemCap);
     attr_set = true;
   }
   kern<<<grid, block, smem, s>>>(d, in, (T *)out, arg, rb, t0, t1);
   return cudaGetLastError();
 }
 
-template <typename T, bool SP>
-cudaError_t dispatch(int R, int R2, int DV, const FastDesc *d, const InPtrs &in, void *out,
+// consumer groups per CTA: two (one CTA per SM, shared ring) for int32 shapes
+// whose register blocks fit 120 registers per thread; f64 and the large
+// int32 shapes run one group (their register blocks need up to 168).
+constexpr int ng_of(int es, int R, int R2, int DV) { return (es == 4 && R * R2 * DV <= 27) ? 2 : 1; }
+
+template <typename T, bool SP, bool NF>
+cudaError_t dispatch(int R, int R2, int DV, int NGr, const FastDesc *d, const InPtrs &in, void *out,
                      uint8_t *arg, int64_t rb, int64_t t0, int64_t t1, int grid, int block,
                      int smem, cudaStream_t s) {
-#define GBE_CASE(r, r2, dv) \
-  if (R == r && R2 == r2 && DV == dv) return launch_one<T, r, r2, dv, SP>(d, in, out, arg, rb, t0, t1, grid, block, smem, s);
+#define GBE_CASE(r, r2, dv)                                                                                  \
+  if (R == r && R2 == r2 && DV == dv) {                                                                      \
+    constexpr int ng = ng_of((int)sizeof(T), r, r2, dv);                                                     \
+    if (NGr != ng) return cudaErrorInvalidValue;                                                             \
+    return launch_one<T, r, r2, dv, SP, NF, ng>(d, in, out, arg, rb, t0, t1, grid, block, smem, s);          \
+  }
   GBE_CASE(2, 2, 2) GBE_CASE(2, 2, 3) GBE_CASE(2, 2, 4) GBE_CASE(2, 2, 5) GBE_CASE(3, 3, 2) GBE_CASE(3, 3, 3)
   GBE_CASE(3, 1, 2) GBE_CASE(3, 1, 3) GBE_CASE(3, 1, 4) GBE_CASE(3, 1, 5)
   GBE_CASE(4, 1, 2) GBE_CASE(4, 1, 3) GBE_CASE(4, 1, 4) GBE_CASE(4, 1, 5)
@@ -575,7 +700,7 @@ bool supported(int R, int R2, int DV, int es) {
 // layout; false when the bucket does not fit this kernel (-> bk_generic)
 
 bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int num_sms,
-               FastDesc &F, BkfLaunch &L) {
+               FastDesc &F, BkfLaunch &L, bool noinf) {
   const int m = h.nsep, k = h.ninputs, DV = h.d;
   const int es = h.semiring == GBE_MINSUM_I32 ? 4 : 8;
   if (m < 2 || k < 1 || k > 32 || DV < 2 || DV > 5) return false;
@@ -584,15 +709,18 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
   // tables, mbarrier ring) costs more than the bucket; bk_generic is faster
   if ((row_end - row_begin) * DV < kMinCells) return false;
   const int64_t kPLMax = 16384;
-  // shared-memory budget per CTA (2 CTAs/SM by default); GBE_FAST_SMEM_KB
-  // overrides it for tuning experiments
-  // (f64: 1 CTA/SM with larger tiles measured 24 % faster on C5, because its
-  // 8-byte slices otherwise cap the tile below one group per consumer thread)
+  // one CTA per SM: dynamic shared-memory budget; GBE_FAST_SMEM_KB overrides
+  // it for tuning experiments
   static const char *smem_env = std::getenv("GBE_FAST_SMEM_KB");
-  const size_t kSmemMax = (size_t)(smem_env ? std::atoi(smem_env) : (es == 8 ? 200 : 112)) * 1024;
   static const int kStagesMax = [] {
     const char *e = std::getenv("GBE_FAST_STAGES");
     return e ? std::max(2, std::min(kMaxStages, std::atoi(e))) : kMaxStages;
+  }();
+  // stages wanted in the ring: with two consumer groups, two stages can be
+  // held by compute while the rest are in flight
+  static const int kStagesWant = [] {
+    const char *e = std::getenv("GBE_FAST_WANT_STAGES");
+    return e ? std::max(2, std::min(kMaxStages, std::atoi(e))) : 4;
   }();
   // inputs' sizes (cells) to find the largest
   auto has = [&](int j, int p) { return h.stride[j][p] != 0; };
@@ -604,6 +732,9 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
   for (int j = 1; j < k; j++)
     if (cells[j] > cells[big]) big = j;
 
+  // pass 0: the largest tile whose ring holds kStagesWant stages; pass 1: the
+  // largest tile that fits at all
+  for (int pass = 0; pass < 2; pass++) {
   for (int nl = m; nl >= 2; nl--) {
     int64_t PL = 1;
     for (int p = m - nl; p < m; p++) PL *= h.radix[p];
@@ -642,6 +773,9 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     const int R2 = g2 >= 0 ? R : 1;
     const int64_t Pmid = PL / (R * R2);
     if (row_begin % PL || row_end % PL) continue;
+    const int NG = ng_of(es, R, R2, DV);
+    const size_t kSmemMax = (size_t)(smem_env ? std::atoi(smem_env) : (NG == 2 ? 200 : 196)) * 1024;
+    const int min_st = pass == 0 ? std::max(kStagesWant, NG + 1) : NG + 1;
     // classes
     std::memset(&F, 0, sizeof(F));
     FastHot &f = F.hot;
@@ -716,16 +850,16 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     f.stage_bytes = (int32_t)off;
     f.out_bytes = (int32_t)(((size_t)PL * es + 16 + 127) & ~size_t(127));
     f.arg_bytes = (int32_t)(((size_t)PL + 16 + 127) & ~size_t(127));
-    size_t fixed = kOutBufs * ((size_t)f.out_bytes + f.arg_bytes) + (size_t)(k + 1) * Pmid * 4 + 256;
-    // 2 CTAs per SM when possible (~110 KB each), 2..4 input stages
+    size_t fixed = (size_t)NG * kOutBufs * ((size_t)f.out_bytes + f.arg_bytes) + (size_t)(k + 1) * Pmid * 4 + 256;
     int nst = kStagesMax;
-    while (nst > 2 && fixed + nst * off > kSmemMax) nst--;
+    while (nst > min_st && fixed + nst * off > kSmemMax) nst--;
+    if (fixed + nst * off > kSmemMax) continue;
     f.nstages = nst;
     off = nst * off;
     f.off_out = (int32_t)off;
-    off += kOutBufs * (size_t)f.out_bytes;
+    off += (size_t)NG * kOutBufs * f.out_bytes;
     f.off_arg = (int32_t)off;
-    off += kOutBufs * (size_t)f.arg_bytes;
+    off += (size_t)NG * kOutBufs * f.arg_bytes;
     f.off_tab = (int32_t)off;
     off += (size_t)k * Pmid * 4;
     f.off_mrow = (int32_t)off;
@@ -733,11 +867,15 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     off = (off + 127) & ~size_t(127);
     if (off > kSmemMax) continue;
     L.smem = (int)off;
-    L.block = kThreads;
+    L.NG = NG;
+    L.g1 = g1;
+    L.g2 = g2;
+    L.nf = noinf && es == 4 && h.semiring == GBE_MINSUM_I32;
+    L.block = (NG * kGroupWarps + 1) * 32;
     L.t_begin = row_begin / PL;
     L.t_end = row_end / PL;
     int per_sm = (int)std::min<size_t>(std::max<size_t>(1, (220 * 1024) / (off + 4096)), 2048 / L.block);
-    per_sm = std::max(1, std::min(per_sm, 8));
+    per_sm = std::max(1, std::min(per_sm, NG == 2 ? 1 : 8));
     int64_t tiles = L.t_end - L.t_begin;
     L.grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms * per_sm));
     L.R = R;
@@ -747,19 +885,23 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     L.sp = h.semiring == GBE_SUMPROD_F64;
     return true;
   }
+  }
   return false;
 }
 
 cudaError_t bkf_launch(const FastDesc *dev_f, const BkfLaunch &L, const InPtrs &in, void *out,
                        uint8_t *arg, int64_t row_begin, cudaStream_t s) {
   if (L.sp)
-    return dispatch<double, true>(L.R, L.R2, L.DV, dev_f, in, out, arg, row_begin, L.t_begin, L.t_end,
-                                  L.grid, L.block, L.smem, s);
+    return dispatch<double, true, false>(L.R, L.R2, L.DV, L.NG, dev_f, in, out, arg, row_begin, L.t_begin,
+                                         L.t_end, L.grid, L.block, L.smem, s);
   if (L.es == 8)
-    return dispatch<double, false>(L.R, L.R2, L.DV, dev_f, in, out, arg, row_begin, L.t_begin, L.t_end, L.grid,
-                            L.block, L.smem, s);
-  return dispatch<int32_t, false>(L.R, L.R2, L.DV, dev_f, in, out, arg, row_begin, L.t_begin, L.t_end, L.grid,
-                           L.block, L.smem, s);
+    return dispatch<double, false, false>(L.R, L.R2, L.DV, L.NG, dev_f, in, out, arg, row_begin, L.t_begin,
+                                          L.t_end, L.grid, L.block, L.smem, s);
+  if (L.nf)
+    return dispatch<int32_t, false, true>(L.R, L.R2, L.DV, L.NG, dev_f, in, out, arg, row_begin, L.t_begin,
+                                          L.t_end, L.grid, L.block, L.smem, s);
+  return dispatch<int32_t, false, false>(L.R, L.R2, L.DV, L.NG, dev_f, in, out, arg, row_begin, L.t_begin,
+                                         L.t_end, L.grid, L.block, L.smem, s);
 }
 
 }  // namespace gbe

@@ -37,12 +37,15 @@ struct FastDesc {
 struct BkfLaunch {
   int R = 0, R2 = 0, DV = 0, es = 4;
   bool sp = false;  // sum-product elimination (GBE_SUMPROD_F64)
+  bool nf = false;  // infinity-free int32 tables: packed-key argmin (no clamps)
+  int NG = 1;       // consumer groups per CTA
+  int g1 = -1, g2 = -1;  // group (register-blocking) digits
   int grid = 1, block = 256, smem = 0;
   int64_t t_begin = 0, t_end = 0;
 };
 
 bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int num_sms,
-               FastDesc &F, BkfLaunch &L);
+               FastDesc &F, BkfLaunch &L, bool noinf = false);
 cudaError_t bkf_launch(const FastDesc *dev_f, const BkfLaunch &L, const InPtrs &in, void *out,
                        uint8_t *arg, int64_t row_begin, cudaStream_t s);
 

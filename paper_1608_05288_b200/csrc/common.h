@@ -49,6 +49,8 @@ struct Problem {
   std::vector<int64_t> table_off; // [nf+1]
   std::vector<int32_t> icost;     // int32 semiring
   std::vector<double> fcost;      // f64 semiring
+  bool has_inf = false;           // int32: some entry is INF (A9)
+  int64_t maxsum = 0;             // int32: sum of the largest finite entries (< 2^30, A9)
   bool is_f64() const { return sr == GBE_MINSUM_F64; }
   size_t elem() const { return is_f64() ? 8 : 4; }
   const int32_t *scope(int f) const { return scopes.data() + scope_off[f]; }

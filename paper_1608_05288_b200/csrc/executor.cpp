@@ -80,6 +80,19 @@ struct DevPlan {
   std::vector<FastDesc> h_fast;
   std::vector<BkfLaunch> fl;
   std::vector<char> use_fast;
+  // pre-aggregation of small inputs (DESIGN.md §5 "input merging"): merge mi
+  // sums some inputs of task merges[mi].task into one table, a d = 1 bucket
+  struct Merge {
+    int32_t task = -1;
+    gbe_bucket_desc h{};
+    BkLaunchInfo li{};
+    std::vector<int32_t> src;  // task input indices (canonical member positions)
+    size_t bytes = 0;
+  };
+  std::vector<Merge> merges;
+  std::vector<std::vector<int32_t>> task_merges;  // per task: its merges
+  std::vector<std::vector<int32_t>> in_map;       // per task input: member index, or -(1 + merge)
+  gbe_bucket_desc *d_mdesc = nullptr;
   FastDesc *d_fast = nullptr;
   gbe_bucket_desc *d_desc = nullptr;
   int64_t *d_off = nullptr;
@@ -96,7 +109,7 @@ struct DevPlan {
   struct Arena {
     bool planned = false;
     size_t bytes = 0, off_raw = 0, off_sorted = 0;
-    std::vector<size_t> off_out, off_full, off_arg;
+    std::vector<size_t> off_out, off_full, off_arg, off_merge;
     // UTIL-phase DAG: deps[t] = tasks that must finish before task t starts
     // (its producers and the last users of arena ranges it overwrites)
     std::vector<std::vector<int32_t>> deps;
@@ -131,6 +144,7 @@ struct DevPlan {
         else cudaFree(a.mem);
       }
     cudaFree(d_desc);
+    cudaFree(d_mdesc);
     cudaFree(d_fast);
     cudaFree(d_off);
     cudaFree(d_poff);
@@ -200,11 +214,16 @@ static void plan_arena(const Plan &P, DevPlan *D, bool mbe_mode) {
   auto put = [&](size_t ti, size_t o, size_t b) {
     ranges[ti].push_back({o, o + std::max<size_t>((b + 255) & ~size_t(255), 256)});
   };
+  A.off_merge.assign(D->merges.size(), SIZE_MAX);
   for (size_t ti = 0; ti < nt; ti++) {
     const Task &t = P.tasks[ti];
     const Shard &sh = t.shard;
     int64_t local = sh.on ? sh.hi - sh.lo : t.rows;
     int64_t cap = sh.on ? sh.per * sh.block_rows : t.rows;
+    for (int32_t mi : D->task_merges[ti]) {  // live only while task ti runs
+      A.off_merge[mi] = fl.alloc(D->merges[mi].bytes);
+      put(ti, A.off_merge[mi], D->merges[mi].bytes);
+    }
     out_b[ti] = el * (size_t)cap;
     A.off_out[ti] = fl.alloc(out_b[ti]);
     put(ti, A.off_out[ti], out_b[ti]);
@@ -219,6 +238,7 @@ static void plan_arena(const Plan &P, DevPlan *D, bool mbe_mode) {
       fl.release(A.off_out[ti], out_b[ti]);
       out_b[ti] = 0;
     }
+    for (int32_t mi : D->task_merges[ti]) fl.release(A.off_merge[mi], D->merges[mi].bytes);
     if ((!mbe_mode || P.ex.retain == 0) && P.ex.retain < 2)
       for (auto &m : t.members)
         if (m.kind == 1) {
@@ -272,6 +292,134 @@ static void plan_arena(const Plan &P, DevPlan *D, bool mbe_mode) {
   A.planned = true;
 }
 
+// Input merging (pre-aggregation): inside a large bucket, inputs that lack
+// the same group digits of the tiled kernel (same "class", bk_fast.cu) are
+// each re-loaded per register block; the small ones are summed ONCE into one
+// table over the union of their scopes — a d = 1 bucket (out = the sum of its
+// members, the minimum over a single value being the identity) — and the
+// bucket reads that table instead.  Small class-0 inputs (neither group
+// digit) fold into the merged table of another class when one exists: the
+// fold adds no per-cell loads.  Sums are the same ones Alg. 1 line 3 forms
+// (P:204-205); for int32 with the clamp of A9 they are bit-identical, for
+// f64 the summation order changes (canonical order note).
+static void plan_merges(const Plan &P, DevPlan *D, size_t ti, gbe_bucket_desc &h, bool noinf) {
+  static const bool off = std::getenv("GBE_NO_MERGE") != nullptr;  // A/B knob
+  const Task &t = P.tasks[ti];
+  const int k = h.ninputs, m = h.nsep, d = h.d;
+  auto &map = D->in_map[ti];
+  map.resize(k);
+  for (int j = 0; j < k; j++) map[j] = j;
+  if (off || P.ex.kernel == 0 || k < 2) return;
+  const int64_t C = (t.shard.hi - t.shard.lo) * d;
+  if (C < (int64_t(1) << 22)) return;  // small buckets: the extra launches cost more than they save
+  FastDesc *F = new FastDesc();
+  BkfLaunch L;
+  const bool ok = bkf_build(h, t.shard.lo, t.shard.hi, D->num_sms, *F, L, noinf);
+  delete F;
+  if (!ok) return;
+  auto has = [&](int j, int p) { return h.stride[j][p] != 0; };
+  auto union_cells = [&](const std::vector<int> &js) {
+    int64_t c = d;
+    for (int p = 0; p < m; p++)
+      for (int j : js)
+        if (has(j, p)) {
+          c *= h.radix[p];
+          break;
+        }
+    return c;
+  };
+  const int64_t small = C / 64, cap = std::min<int64_t>(C / 32, int64_t(1) << 26);
+  std::vector<int> cand[4];
+  for (int j = 0; j < k; j++) {
+    if (h.shift[j] != 0) continue;
+    if (union_cells({j}) > small) continue;
+    const int cls = (has(j, L.g1) ? 1 : 0) + (L.g2 >= 0 && has(j, L.g2) ? 2 : 0);
+    cand[cls].push_back(j);
+  }
+  if (!cand[0].empty()) {  // fold class 0 into the class whose union stays smallest
+    int best = -1;
+    int64_t bestc = INT64_MAX;
+    for (int c = 1; c < 4; c++) {
+      if (cand[c].empty()) continue;
+      std::vector<int> u = cand[c];
+      u.insert(u.end(), cand[0].begin(), cand[0].end());
+      const int64_t uc = union_cells(u);
+      if (uc <= cap && uc < bestc) {
+        bestc = uc;
+        best = c;
+      }
+    }
+    if (best > 0) {
+      cand[best].insert(cand[best].end(), cand[0].begin(), cand[0].end());
+      std::sort(cand[best].begin(), cand[best].end());
+      cand[0].clear();
+    }
+  }
+  std::vector<std::vector<int>> sets;
+  for (int c = 0; c < 4; c++)
+    if (cand[c].size() >= 2 && union_cells(cand[c]) <= cap) sets.push_back(cand[c]);
+  if (sets.empty()) return;
+  std::vector<char> merged(k, 0);
+  for (auto &st : sets)
+    for (int j : st) merged[j] = 1;
+  gbe_bucket_desc h2 = h;
+  std::memset(h2.stride, 0, sizeof(h2.stride));
+  std::memset(h2.shift, 0, sizeof(h2.shift));
+  map.clear();
+  int n2 = 0;
+  for (int j = 0; j < k; j++)
+    if (!merged[j]) {
+      for (int p = 0; p < m; p++) h2.stride[n2][p] = h.stride[j][p];
+      h2.shift[n2] = h.shift[j];
+      map.push_back(j);
+      n2++;
+    }
+  const size_t el = h.semiring == GBE_MINSUM_I32 ? 4 : 8;
+  for (auto &st : sets) {
+    std::vector<int> U;  // union scope, ascending output position (lexicographic layout)
+    for (int p = 0; p < m; p++)
+      for (int j : st)
+        if (has(j, p)) {
+          U.push_back(p);
+          break;
+        }
+    DevPlan::Merge M;
+    M.task = (int32_t)ti;
+    M.src.assign(st.begin(), st.end());
+    gbe_bucket_desc &hm = M.h;
+    std::memset(&hm, 0, sizeof(hm));
+    hm.semiring = h.semiring == GBE_MINSUM_I32 ? GBE_MINSUM_I32 : GBE_MINSUM_F64;
+    hm.nsep = (int32_t)U.size() + 1;  // U, then the eliminated variable as a plain digit
+    hm.d = 1;
+    hm.ninputs = (int32_t)st.size();
+    hm.rows = 1;
+    for (size_t q = 0; q < U.size(); q++) {
+      hm.radix[q] = h.radix[U[q]];
+      hm.rows *= h.radix[U[q]];
+    }
+    hm.radix[U.size()] = d;
+    hm.rows *= d;
+    for (size_t i = 0; i < st.size(); i++) {
+      for (size_t q = 0; q < U.size(); q++) hm.stride[i][q] = h.stride[st[i]][U[q]];
+      hm.stride[i][U.size()] = 1;
+    }
+    M.li = bk_plan_launch(hm, 0, hm.rows, BK_GENERIC, D->num_sms);
+    M.bytes = el * (size_t)hm.rows;
+    // the bucket reads the merged table with its own mixed-radix strides
+    int64_t st_ = d;
+    for (int q = (int)U.size() - 1; q >= 0; q--) {
+      h2.stride[n2][U[q]] = st_;
+      st_ *= h.radix[U[q]];
+    }
+    map.push_back(-(1 + (int32_t)D->merges.size()));
+    D->task_merges[ti].push_back((int32_t)D->merges.size());
+    D->merges.push_back(std::move(M));
+    n2++;
+  }
+  h2.ninputs = n2;
+  h = h2;
+}
+
 static DevPlan *dev_plan(gbe_plan *gp) {
   if (gp->dev) return (DevPlan *)gp->dev;
   const Plan &P = *gp->plan;
@@ -284,12 +432,18 @@ static DevPlan *dev_plan(gbe_plan *gp) {
   auto *D = new DevPlan();
   D->device = P.ex.device;
   CK(cudaDeviceGetAttribute(&D->num_sms, cudaDevAttrMultiProcessorCount, D->device));
+  // infinity-free int32 problems take the packed-key kernels: no entry is INF,
+  // so no table is, and every cell sum stays below (maxsum << 3) + 7 < 2^32
+  static const bool nf_off = std::getenv("GBE_NO_NF") != nullptr;  // A/B knob
+  const bool noinf = !nf_off && !p.is_f64() && !P.ex.sumprod && !p.has_inf && p.maxsum < (int64_t(1) << 29) - 1;
   // descriptors with the per-rank input shifts (row-sharded messages kept local)
   D->h_desc.resize(P.tasks.size());
   D->launch.resize(P.tasks.size());
   D->h_fast.resize(P.tasks.size());
   D->fl.resize(P.tasks.size());
   D->use_fast.assign(P.tasks.size(), 0);
+  D->task_merges.assign(P.tasks.size(), {});
+  D->in_map.assign(P.tasks.size(), {});
   for (size_t ti = 0; ti < P.tasks.size(); ti++) {
     const Task &t = P.tasks[ti];
     gbe_bucket_desc h = t.desc;
@@ -301,9 +455,11 @@ static DevPlan *dev_plan(gbe_plan *gp) {
         if (src.shard.on && !src.shard.gather) h.shift[j] = src.shard.lo;
       }
     }
+    plan_merges(P, D, ti, h, noinf);
     D->h_desc[ti] = h;
     D->launch[ti] = bk_plan_launch(h, t.shard.lo, t.shard.hi, P.ex.kernel, D->num_sms);
-    if (P.ex.kernel != 0 && bkf_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_fast[ti], D->fl[ti])) {
+    if (P.ex.kernel != 0 &&
+        bkf_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_fast[ti], D->fl[ti], noinf)) {
       D->use_fast[ti] = 1;
       D->launch[ti].variant = 1;
     }
@@ -312,6 +468,9 @@ static DevPlan *dev_plan(gbe_plan *gp) {
   if (!P.tasks.empty())
     CK(cudaMemcpy(D->d_fast, D->h_fast.data(), sizeof(FastDesc) * P.tasks.size(), cudaMemcpyHostToDevice));
   size_t nt = std::max<size_t>(P.tasks.size(), 1);
+  CK(cudaMalloc(&D->d_mdesc, sizeof(gbe_bucket_desc) * std::max<size_t>(D->merges.size(), 1)));
+  for (size_t mi = 0; mi < D->merges.size(); mi++)
+    CK(cudaMemcpy(D->d_mdesc + mi, &D->merges[mi].h, sizeof(gbe_bucket_desc), cudaMemcpyHostToDevice));
   CK(cudaMalloc(&D->d_desc, sizeof(gbe_bucket_desc) * nt));
   if (!P.tasks.empty())
     CK(cudaMemcpy(D->d_desc, D->h_desc.data(), sizeof(gbe_bucket_desc) * P.tasks.size(), cudaMemcpyHostToDevice));
@@ -489,13 +648,18 @@ static void run_util(RunImpl &R) {
   }
   R.d_sorted = R.base + R.A->off_sorted;
   const bool want_arg = (!R.mbe && P.ex.retain >= 1) || P.ex.retain >= 2;
-  std::vector<InPtrs> ins(nt);
+  std::vector<InPtrs> ins(nt), mins(D->merges.size());
   std::vector<void *> gathered_src(nt, nullptr);
   for (size_t ti = 0; ti < nt; ti++) {
     const Task &t = P.tasks[ti];
     R.out[ti] = R.base + R.A->off_out[ti];
     if (want_arg) R.arg[ti] = (uint8_t *)(R.base + R.A->off_arg[ti]);
-    for (int j = 0; j < t.desc.ninputs; j++) ins[ti].p[j] = R.member_ptr(t.members[j]);
+    const std::vector<int32_t> &map = D->in_map[ti];
+    for (size_t j = 0; j < map.size(); j++)
+      ins[ti].p[j] = map[j] >= 0 ? R.member_ptr(t.members[map[j]]) : R.base + R.A->off_merge[-(map[j] + 1)];
+    for (int32_t mi : D->task_merges[ti])
+      for (size_t q = 0; q < D->merges[mi].src.size(); q++)
+        mins[mi].p[q] = R.member_ptr(t.members[D->merges[mi].src[q]]);
     if (t.shard.on && t.shard.gather) {
       gathered_src[ti] = R.out[ti];
       R.full[ti] = R.base + R.A->off_full[ti];
@@ -595,6 +759,10 @@ static void run_util(RunImpl &R) {
       void *out = gathered_src[ti] ? gathered_src[ti] : R.base + R.A->off_out[ti];
       uint8_t *argp = want_arg ? (uint8_t *)(R.base + R.A->off_arg[ti]) : nullptr;
       if (P.ex.timing) rec(ev[2 * ti]);
+      for (int32_t mi : D->task_merges[ti]) {
+        const DevPlan::Merge &M = D->merges[mi];
+        CK(bk_launch(M.h, D->d_mdesc + mi, mins[mi], R.base + R.A->off_merge[mi], nullptr, 0, M.h.rows, M.li, st));
+      }
       if (D->use_fast[ti])
         CK(bkf_launch(D->d_fast + ti, D->fl[ti], ins[ti], out, argp, sh.lo, st));
       else

@@ -144,14 +144,19 @@ std::shared_ptr<Problem> problem_create(int32_t n, const int32_t *dom, int32_t n
       for (int64_t i = p->table_off[f]; i < p->table_off[f + 1]; i++) {
         int32_t &x = p->icost[i];
         if (x < 0) GBE_FAIL(GBE_E_INVALID, "function %d: negative cost %d", f, x);
-        if (x >= kInfI32) x = kInfI32;
-        else if (x > mx) mx = x;
+        if (x >= kInfI32) {
+          x = kInfI32;
+          p->has_inf = true;
+        } else if (x > mx) {
+          mx = x;
+        }
       }
       maxsum += mx;
     }
     // A9: exactness of saturating arithmetic needs finite sums < 2^30
     if (maxsum >= kInfI32)
       GBE_FAIL(GBE_E_INVALID, "sum of the largest finite costs (%lld) >= 2^30", (long long)maxsum);
+    p->maxsum = maxsum;
   } else {
     const double *c = (const double *)costs;
     p->fcost.assign(c, c + tot);
