@@ -600,6 +600,11 @@ __global__ void __launch_bounds__((NG * kGroupWarps + 1) * 32, 1)
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);  // input stage free
     fence_proxy_async_smem();                             // staged rows -> async proxy
+    // the staging buffer the NEXT tile writes was last stored kOutBufs - 1
+    // tiles ago: its bulk store must have finished reading before this
+    // barrier releases the group (the barrier orders the wait before every
+    // writer of the next tile)
+    if (ctid == 0) bulk_wait_read<kOutBufs - 2>();
     group_sync(bar_id);
     if (ctid < 32) {  // first warp of the group: aligned interior by TMA bulk stores, ragged ends plainly
       T *gout = out + o0;
@@ -619,13 +624,7 @@ __global__ void __launch_bounds__((NG * kGroupWarps + 1) * 32, 1)
         if (ctid < ha) ga[ctid] = args[ctid];
         if (ctid < tla) ga[ha + nmida + ctid] = args[ha + nmida + ctid];
       }
-      if (ctid == 0) {
-        bulk_commit();
-        // staging buffer of this group's tile (i - kOutBufs + 1) is free once
-        // its store has read it; ordered before that buffer's next writers by
-        // the next group_sync
-        bulk_wait_read<kOutBufs - 1>();
-      }
+      if (ctid == 0) bulk_commit();
     }
     s += NG;
     if (s >= nst) {
@@ -708,7 +707,10 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
   // tiny buckets: the tiled kernel's per-CTA setup (descriptor copy, offset
   // tables, mbarrier ring) costs more than the bucket; bk_generic is faster
   if ((row_end - row_begin) * DV < kMinCells) return false;
-  const int64_t kPLMax = 16384;
+  static const int64_t kPLMax = [] {  // rows per tile cap (GBE_FAST_PLMAX: tuning knob)
+    const char *e = std::getenv("GBE_FAST_PLMAX");
+    return e ? std::max<int64_t>(8, std::atoll(e)) : int64_t(16384);
+  }();
   // one CTA per SM: dynamic shared-memory budget; GBE_FAST_SMEM_KB overrides
   // it for tuning experiments
   static const char *smem_env = std::getenv("GBE_FAST_SMEM_KB");
@@ -775,7 +777,7 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     if (row_begin % PL || row_end % PL) continue;
     const int NG = ng_of(es, R, R2, DV);
     const size_t kSmemMax = (size_t)(smem_env ? std::atoi(smem_env) : (NG == 2 ? 200 : 196)) * 1024;
-    const int min_st = pass == 0 ? std::max(kStagesWant, NG + 1) : NG + 1;
+    const int min_st = pass == 0 ? std::max(kStagesWant, 2 * NG) : NG;
     // classes
     std::memset(&F, 0, sizeof(F));
     FastHot &f = F.hot;
@@ -851,9 +853,14 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     f.out_bytes = (int32_t)(((size_t)PL * es + 16 + 127) & ~size_t(127));
     f.arg_bytes = (int32_t)(((size_t)PL + 16 + 127) & ~size_t(127));
     size_t fixed = (size_t)NG * kOutBufs * ((size_t)f.out_bytes + f.arg_bytes) + (size_t)(k + 1) * Pmid * 4 + 256;
-    int nst = kStagesMax;
-    while (nst > min_st && fixed + nst * off > kSmemMax) nst--;
-    if (fixed + nst * off > kSmemMax) continue;
+    // the ring length is a multiple of NG: stage s then always serves group
+    // s mod NG, so a group waiting on a stage has consumed that stage's
+    // previous round itself and the mbarrier parity wait cannot alias a
+    // phase two rounds back (with an odd ring a group could wait on a stage
+    // whose previous round, the other group's, was not even issued yet)
+    int nst = kStagesMax - kStagesMax % NG;
+    while (nst > min_st && fixed + nst * off > kSmemMax) nst -= NG;
+    if (nst < NG || fixed + nst * off > kSmemMax) continue;
     f.nstages = nst;
     off = nst * off;
     f.off_out = (int32_t)off;

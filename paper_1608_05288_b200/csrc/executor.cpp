@@ -762,12 +762,27 @@ static void run_util(RunImpl &R) {
       for (int32_t mi : D->task_merges[ti]) {
         const DevPlan::Merge &M = D->merges[mi];
         CK(bk_launch(M.h, D->d_mdesc + mi, mins[mi], R.base + R.A->off_merge[mi], nullptr, 0, M.h.rows, M.li, st));
+        static const bool sync_m = std::getenv("GBE_SYNC_EACH") != nullptr;  // debugging knob
+        if (sync_m && !capturing) {
+          cudaError_t e = cudaStreamSynchronize(st);
+          if (e != cudaSuccess)
+            GBE_FAIL(GBE_E_CUDA, "merge %d of task %zu (rows %lld, k %d): %s", mi, ti, (long long)M.h.rows,
+                     M.h.ninputs, cudaGetErrorString(e));
+        }
       }
       if (D->use_fast[ti])
         CK(bkf_launch(D->d_fast + ti, D->fl[ti], ins[ti], out, argp, sh.lo, st));
       else
         CK(bk_launch(D->h_desc[ti], D->d_desc + ti, ins[ti], out, argp, sh.lo, sh.hi, D->launch[ti], st));
       if (P.ex.timing) rec(ev[2 * ti + 1]);
+      static const bool sync_each = std::getenv("GBE_SYNC_EACH") != nullptr;  // debugging knob
+      if (sync_each && !capturing) {
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess)
+          GBE_FAIL(GBE_E_CUDA, "task %zu (x%d, %zu merges, fast=%d nst=%d PL=%d k=%d): %s", ti, t.var,
+                   D->task_merges[ti].size(), (int)D->use_fast[ti], D->h_fast[ti].hot.nstages,
+                   D->h_fast[ti].hot.PL, D->h_fast[ti].hot.k, cudaGetErrorString(e));
+      }
       if (gathered_src[ti]) {
         if (!g_ag) GBE_FAIL(GBE_E_COMM, "bucket x%d is row-sharded but no all-gather hook is set", t.var);
         size_t bytes = el * (size_t)(sh.per * sh.block_rows);
