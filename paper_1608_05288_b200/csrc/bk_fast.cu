@@ -39,7 +39,7 @@ namespace {
 
 constexpr uint32_t kInf = GBE_INF_I32;
 constexpr int kMaxStages = 8;
-constexpr int kOutBufs = 2;
+constexpr int kOutBufsMax = 3;  // output staging buffers per consumer group (2 or 3)
 constexpr int64_t kMinCells = 1 << 10;  // measured: the tiled kernel beats bk_generic from ~1e3 cells
 constexpr int kGroupWarps = 8;  // warps per consumer group
 constexpr int kSmemCap = 200 * 1024;  // dynamic shared memory cap per CTA
@@ -153,9 +153,6 @@ __device__ __forceinline__ void bulk_wait_read() {
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-}
-__device__ __forceinline__ void group_sync(uint32_t id) {  // named barrier over one consumer group
-  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "n"(kGroupWarps * 32) : "memory");
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -370,9 +367,9 @@ __device__ __forceinline__ void combine_nf(const uint32_t (&P0)[DV], const uint3
 // nstages - 2 tiles in flight per SM).  Each group stages its rows in its own
 // output buffers and stores them with TMA bulk copies.
 template <typename T, int R, int R2, int DV, bool SP, bool NF, int NG>
-// (registers: 17 warps put 5 on one SM sub-partition, so NG = 2 gets 96 per
+// (registers: 18 warps put 5 on one SM sub-partition, so NG = 2 gets 96 per
 // thread; NG = 1 gets 168)
-__global__ void __launch_bounds__((NG * kGroupWarps + 1) * 32, 1)
+__global__ void __launch_bounds__((NG * kGroupWarps + 2) * 32, 1)
     bk_fast_kernel(const FastDesc *__restrict__ Fg, InPtrs in, T *__restrict__ out,
                    uint8_t *__restrict__ arg, int64_t row_begin, int64_t t_begin, int64_t t_end) {
   using S = SrF<T>;
@@ -383,6 +380,11 @@ __global__ void __launch_bounds__((NG * kGroupWarps + 1) * 32, 1)
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ int32_t sbase[kMaxStages * 32];
   __shared__ int64_t rowstart[kMaxStages];
+  // output staging handshake: ofull[g][b] completes when the 8 warps of group
+  // g have staged a tile in buffer b; oempty[g][b] when its bulk store has
+  // read it; ostart[g][b] = that tile's first output row (relative)
+  __shared__ uint64_t ofull[NG][kOutBufsMax], oempty[NG][kOutBufsMax];
+  __shared__ int64_t ostart[NG][kOutBufsMax];
   __shared__ ProdSmem ps;  // producer's decode tables
   for (int i = threadIdx.x; i < kMaxH * 32; i += blockDim.x) ps.hstr[i / 32][i % 32] = Fg->hstr[i / 32][i % 32];
   if (threadIdx.x < kMaxH) {
@@ -400,6 +402,11 @@ __global__ void __launch_bounds__((NG * kGroupWarps + 1) * 32, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kGroupWarps);
     }
+    for (int g = 0; g < NG; g++)
+      for (int b = 0; b < kOutBufsMax; b++) {
+        mbar_init(&ofull[g][b], kGroupWarps);
+        mbar_init(&oempty[g][b], 1);
+      }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -440,11 +447,56 @@ __global__ void __launch_bounds__((NG * kGroupWarps + 1) * 32, 1)
     }
     return;
   }
+  const int PL = f.PL, es = (int)sizeof(T);
+  const int nob = f.nout;
+
+  if (warp == NG * kGroupWarps + 1) {  // ---- storer warp: TMA bulk stores of staged tiles ----
+    // tiles in CTA order (tile i: group i mod NG, its buffer (i / NG) mod nob);
+    // the buffer of tile i - 1 is released once tile i is committed and at
+    // most one store group is still reading shared memory
+    const int lane = threadIdx.x & 31;
+    int i = 0, pg = -1, pb = 0;
+    for (int64_t t = t_begin + blockIdx.x; t < t_end; t += gridDim.x, i++) {
+      const int g = i % NG, jg = i / NG, b = jg % nob;
+      mbar_wait(&ofull[g][b], (uint32_t)((jg / nob) & 1));
+      const int64_t o0 = ostart[g][b];
+      T *outs = (T *)(sm + f.off_out + (g * nob + b) * f.out_bytes) + (int)((((uintptr_t)(out + o0)) & 15) / es);
+      uint8_t *args = sm + f.off_arg + (g * nob + b) * f.arg_bytes + (int)(((uintptr_t)(arg + o0)) & 15);
+      T *gout = out + o0;
+      const int h = (int)(((16 - (((uintptr_t)gout) & 15)) & 15) / es);
+      const int hh = min(h, PL);
+      const int nmid = ((PL - hh) * es / 16) * 16 / es;
+      const int tl = PL - hh - nmid;
+      if (lane == 0 && nmid > 0) tma_store_1d(gout + hh, outs + hh, (uint32_t)(nmid * es));
+      if (lane < hh) gout[lane] = outs[lane];
+      if (lane < tl) gout[hh + nmid + lane] = outs[hh + nmid + lane];
+      if (arg) {
+        uint8_t *ga = arg + o0;
+        const int ha = min((int)((16 - (((uintptr_t)ga) & 15)) & 15), PL);
+        const int nmida = ((PL - ha) / 16) * 16;
+        const int tla = PL - ha - nmida;
+        if (lane == 0 && nmida > 0) tma_store_1d(ga + ha, args + ha, (uint32_t)nmida);
+        if (lane < ha) ga[lane] = args[lane];
+        if (lane < tla) ga[ha + nmida + lane] = args[ha + nmida + lane];
+      }
+      __syncwarp();  // ragged ends read before the buffer is released
+      if (lane == 0) {
+        bulk_commit();
+        if (pg >= 0) {
+          bulk_wait_read<1>();
+          mbar_arrive(&oempty[pg][pb]);
+        }
+      }
+      pg = g;
+      pb = b;
+    }
+    if (lane == 0) bulk_wait_all();
+    return;
+  }
 
   // ---- consumer groups ----
   const int g = warp / kGroupWarps;
   const int ctid = threadIdx.x - g * kGT;  // 0 .. kGT-1 inside the group
-  const int PL = f.PL, es = (int)sizeof(T);
   const int c0 = f.cls_off[0], c1 = f.cls_off[1], c2 = f.cls_off[2], c3 = f.cls_off[3], c4 = f.cls_off[4];
   const int sel = (c2 > c1 ? 1 : 0) | (c3 > c2 ? 2 : 0) | (c4 > c3 ? 4 : 0);
   int loff[R][R2];  // in-tile row offsets of the group digits (tile-invariant)
@@ -452,13 +504,14 @@ __global__ void __launch_bounds__((NG * kGroupWarps + 1) * 32, 1)
   for (int a = 0; a < R; a++)
 #pragma unroll
     for (int bb = 0; bb < R2; bb++) loff[a][bb] = a * f.rs1 + bb * f.rs2;
-  unsigned char *const obase = sm + f.off_out + g * kOutBufs * f.out_bytes;
-  unsigned char *const abase = sm + f.off_arg + g * kOutBufs * f.arg_bytes;
-  const uint32_t bar_id = 1 + g;
+  unsigned char *const obase = sm + f.off_out + g * nob * f.out_bytes;
+  unsigned char *const abase = sm + f.off_arg + g * nob * f.arg_bytes;
+  uint32_t oph = 0;  // use round of the group's staging buffers (parity)
   int s = g % nst, b = 0;
   uint32_t ph = (uint32_t)((g / nst) & 1);
   for (int64_t t = t_begin + blockIdx.x + (int64_t)g * gridDim.x; t < t_end; t += (int64_t)NG * gridDim.x) {
     mbar_wait(&full[s], ph);
+    mbar_wait(&oempty[g][b], oph ^ 1u);  // staging buffer b: previous store has read it
     const int32_t *sb = sbase + s * 32;
     const int64_t o0 = rowstart[s] - row_begin;
     // staging: element l of this tile lives at index l + sh (16-byte phase of
@@ -599,41 +652,22 @@ __global__ void __launch_bounds__((NG * kGroupWarps + 1) * 32, 1)
     }
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);  // input stage free
-    fence_proxy_async_smem();                             // staged rows -> async proxy
-    // the staging buffer the NEXT tile writes was last stored kOutBufs - 1
-    // tiles ago: its bulk store must have finished reading before this
-    // barrier releases the group (the barrier orders the wait before every
-    // writer of the next tile)
-    if (ctid == 0) bulk_wait_read<kOutBufs - 2>();
-    group_sync(bar_id);
-    if (ctid < 32) {  // first warp of the group: aligned interior by TMA bulk stores, ragged ends plainly
-      T *gout = out + o0;
-      const int h = (int)(((16 - (((uintptr_t)gout) & 15)) & 15) / es);
-      const int hh = min(h, PL);
-      const int nmid = ((PL - hh) * es / 16) * 16 / es;
-      const int tl = PL - hh - nmid;
-      if (ctid == 0 && nmid > 0) tma_store_1d(gout + hh, outs + hh, (uint32_t)(nmid * es));
-      if (ctid < hh) gout[ctid] = outs[ctid];
-      if (ctid < tl) gout[hh + nmid + ctid] = outs[hh + nmid + ctid];
-      if (arg) {
-        uint8_t *ga = arg + o0;
-        const int ha = min((int)((16 - (((uintptr_t)ga) & 15)) & 15), PL);
-        const int nmida = ((PL - ha) / 16) * 16;
-        const int tla = PL - ha - nmida;
-        if (ctid == 0 && nmida > 0) tma_store_1d(ga + ha, args + ha, (uint32_t)nmida);
-        if (ctid < ha) ga[ctid] = args[ctid];
-        if (ctid < tla) ga[ha + nmida + ctid] = args[ha + nmida + ctid];
-      }
-      if (ctid == 0) bulk_commit();
+    fence_proxy_async_smem();  // staged rows -> async proxy (the storer's bulk copy)
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      if (ctid == 0) ostart[g][b] = o0;
+      mbar_arrive(&ofull[g][b]);
     }
     s += NG;
     if (s >= nst) {
       s -= nst;
       ph ^= 1u;
     }
-    if (++b == kOutBufs) b = 0;
+    if (++b == nob) {
+      b = 0;
+      oph ^= 1u;
+    }
   }
-  if (ctid == 0) bulk_wait_all();
 }
 
 // ---------------------------------------------------------------------------
@@ -852,7 +886,18 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     f.stage_bytes = (int32_t)off;
     f.out_bytes = (int32_t)(((size_t)PL * es + 16 + 127) & ~size_t(127));
     f.arg_bytes = (int32_t)(((size_t)PL + 16 + 127) & ~size_t(127));
-    size_t fixed = (size_t)NG * kOutBufs * ((size_t)f.out_bytes + f.arg_bytes) + (size_t)(k + 1) * Pmid * 4 + 256;
+    // 3 staging buffers when they fit beside the wanted ring (the store of
+    // a tile then has a whole tile of compute to drain), else 2
+    const size_t tabs = (size_t)(k + 1) * Pmid * 4 + 256;
+    const size_t obuf = (size_t)NG * ((size_t)f.out_bytes + f.arg_bytes);
+    static const int kNob = [] {  // GBE_FAST_NOUT: tuning knob (2 or 3)
+      const char *e = std::getenv("GBE_FAST_NOUT");
+      return e ? std::max(2, std::min(kOutBufsMax, std::atoi(e))) : kOutBufsMax;
+    }();
+    int nob = kNob;
+    while (nob > 2 && obuf * nob + tabs + (size_t)min_st * off > kSmemMax) nob--;
+    f.nout = nob;
+    size_t fixed = obuf * nob + tabs;
     // the ring length is a multiple of NG: stage s then always serves group
     // s mod NG, so a group waiting on a stage has consumed that stage's
     // previous round itself and the mbarrier parity wait cannot alias a
@@ -864,9 +909,9 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     f.nstages = nst;
     off = nst * off;
     f.off_out = (int32_t)off;
-    off += (size_t)NG * kOutBufs * f.out_bytes;
+    off += (size_t)NG * nob * f.out_bytes;
     f.off_arg = (int32_t)off;
-    off += (size_t)NG * kOutBufs * f.arg_bytes;
+    off += (size_t)NG * nob * f.arg_bytes;
     f.off_tab = (int32_t)off;
     off += (size_t)k * Pmid * 4;
     f.off_mrow = (int32_t)off;
@@ -878,7 +923,7 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     L.g1 = g1;
     L.g2 = g2;
     L.nf = noinf && es == 4 && h.semiring == GBE_MINSUM_I32;
-    L.block = (NG * kGroupWarps + 1) * 32;
+    L.block = (NG * kGroupWarps + 2) * 32;
     L.t_begin = row_begin / PL;
     L.t_end = row_end / PL;
     int per_sm = (int)std::min<size_t>(std::max<size_t>(1, (220 * 1024) / (off + 4096)), 2048 / L.block);
