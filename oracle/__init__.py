@@ -60,6 +60,12 @@ def lib():
                                         I32P, ctypes.c_int64, ctypes.c_int64, F64P, ctypes.c_int32]
         L.or_solve_sumprod.argtypes = [PP, I32P, ctypes.c_int32, ctypes.c_int32]
         L.or_solve_sumprod.restype = ctypes.c_void_p
+        L.or_solve_count.argtypes = [PP, I32P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
+        L.or_solve_count.restype = ctypes.c_void_p
+        L.or_run_count.argtypes = [ctypes.c_void_p]
+        L.or_run_count.restype = ctypes.c_double
+        L.or_run_table_count.argtypes = [ctypes.c_void_p, ctypes.c_int32, F64P]
+        L.or_run_table_count.restype = ctypes.c_int32
         L.or_run_status.argtypes = [ctypes.c_void_p]
         L.or_run_status.restype = ctypes.c_int32
         L.or_run_ntables.argtypes = [ctypes.c_void_p]
@@ -235,7 +241,7 @@ def bucket_eval_sp(dom, x, members, sep, row_begin=0, row_end=None, nthreads=0):
 
 
 class Table:
-    __slots__ = ("var", "mb", "sep", "rows", "dest", "members", "out", "arg", "digest")
+    __slots__ = ("var", "mb", "sep", "rows", "dest", "members", "out", "arg", "digest", "count")
 
 
 class Run:
@@ -243,15 +249,23 @@ class Run:
     assignment."""
 
     def __init__(self, inst, order, ibound=-1, keep_tables=True, nthreads=0, table_fn=None,
-                 sumprod=False):
+                 sumprod=False, count=None):
         """table_fn(t, table, out, arg), if given, receives each kept table
         instead of the Run storing a copy (bounded memory for big runs).
-        sumprod: exact BE in the sum-product semiring (f64; value = -log Z)."""
+        sumprod: exact BE in the sum-product semiring (f64; value = -log Z).
+        count: "optimal" / "consistent" -- exact BE in the (min, count)
+        semiring; .count = number of optimal / consistent solutions and every
+        kept table gets .count (doubles)."""
         self.inst = inst
         self._P = Problem(inst)
         self.order = np.ascontiguousarray(order, dtype=np.int32)
         L = lib()
-        if sumprod:
+        if count is not None:
+            if ibound >= 0 or count not in ("optimal", "consistent"):
+                raise ValueError("counting oracle: exact BE, count = 'optimal' or 'consistent'")
+            h = L.or_solve_count(self._P.ref, _p(self.order, ctypes.c_int32), int(count == "consistent"),
+                                 int(bool(keep_tables)), int(nthreads))
+        elif sumprod:
             if not inst.is_f64 or ibound >= 0:
                 raise ValueError("sum-product oracle: f64 problems, exact BE only")
             h = L.or_solve_sumprod(self._P.ref, _p(self.order, ctypes.c_int32),
@@ -278,7 +292,11 @@ class Run:
                     L.or_run_table_members(h, t, _p(kind, ctypes.c_int32), _p(idx, ctypes.c_int32))
                     T.members = [(int(kind[k]), int(idx[k])) for k in range(nmem.value)]
                     T.digest = int(L.or_run_table_digest(h, t))
-                    T.out, T.arg = None, None
+                    T.out, T.arg, T.count = None, None, None
+                    if keep_tables and count is not None:
+                        c = np.zeros(T.rows, dtype=np.float64)
+                        if L.or_run_table_count(h, t, _p(c, ctypes.c_double)):
+                            T.count = c
                     if keep_tables:
                         out = np.zeros(T.rows, dtype=np.float64 if inst.is_f64 else np.int32)
                         arg = np.zeros(T.rows, dtype=np.uint8)
@@ -298,6 +316,7 @@ class Run:
                 else:
                     self.value = int(L.or_run_value_i(h))
                     self.upper = int(L.or_run_upper_i(h))
+                self.count = float(L.or_run_count(h)) if count is not None else None
                 a = np.zeros(max(inst.n, 1), dtype=np.int32)
                 self.assignment = a[:inst.n].copy() if L.or_run_assignment(h, _p(a, ctypes.c_int32)) else None
                 if self.assignment is not None:
@@ -317,3 +336,10 @@ def solve_mbe(inst, order, ibound, keep_tables=True, nthreads=0) -> Run:
 def solve_sumprod(inst, order, keep_tables=True, nthreads=0) -> Run:
     """Exact BE in the sum-product semiring: .value = -log Z."""
     return Run(inst, order, -1, keep_tables, nthreads, sumprod=True)
+
+
+def solve_count(inst, order, count="optimal", keep_tables=True, nthreads=0) -> Run:
+    """Exact BE in the (min, count) semiring:
+    .count = number of optimal (count="optimal") or consistent
+    (count="consistent") solutions."""
+    return Run(inst, order, -1, keep_tables, nthreads, count=count)

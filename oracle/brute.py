@@ -132,3 +132,36 @@ def neg_log_z(inst, limit=2_000_000):
     if math.isinf(m):
         return math.inf
     return m - math.log(math.fsum(math.exp(m - c) for c in costs))
+
+
+def count_solutions(inst, limit=50_000_000):
+    """Counting by enumeration (P:245's "number of consistent solutions";
+    SURVEY §8(f) row 4): returns (optimum, number of assignments whose cost
+    equals the optimum, number of assignments of finite cost), the cost
+    being Eq. (1) computed as in brute_force_np.  An infeasible problem has
+    no optimal and no consistent assignment (counts 0, 0).  Exact Python
+    integers."""
+    import numpy as np
+    n = inst.n
+    dims = [int(inst.dom[v]) for v in range(n)]
+    space = int(np.prod(dims, dtype=np.int64)) if dims else 1
+    if space > limit:
+        raise ValueError(f"state space {space} exceeds limit {limit}")
+    idx = np.arange(space, dtype=np.int64)
+    vals = np.zeros((n, space), dtype=np.int64)
+    rem = idx.copy()
+    for pos in range(n - 1, -1, -1):
+        vals[pos] = rem % dims[pos]
+        rem //= dims[pos]
+    total = np.zeros(space, dtype=np.float64 if inst.is_f64 else np.int64)
+    for f in range(inst.nf):
+        k = np.zeros(space, dtype=np.int64)
+        for v in (int(x) for x in inst.scope(f)):
+            k = k * int(inst.dom[v]) + vals[v]
+        t = inst.table(f)[k]
+        total = total + t if inst.is_f64 else np.minimum(total + t.astype(np.int64), INF_I32)
+    finite = np.isfinite(total) if inst.is_f64 else total < INF_I32
+    opt = total.min()
+    n_cons = int(finite.sum())
+    n_opt = int((total == opt).sum()) if n_cons else 0
+    return (float(opt) if inst.is_f64 else int(opt)), n_opt, n_cons

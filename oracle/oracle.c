@@ -260,6 +260,85 @@ void or_bucket_rows_sp(const int32_t *dom, int32_t n, int32_t x, int32_t nmem,
   }
 }
 
+/* Counting bucket ("as a byproduct ... BE can
+ * compute the number of consistent solutions").  The (min, count)
+ * semiring: every member carries a count table beside its cost table
+ * (ctab[k] == NULL for an original function: every entry counts 1).  For
+ * theta.v the cost s_v is the sum of or_bucket_rows and c_v = prod_k
+ * count_k(theta.v) (doubles, member order).  The row keeps
+ *     out   = min_v s_v                     (first minimiser in arg, A8)
+ *     count = sum over v = 0..d-1 with s_v == out of c_v
+ * and count = 0 when the minimum is infinite (no finite completion).
+ * consistent = 1 reads every finite member entry as cost 0: s_v is then 0
+ * or infinite and count is the number of consistent completions. */
+void or_bucket_rows_cnt(const int32_t *dom, int32_t n, int32_t is_f64, int32_t x,
+                        int32_t nmem, const int32_t *mar, const int64_t *moff,
+                        const int32_t *mscope, const int32_t *const *itab,
+                        const double *const *ftab, const double *const *ctab,
+                        int32_t consistent, int32_t nsep, const int32_t *sep,
+                        int64_t row_begin, int64_t row_end, int32_t *out_i,
+                        double *out_f, double *out_c, uint8_t *arg, int32_t nthreads) {
+#ifdef _OPENMP
+  if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel num_threads(nthreads)
+#endif
+  {
+    int32_t *a = (int32_t *)calloc(n ? n : 1, sizeof(int32_t));
+    int64_t *si = (int64_t *)malloc(sizeof(int64_t) * (dom[x] ? dom[x] : 1));
+    double *sf = (double *)malloc(sizeof(double) * (dom[x] ? dom[x] : 1));
+    double *c = (double *)malloc(sizeof(double) * (dom[x] ? dom[x] : 1));
+#ifdef _OPENMP
+#pragma omp for schedule(static)
+#endif
+    for (int64_t row = row_begin; row < row_end; row++) {
+      int64_t r = row;
+      for (int q = nsep - 1; q >= 0; q--) {
+        a[sep[q]] = (int32_t)(r % dom[sep[q]]);
+        r /= dom[sep[q]];
+      }
+      for (int v = 0; v < dom[x]; v++) {
+        a[x] = v;
+        si[v] = 0;
+        sf[v] = 0.0;
+        c[v] = 1.0;
+        for (int k = 0; k < nmem; k++) {
+          const int32_t *sc = mscope + moff[k];
+          int64_t idx = 0;
+          for (int q = 0; q < mar[k]; q++) idx = idx * dom[sc[q]] + a[sc[q]];
+          if (is_f64) {
+            double f = ftab[k][idx];
+            if (consistent && f < INFINITY) f = 0.0;
+            sf[v] = sf[v] + f;
+          } else {
+            int32_t f = itab[k][idx];
+            if (consistent && f < OR_INF_I32) f = 0;
+            si[v] = add_i(si[v], f);
+          }
+          if (ctab[k]) c[v] = c[v] * ctab[k][idx];
+        }
+      }
+      int best_v = 0;
+      for (int v = 1; v < dom[x]; v++)
+        if (is_f64 ? sf[v] < sf[best_v] : si[v] < si[best_v]) best_v = v;
+      const int inf = is_f64 ? !(sf[best_v] < INFINITY) : si[best_v] >= OR_INF_I32;
+      double cnt = 0.0;
+      if (!inf)
+        for (int v = 0; v < dom[x]; v++)
+          if (is_f64 ? sf[v] == sf[best_v] : si[v] == si[best_v]) cnt = cnt + c[v];
+      if (is_f64)
+        out_f[row - row_begin] = sf[best_v];
+      else
+        out_i[row - row_begin] = (int32_t)si[best_v];
+      out_c[row - row_begin] = cnt;
+      if (arg) arg[row - row_begin] = (uint8_t)best_v;
+    }
+    free(c);
+    free(sf);
+    free(si);
+    free(a);
+  }
+}
+
 /* ------------------------------------------------------------------ */
 /* whole solve: Alg. 1 (BE) / Alg. 2 (MBE)                              */
 
@@ -275,6 +354,7 @@ typedef struct {
   int64_t rows;
   int32_t *out_i;
   double *out_f;
+  double *out_c; /* counting mode: completions attaining out */
   uint8_t *arg;
   uint64_t digest;
 } otable;
@@ -292,6 +372,7 @@ struct or_run {
   double value_f, upper_f;
   int32_t have_assign;
   int32_t *assign;
+  double count; /* counting mode: number of optimal (or consistent) solutions */
 };
 
 static void ml_push(mlist *l, int32_t kind, int32_t index) {
@@ -326,7 +407,9 @@ static int cmp_by_pos(const void *a, const void *b) {
 }
 
 static or_run *or_solve_impl(const or_problem *p, const int32_t *order, int32_t ibound,
-                             int32_t keep_tables, int32_t nthreads, int32_t sumprod) {
+                             int32_t keep_tables, int32_t nthreads, int32_t mode) {
+  /* mode: 0 min-sum, 1 sum-product, 2 count optimal, 3 count consistent */
+  const int sumprod = mode == 1, counting = mode >= 2;
   int n = p->n;
   or_run *r = (or_run *)calloc(1, sizeof(or_run));
   r->is_f64 = p->is_f64;
@@ -480,7 +563,14 @@ static or_run *or_solve_impl(const or_problem *p, const int32_t *order, int32_t 
         it[k] = p->is_f64 ? NULL : mem_itab(p, r, t.mem[k]);
         ft[k] = p->is_f64 ? mem_ftab(p, r, t.mem[k]) : NULL;
       }
-      if (sumprod) {
+      if (counting) {
+        const double **ct = (const double **)malloc(sizeof(void *) * (t.nmem ? t.nmem : 1));
+        for (int k = 0; k < t.nmem; k++) ct[k] = t.mem[k].kind == 1 ? r->tab[t.mem[k].index].out_c : NULL;
+        t.out_c = (double *)malloc(sizeof(double) * t.rows);
+        or_bucket_rows_cnt(p->dom, n, p->is_f64, x, t.nmem, mar, moff, msc, it, ft, ct, mode == 3,
+                           t.nsep, t.sep, 0, t.rows, t.out_i, t.out_f, t.out_c, t.arg, nthreads);
+        free(ct);
+      } else if (sumprod) {
         or_bucket_rows_sp(p->dom, n, x, t.nmem, mar, moff, msc, ft, t.nsep, t.sep, 0, t.rows,
                           t.out_f, nthreads);
         memset(t.arg, 0, t.rows); /* no argmin in the sum-product semiring */
@@ -523,8 +613,10 @@ static or_run *or_solve_impl(const or_problem *p, const int32_t *order, int32_t 
           otable *c = &r->tab[B->m[k].index];
           free(c->out_i);
           free(c->out_f);
+          free(c->out_c);
           c->out_i = NULL;
           c->out_f = NULL;
+          c->out_c = NULL;
         }
   }
 
@@ -542,11 +634,29 @@ static or_run *or_solve_impl(const or_problem *p, const int32_t *order, int32_t 
     }
     r->value_i = vi;
     r->value_f = vf;
+    if (counting) {
+      /* counting: the components' counts multiply (P:639-640 for the costs);
+       * an original constant is one assignment of no variable (count 1) */
+      if (mode == 3) { /* consistent: every finite constant reads as 0 */
+        int inf = 0;
+        for (int k = 0; k < constants.n; k++) {
+          member m = constants.m[k];
+          if (p->is_f64 ? !(mem_ftab(p, r, m)[0] < INFINITY) : mem_itab(p, r, m)[0] >= OR_INF_I32) inf = 1;
+        }
+        r->value_i = inf ? OR_INF_I32 : 0;
+        r->value_f = inf ? INFINITY : 0.0;
+      }
+      double cnt = 1.0;
+      for (int k = 0; k < constants.n; k++)
+        if (constants.m[k].kind == 1) cnt = cnt * r->tab[constants.m[k].index].out_c[0];
+      const int inf = p->is_f64 ? !(r->value_f < INFINITY) : r->value_i >= OR_INF_I32;
+      r->count = inf ? 0.0 : cnt;
+    }
 
     /* Value assignment phase (Alg. 1 lines 6-7; MBE: Example 4,
      * P:341, reading A7): for x = first..last pick the value minimising the
      * sum of ALL functions of B_x (canonical order) given earlier values. */
-    if (keep_tables && !sumprod) {
+    if (keep_tables && !sumprod && mode != 3) {
       int32_t *a = r->assign;
       for (int i = 0; i < n; i++) {
         int x = order[i];
@@ -647,6 +757,7 @@ void or_run_free(or_run *r) {
     free(r->tab[t].mem);
     free(r->tab[t].out_i);
     free(r->tab[t].out_f);
+    free(r->tab[t].out_c);
     free(r->tab[t].arg);
   }
   free(r->tab);
@@ -706,6 +817,19 @@ double or_evaluate_f(const or_problem *p, const int32_t *assign) {
 or_run *or_solve(const or_problem *p, const int32_t *order, int32_t ibound,
                  int32_t keep_tables, int32_t nthreads) {
   return or_solve_impl(p, order, ibound, keep_tables, nthreads, 0);
+}
+
+or_run *or_solve_count(const or_problem *p, const int32_t *order, int32_t consistent,
+                       int32_t keep_tables, int32_t nthreads) {
+  return or_solve_impl(p, order, -1, keep_tables, nthreads, consistent ? 3 : 2);
+}
+
+double or_run_count(const or_run *r) { return r->count; }
+
+int32_t or_run_table_count(const or_run *r, int32_t t, double *out_c) {
+  if (!r->tab[t].out_c) return 0;
+  memcpy(out_c, r->tab[t].out_c, sizeof(double) * r->tab[t].rows);
+  return 1;
 }
 
 or_run *or_solve_sumprod(const or_problem *p, const int32_t *order, int32_t keep_tables,

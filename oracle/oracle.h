@@ -84,6 +84,20 @@ void or_bucket_rows_sp(const int32_t *dom, int32_t n, int32_t x, int32_t nmem,
                        const double *const *ftab, int32_t nsep, const int32_t *sep,
                        int64_t row_begin, int64_t row_end, double *out_f, int32_t nthreads);
 
+/* Counting variant of the bucket: the (min,
+ * count) semiring.  ctab[k] = member k's count table (NULL: an original,
+ * every entry 1).  out = min_v s_v (arg = first minimiser), out_c = sum of
+ * prod_k count_k over the v attaining it (0 if the minimum is infinite).
+ * consistent = 1 reads every finite member entry as cost 0, so out_c counts
+ * the consistent completions. */
+void or_bucket_rows_cnt(const int32_t *dom, int32_t n, int32_t is_f64, int32_t x,
+                        int32_t nmem, const int32_t *mar, const int64_t *moff,
+                        const int32_t *mscope, const int32_t *const *itab,
+                        const double *const *ftab, const double *const *ctab,
+                        int32_t consistent, int32_t nsep, const int32_t *sep,
+                        int64_t row_begin, int64_t row_end, int32_t *out_i,
+                        double *out_f, double *out_c, uint8_t *arg, int32_t nthreads);
+
 /* ---- whole solve: BE (ibound < 0) or MBE(ibound) (Alg. 1, Alg. 2) ----- */
 typedef struct or_run or_run;
 /* keep_tables: 1 keeps every (mini-)bucket table and argmin for inspection
@@ -98,6 +112,16 @@ or_run *or_solve(const or_problem *p, const int32_t *order, int32_t ibound,
  * tables are all zero. */
 or_run *or_solve_sumprod(const or_problem *p, const int32_t *order, int32_t keep_tables,
                          int32_t nthreads);
+/* Exact BE in the (min, count) semiring:
+ * consistent = 0 counts the optimal assignments (value = the optimum),
+ * consistent = 1 the assignments of finite cost (value 0, or INF when there
+ * is none).  Counts are doubles (exact integers below 2^53). */
+or_run *or_solve_count(const or_problem *p, const int32_t *order, int32_t consistent,
+                       int32_t keep_tables, int32_t nthreads);
+/* number of optimal / consistent solutions of a counting run */
+double or_run_count(const or_run *r);
+/* count table of table t (counting runs, kept tables); 0 if unavailable */
+int32_t or_run_table_count(const or_run *r, int32_t t, double *out_c);
 /* 0 ok; 1 invalid i-bound (a member cannot fit, A5/A6); 2 out of memory */
 int32_t or_run_status(const or_run *r);
 int32_t or_run_ntables(const or_run *r);

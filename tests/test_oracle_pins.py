@@ -505,3 +505,79 @@ def test_sumprod_bucket_rows_special_cases():
         assert _close(out2[r], -logsumexp(-(t[r * 6:(r + 1) * 6] + u[b * 6:(b + 1) * 6])), 1e-13)
     one = oracle.bucket_eval_sp([3, 1], 1, [([0, 1], np.array([1.5, 2.0, 7.0]))], [0])
     np.testing.assert_array_equal(one, [1.5, 2.0, 7.0])
+
+
+# ------------------------------------------ solution counting (§8(f) row 4)
+# "as a byproduct ... BE can compute the number of consistent
+# solutions".  The (min, count) semiring: count = number of optimal
+# assignments; with every finite cost read as 0 it counts the consistent ones.
+
+@pytest.mark.parametrize("seed", range(40))
+def test_count_against_brute_force(seed):
+    """Optimal and consistent counts equal enumeration (exact integers),
+    with forbidden cells (p2 > 0) and small cost ranges (many ties)."""
+    from oracle.brute import count_solutions
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(5, 9))
+    d = int(rng.integers(2, 4))
+    p2 = [0.0, 0.2, 0.4][seed % 3]
+    cmax = [1, 2, 100][seed % 3 if seed % 5 else 0]
+    inst = gen.random_network(n, d, d, int(rng.integers(n, 2 * n)), 1, 3, cmax, p2, seed)
+    order = oracle.minfill_order(inst) if seed % 2 else oracle.degree_order(inst)
+    opt, n_opt, n_cons = count_solutions(inst)
+    ro = oracle.solve_count(inst, order, "optimal")
+    assert ro.value == opt and ro.count == n_opt, (ro.value, opt, ro.count, n_opt)
+    rc = oracle.solve_count(inst, order, "consistent")
+    assert rc.count == n_cons, (rc.count, n_cons)
+    assert rc.value == (0 if n_cons else INF)
+    # the min-sum tables and argmins are those of plain BE
+    rb = oracle.solve_be(inst, order)
+    assert all(a.digest == b.digest for a, b in zip(ro.tables, rb.tables))
+
+
+def test_count_f64_against_brute_force():
+    """f64 (MPE-style) problems: optimal count (ties at equal doubles) and
+    consistent count (p = 0 cells) by enumeration."""
+    from oracle.brute import count_solutions
+    for seed in range(6):
+        inst = gen.random_network_f64(7, 2, 3, 10, 1, 3, 4.0, 0.3, seed)
+        order = oracle.minfill_order(inst)
+        opt, n_opt, n_cons = count_solutions(inst)
+        assert oracle.solve_count(inst, order, "optimal").count == n_opt
+        assert oracle.solve_count(inst, order, "consistent").count == n_cons
+
+
+def test_count_closed_forms():
+    """All-zero costs: every assignment optimal and consistent, prod d_i.
+    Unary-only: prod_i (#values attaining the unary minimum).  All-INF: 0.
+    Two disjoint copies of an instance: the counts multiply."""
+    dom = [2, 3, 4, 3]
+    z = gen.Instance.from_functions(dom, [((0, 1), [0] * 6), ((1, 2, 3), [0] * 36)])
+    for mode in ("optimal", "consistent"):
+        assert oracle.solve_count(z, oracle.minfill_order(z), mode).count == 2 * 3 * 4 * 3
+    un = [[3, 1, 1], [0, 5], [2, 2, 2, 9]]
+    u = gen.Instance.from_functions([3, 2, 4], [((i,), t) for i, t in enumerate(un)])
+    r = oracle.solve_count(u, [0, 1, 2], "optimal")
+    assert r.value == 1 + 0 + 2 and r.count == 2 * 1 * 3
+    assert oracle.solve_count(u, [0, 1, 2], "consistent").count == 3 * 2 * 4
+    ai = gen.Instance.from_functions([2, 2], [((0, 1), [INF] * 4)])
+    for mode in ("optimal", "consistent"):
+        assert oracle.solve_count(ai, [0, 1], mode).count == 0
+    base = gen.random_network(5, 3, 3, 7, 1, 3, 2, 0.2, 4)
+    funcs = [(list(base.scope(f)), base.table(f)) for f in range(base.nf)]
+    two = gen.Instance.from_functions(list(base.dom) * 2, funcs + [([v + 5 for v in s], t) for s, t in funcs])
+    for mode in ("optimal", "consistent"):
+        c1 = oracle.solve_count(base, oracle.minfill_order(base), mode).count
+        c2 = oracle.solve_count(two, oracle.minfill_order(two), mode).count
+        assert c2 == c1 * c1
+
+
+def test_count_tree_closed_form():
+    """A chain x0 - x1 - ... - x7 with 0/1 costs f(a, b) = [a != b]: optimum
+    0, attained by the d constant assignments; every assignment consistent."""
+    d, n = 3, 8
+    t = [0 if a == b else 1 for a in range(d) for b in range(d)]
+    ch = gen.Instance.from_functions([d] * n, [((i, i + 1), t) for i in range(n - 1)])
+    r = oracle.solve_count(ch, oracle.minfill_order(ch), "optimal")
+    assert r.value == 0 and r.count == d
+    assert oracle.solve_count(ch, oracle.minfill_order(ch), "consistent").count == d ** n
