@@ -230,6 +230,7 @@ def main():
         ms_t, stats, _ = timed(dict(resident_inputs=True, timing=True), args.steps)
     clocks = clk.summary()
 
+    st_last = stats[-1]
     # roofline of the dominant kernel (BK), from the live per-launch events
     bk_ms = sum(t["ms"] for s in stats for t in s["tasks"]) / len(stats)
     bk_bytes = sum(t["bytes"] for t in stats[0]["tasks"])
@@ -276,7 +277,8 @@ def main():
         "e2e": {"value": total_cells / (ms_e2e * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": int(inst.costs.nbytes),
                 "d2h_bytes_per_step": int(4 * inst.n + 8), "ms_per_step": ms_e2e},
-        "gpu_launches": args.steps * (ntasks + 3),  # relayout + buckets + constants + value
+        # relayout + buckets + input merges + constants (run stats) + the value kernel
+        "gpu_launches": args.steps * (int(st_last.get("util_launches", ntasks + 2)) + 1),
         "optimum": root,
         "cpu_baseline": cpu,
     }

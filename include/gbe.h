@@ -145,7 +145,7 @@ gbe_status gbe_pseudotree(const gbe_problem *p, const int32_t *order,
  *   {"device":0, "budget_bytes":N, "world_size":W, "rank":r,
  *    "shard_min_rows":N, "retain":"none"|"args"|"all", "timing":true,
  *    "kernel":-1|0|1, "resident_inputs":false, "graph":true, "concurrent":true,
- *    "semiring":"minsum"|"sumprod"}
+ *    "semiring":"minsum"|"sumprod", "count":"none"|"optimal"|"consistent"}
  * "retain":"all" keeps every table on the device for gbe_run_table().
  * "kernel" forces the generic (0) or tiled (1) bucket kernel (-1 = auto).
  * "resident_inputs" keeps the uploaded tables on the device between solves.
@@ -158,6 +158,13 @@ gbe_status gbe_pseudotree(const gbe_problem *p, const int32_t *order,
  * GBE_E_INVALID): every bucket eliminates by -log sum exp(-.), so
  * gbe_solve_be's opt is -log Z; there is no assignment (assign_out must be
  * NULL, gbe_dpop_value fails) and argmin tables read back as zeros.
+ * "count" (exact BE on one rank only, not with sumprod, else GBE_E_INVALID):
+ * solution counting, the (min, count) semiring:
+ * every table also carries a float64 count table (8 bytes per row), the
+ * number of completions of the eliminated variables attaining its value;
+ * "optimal" counts the optimal assignments, "consistent" the assignments of
+ * finite cost (every finite cost read as 0: opt is then 0 or INF).  Counts
+ * are exact integers below 2^53.  Read with gbe_solve_count / gbe_run_count.
  * Errors: GBE_E_INVALID (bad order, i-bound < member arity - 1),
  * GBE_E_BUDGET (names the bucket and its rows). */
 gbe_status gbe_plan_create(const gbe_problem *p, const int32_t *order, int32_t ibound,
@@ -177,6 +184,14 @@ void gbe_plan_destroy(gbe_plan *plan);
  * (NULL ok) receives per-bucket timings when the plan has "timing":true. */
 gbe_status gbe_solve_be(gbe_plan *plan, void *stream, gbe_value *opt, int32_t *assign_out,
                         char *stats_json, size_t cap);
+
+/* Solution counting ("as a byproduct ... BE can compute the number
+ * of consistent solutions"), plan built with "count": runs the UTIL phase
+ * in the (min, count) semiring and returns opt (optimum; 0 / INF for
+ * "consistent") and *count = number of optimal / consistent solutions (the
+ * product over connected components; 0 if infeasible).  Caller-owned
+ * outputs; GBE_E_INVALID for a plan without "count". */
+gbe_status gbe_solve_count(gbe_plan *plan, void *stream, gbe_value *opt, double *count);
 
 /* MBE(i) (Alg. 2): lower = sum of constants; upper = evaluate(assignment);
  * the value phase minimises the sum of all mini-bucket functions (A7), so the
@@ -202,6 +217,11 @@ gbe_status gbe_run_stats(const gbe_run *run, char *buf, size_t cap);
  * "retain":"all".  host_out: rows * (4 or 8) bytes; host_arg: rows bytes
  * (either may be NULL).  Only rows owned by this rank are written. */
 gbe_status gbe_run_table(const gbe_run *run, int32_t t, void *host_out, uint8_t *host_arg);
+/* counting runs (plan with "count"): number of optimal / consistent
+ * solutions, and the count table of table t (host_out: rows doubles; needs
+ * "retain":"all"; GBE_E_INVALID otherwise) */
+gbe_status gbe_run_count(const gbe_run *run, double *count);
+gbe_status gbe_run_count_table(const gbe_run *run, int32_t t, double *host_out);
 void gbe_run_destroy(gbe_run *run);
 
 /* ---------------------------------------------------------------------

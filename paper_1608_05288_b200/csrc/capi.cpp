@@ -51,6 +51,10 @@ ExecOptions parse_exec(const char *json) {
   std::string sr = j.s("semiring", "minsum");
   if (sr == "sumprod") ex.sumprod = true;
   else if (sr != "minsum") GBE_FAIL(GBE_E_INVALID, "semiring must be minsum|sumprod");
+  std::string c = j.s("count", "none");
+  if (c == "optimal") ex.count = 1;
+  else if (c == "consistent") ex.count = 2;
+  else if (c != "none") GBE_FAIL(GBE_E_INVALID, "count must be none|optimal|consistent");
   return ex;
 }
 
@@ -185,6 +189,36 @@ gbe_status gbe_solve_be(gbe_plan *plan, void *stream, gbe_value *opt, int32_t *a
     if (plan->plan->ex.sumprod && assign_out)
       GBE_FAIL(GBE_E_INVALID, "a sum-product plan has no assignment (pass assign_out = NULL)");
     solve(plan, stream, false, opt, nullptr, assign_out, stats_json, cap);
+  });
+}
+
+gbe_status gbe_solve_count(gbe_plan *plan, void *stream, gbe_value *opt, double *count) {
+  return guard([&] {
+    if (!plan || !count) GBE_FAIL(GBE_E_INVALID, "null argument");
+    if (!plan->plan->ex.count) GBE_FAIL(GBE_E_INVALID, "plan was not built with \"count\"");
+    RunImpl *R = run_create(plan, stream, false);
+    try {
+      if (opt) *opt = run_optimum(R);
+      run_count(R, count, nullptr);
+    } catch (...) {
+      run_destroy(R);
+      throw;
+    }
+    run_destroy(R);
+  });
+}
+
+gbe_status gbe_run_count(const gbe_run *run, double *count) {
+  return guard([&] {
+    if (!run || !count) GBE_FAIL(GBE_E_INVALID, "null argument");
+    run_count(run->impl, count, nullptr);
+  });
+}
+
+gbe_status gbe_run_count_table(const gbe_run *run, int32_t t, double *host_out) {
+  return guard([&] {
+    if (!run || !host_out) GBE_FAIL(GBE_E_INVALID, "null argument");
+    run_count_table(run->impl, t, host_out);
   });
 }
 

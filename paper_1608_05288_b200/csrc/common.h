@@ -115,6 +115,7 @@ struct ExecOptions {
   bool graph = true;            // replay the UTIL phase as a CUDA graph (1 GPU, cached arena)
   bool concurrent = true;       // the graph is the task DAG: sibling subtrees overlap
   bool sumprod = false;         // sum-product semiring (-log Z), f64 exact BE only
+  int count = 0;                // (min, count) semiring: 0 off, 1 optimal, 2 consistent solutions
 };
 
 struct Plan {

@@ -109,7 +109,7 @@ struct DevPlan {
   struct Arena {
     bool planned = false;
     size_t bytes = 0, off_raw = 0, off_sorted = 0;
-    std::vector<size_t> off_out, off_full, off_arg, off_merge;
+    std::vector<size_t> off_out, off_full, off_arg, off_merge, off_cnt;
     // UTIL-phase DAG: deps[t] = tasks that must finish before task t starts
     // (its producers and the last users of arena ranges it overwrites)
     std::vector<std::vector<int32_t>> deps;
@@ -118,7 +118,7 @@ struct DevPlan {
     void *vprog = nullptr;  // cached value-phase program (device)
     cudaGraphExec_t exec = nullptr;  // captured UTIL phase
     int runs = 0;
-    void *d_opt = nullptr, *d_cp = nullptr, *h_opt = nullptr;
+    void *d_opt = nullptr, *d_cp = nullptr, *d_ccp = nullptr, *h_opt = nullptr;
     int32_t *d_assign = nullptr;
     std::vector<cudaEvent_t> ev;
     int vsteps = 0;
@@ -131,6 +131,7 @@ struct DevPlan {
       if (a.exec) cudaGraphExecDestroy(a.exec);
       cudaFree(a.d_opt);
       cudaFree(a.d_cp);
+      cudaFree(a.d_ccp);
       cudaFree(a.d_assign);
       if (a.h_opt) cudaFreeHost(a.h_opt);
       for (auto e : a.ev) cudaEventDestroy(e);
@@ -215,6 +216,8 @@ static void plan_arena(const Plan &P, DevPlan *D, bool mbe_mode) {
     ranges[ti].push_back({o, o + std::max<size_t>((b + 255) & ~size_t(255), 256)});
   };
   A.off_merge.assign(D->merges.size(), SIZE_MAX);
+  A.off_cnt.assign(nt, SIZE_MAX);
+  std::vector<size_t> cnt_b(nt, 0);
   for (size_t ti = 0; ti < nt; ti++) {
     const Task &t = P.tasks[ti];
     const Shard &sh = t.shard;
@@ -227,6 +230,11 @@ static void plan_arena(const Plan &P, DevPlan *D, bool mbe_mode) {
     out_b[ti] = el * (size_t)cap;
     A.off_out[ti] = fl.alloc(out_b[ti]);
     put(ti, A.off_out[ti], out_b[ti]);
+    if (P.ex.count) {  // (min, count) semiring: a float64 count per row
+      cnt_b[ti] = 8 * (size_t)cap;
+      A.off_cnt[ti] = fl.alloc(cnt_b[ti]);
+      put(ti, A.off_cnt[ti], cnt_b[ti]);
+    }
     if (want_arg) {
       A.off_arg[ti] = fl.alloc((size_t)std::max<int64_t>(local, 1));
       put(ti, A.off_arg[ti], (size_t)std::max<int64_t>(local, 1));
@@ -244,7 +252,8 @@ static void plan_arena(const Plan &P, DevPlan *D, bool mbe_mode) {
         if (m.kind == 1) {
           if (out_b[m.index]) fl.release(A.off_out[m.index], out_b[m.index]);
           if (full_b[m.index]) fl.release(A.off_full[m.index], full_b[m.index]);
-          out_b[m.index] = full_b[m.index] = 0;
+          if (cnt_b[m.index]) fl.release(A.off_cnt[m.index], cnt_b[m.index]);
+          out_b[m.index] = full_b[m.index] = cnt_b[m.index] = 0;
         }
   }
   A.bytes = std::max<size_t>(fl.top, 256);
@@ -455,10 +464,15 @@ static DevPlan *dev_plan(gbe_plan *gp) {
         if (src.shard.on && !src.shard.gather) h.shift[j] = src.shard.lo;
       }
     }
-    plan_merges(P, D, ti, h, noinf);
+    if (P.ex.count) {  // counting plans: bk_count (generic tiling), inputs as declared
+      D->in_map[ti].resize(h.ninputs);
+      for (int j = 0; j < h.ninputs; j++) D->in_map[ti][j] = j;
+    } else {
+      plan_merges(P, D, ti, h, noinf);
+    }
     D->h_desc[ti] = h;
     D->launch[ti] = bk_plan_launch(h, t.shard.lo, t.shard.hi, P.ex.kernel, D->num_sms);
-    if (P.ex.kernel != 0 &&
+    if (P.ex.kernel != 0 && !P.ex.count &&
         bkf_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_fast[ti], D->fl[ti], noinf)) {
       D->use_fast[ti] = 1;
       D->launch[ti].variant = 1;
@@ -529,6 +543,7 @@ struct RunImpl {
   void *d_opt = nullptr;
   int32_t *d_assign = nullptr, *d_gbuf = nullptr;
   gbe_value optimum{};
+  double count = 0.0;           // counting plans: number of optimal / consistent solutions
   bool util_done = false;
   bool shared_scalars = false;  // d_opt / d_assign belong to the arena (graph path)
   ~RunImpl() { release(); }
@@ -672,6 +687,16 @@ static void run_util(RunImpl &R) {
   }
   std::vector<const void *> cptrs;
   for (auto &m : P.constants) cptrs.push_back(R.member_ptr(m));
+  // counting plans: count tables of the members / constants (nullptr for an
+  // original function: every entry counts 1)
+  auto cnt_ptr = [&](const Member &m) -> const void * {
+    return (P.ex.count && m.kind == 1) ? (const void *)(R.base + R.A->off_cnt[m.index]) : nullptr;
+  };
+  std::vector<const void *> ccptrs;
+  for (auto &m : P.constants) ccptrs.push_back(cnt_ptr(m));
+  std::vector<InPtrs> cins(P.ex.count ? nt : 0);
+  for (size_t ti = 0; ti < cins.size(); ti++)
+    for (int j = 0; j < P.tasks[ti].desc.ninputs; j++) cins[ti].p[j] = cnt_ptr(P.tasks[ti].members[j]);
 
   DevPlan::Arena &A = *R.A;
   const bool graph = P.ex.graph && W == 1 && !g_alloc && !R.arena_own;
@@ -682,6 +707,9 @@ static void run_util(RunImpl &R) {
       CK(cudaMalloc(&A.d_cp, sizeof(void *) * std::max<size_t>(cptrs.size(), 1)));
       if (!cptrs.empty())
         CK(cudaMemcpy(A.d_cp, cptrs.data(), sizeof(void *) * cptrs.size(), cudaMemcpyHostToDevice));
+      CK(cudaMalloc(&A.d_ccp, sizeof(void *) * std::max<size_t>(ccptrs.size(), 1)));
+      if (!ccptrs.empty())
+        CK(cudaMemcpy(A.d_ccp, ccptrs.data(), sizeof(void *) * ccptrs.size(), cudaMemcpyHostToDevice));
       CK(cudaMallocHost(&A.h_opt, 16));
     }
     if (P.ex.timing && A.ev.empty()) {
@@ -701,6 +729,7 @@ static void run_util(RunImpl &R) {
   }
   std::vector<cudaEvent_t> &ev = graph ? A.ev : R.ev;
   void *d_cp = graph ? A.d_cp : nullptr;
+  void *d_ccp = graph ? A.d_ccp : nullptr;
   alignas(16) unsigned char hopt_local[16] = {0};
   unsigned char *hopt = graph ? (unsigned char *)A.h_opt : hopt_local;
 
@@ -770,7 +799,10 @@ static void run_util(RunImpl &R) {
                      M.h.ninputs, cudaGetErrorString(e));
         }
       }
-      if (D->use_fast[ti])
+      if (P.ex.count)
+        CK(bk_count_launch(D->h_desc[ti], D->d_desc + ti, ins[ti], cins[ti], out,
+                           (double *)(R.base + R.A->off_cnt[ti]), argp, sh.lo, sh.hi, P.ex.count == 2, st));
+      else if (D->use_fast[ti])
         CK(bkf_launch(D->d_fast + ti, D->fl[ti], ins[ti], out, argp, sh.lo, st));
       else
         CK(bk_launch(D->h_desc[ti], D->d_desc + ti, ins[ti], out, argp, sh.lo, sh.hi, D->launch[ti], st));
@@ -806,7 +838,18 @@ static void run_util(RunImpl &R) {
     }
     CK(value_launch(p.is_f64(), nullptr, 0, 0, nullptr, nullptr, R.d_assign, nullptr, -1, W,
                     (const void *const *)cp, (int)cptrs.size(), R.d_opt, st));
-    CK(cudaMemcpyAsync(hopt, R.d_opt, el, cudaMemcpyDeviceToHost, st));
+    if (P.ex.count) {  // number of solutions: product of the constants' counts (d_opt + 8)
+      void *ccp = d_ccp;
+      if (!graph) {
+        ccp = dalloc(sizeof(void *) * std::max<size_t>(ccptrs.size(), 1), st);
+        if (!ccptrs.empty())
+          CK(cudaMemcpyAsync(ccp, ccptrs.data(), sizeof(void *) * ccptrs.size(), cudaMemcpyHostToDevice, st));
+      }
+      CK(count_total_launch(p.is_f64(), (const void *const *)cp, (const double *const *)ccp, (int)cptrs.size(),
+                            P.ex.count == 2, R.d_opt, (double *)((char *)R.d_opt + 8), st));
+      if (!graph) dfree(ccp, st);
+    }
+    CK(cudaMemcpyAsync(hopt, R.d_opt, P.ex.count ? 16 : el, cudaMemcpyDeviceToHost, st));
     if (!graph) dfree(cp, st);
   };
 
@@ -833,6 +876,7 @@ static void run_util(RunImpl &R) {
   if (graph) A.runs++;
   CK(cudaStreamSynchronize(s));
   R.optimum = read_value(p, hopt);
+  if (P.ex.count) std::memcpy(&R.count, hopt + 8, sizeof(double));
   if (P.ex.timing) {
     R.ms.assign(nt, 0.f);
     for (size_t ti = 0; ti < nt; ti++) CK(cudaEventElapsedTime(&R.ms[ti], ev[2 * ti], ev[2 * ti + 1]));
@@ -982,12 +1026,22 @@ static std::string stats_json(const RunImpl &R) {
   const Plan &P = *R.gp->plan;
   const Problem &p = *P.prob;
   std::ostringstream o;
-  o << "{\"total_cells\":" << P.total_cells << ",\"total_bytes\":" << P.total_bytes << ",\"tasks\":[";
+  // kernel launches of one UTIL phase: relayout, one per bucket, one per
+  // input merge, constants (+ the count product of counting plans)
+  const size_t util_launches = 2 + P.tasks.size() + R.D->merges.size() + (P.ex.count ? 1 : 0);
+  o << "{\"total_cells\":" << P.total_cells << ",\"total_bytes\":" << P.total_bytes
+    << ",\"merges\":" << R.D->merges.size() << ",\"util_launches\":" << util_launches << ",\"tasks\":[";
   for (size_t ti = 0; ti < P.tasks.size(); ti++) {
     const Task &t = P.tasks[ti];
     int64_t local = t.shard.hi - t.shard.lo;
     int64_t frac_in = t.rows ? (int64_t)((double)t.in_cells * local / t.rows) : 0;
     int64_t bytes = (int64_t)p.elem() * (frac_in + local) + ((!R.mbe || P.ex.retain >= 2) ? local : 0);
+    if (P.ex.count) {  // + the float64 count tables read (messages) and written
+      int64_t msg = 0;
+      for (auto &m : t.members)
+        if (m.kind == 1) msg += P.tasks[m.index].rows;
+      bytes += 8 * ((t.rows ? (int64_t)((double)msg * local / t.rows) : 0) + local);
+    }
     o << (ti ? "," : "") << "{\"var\":" << t.var << ",\"mb\":" << t.mb << ",\"rows\":" << local
       << ",\"d\":" << t.d << ",\"k\":" << t.desc.ninputs << ",\"cells\":" << local * t.d
       << ",\"bytes\":" << bytes << ",\"variant\":" << R.D->launch[ti].variant
@@ -1054,6 +1108,20 @@ void run_table(const RunImpl *R, int32_t t, void *host_out, uint8_t *host_arg) {
     CK(cudaMemcpyAsync(host_arg, R->arg[t], local, cudaMemcpyDeviceToHost, R->stream));
   }
   CK(cudaStreamSynchronize(R->stream));
+}
+
+void run_count(const RunImpl *R, double *count, void *) {
+  if (!R->gp->plan->ex.count) GBE_FAIL(GBE_E_INVALID, "run of a plan without \"count\"");
+  *count = R->count;
+}
+
+void run_count_table(const RunImpl *R, int32_t t, double *host_out) {
+  const Plan &P = *R->gp->plan;
+  if (!P.ex.count) GBE_FAIL(GBE_E_INVALID, "run of a plan without \"count\"");
+  if (t < 0 || (size_t)t >= P.tasks.size()) GBE_FAIL(GBE_E_INVALID, "table %d out of range", t);
+  if (P.ex.retain < 2) GBE_FAIL(GBE_E_INVALID, "count tables need \"retain\":\"all\"");
+  const Task &T = P.tasks[t];
+  CK(cudaMemcpy(host_out, R->base + R->A->off_cnt[t], 8 * (size_t)T.rows, cudaMemcpyDeviceToHost));
 }
 
 void solve(gbe_plan *gp, void *stream, bool mbe, gbe_value *opt, gbe_value *upper,

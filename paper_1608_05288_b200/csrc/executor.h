@@ -19,6 +19,8 @@ gbe_value run_optimum(const RunImpl *R);
 void run_value_phase(RunImpl *R, int32_t *assign_out);
 void run_stats(const RunImpl *R, char *buf, size_t cap);
 void run_table(const RunImpl *R, int32_t t, void *host_out, uint8_t *host_arg);
+void run_count(const RunImpl *R, double *count, void *unused);
+void run_count_table(const RunImpl *R, int32_t t, double *host_out);
 
 void solve(gbe_plan *gp, void *stream, bool mbe, gbe_value *opt, gbe_value *upper,
            int32_t *assign_out, char *stats, size_t cap);

@@ -124,6 +124,117 @@ __global__ void __launch_bounds__(256) bk_generic(const gbe_bucket_desc *__restr
 }
 
 // ---------------------------------------------------------------------------
+// Counting bucket ("as a byproduct ... BE can
+// compute the number of consistent solutions"): the (min, count) semiring.
+// Same tiling and index maps as bk_generic; every message input j also has a
+// count table cin.p[j] (nullptr for an original function: count 1).  For
+// theta.v: s_v = the saturating / IEEE sum of the inputs (CONS: every finite
+// entry read as 0), c_v = prod_j count_j (input order); the row keeps
+// out = min_v s_v, arg = first minimiser (A8) and cnt = sum of c_v over the v
+// attaining the minimum in ascending v (0 when the minimum is infinite).
+
+template <typename T, bool CONS>
+__global__ void __launch_bounds__(256) bk_count(const gbe_bucket_desc *__restrict__ D, InPtrs in,
+                                                InPtrs cin, T *__restrict__ out,
+                                                double *__restrict__ cnt, uint8_t *__restrict__ arg,
+                                                int64_t row_begin, int64_t row_end, int nlow, int plow) {
+  using S = Sr<T>;
+  using Acc = typename S::Acc;
+  extern __shared__ int32_t loff[];  // [k][plow]
+  __shared__ int64_t base[GBE_MAX_INPUTS];
+  const int m = D->nsep, k = D->ninputs, d = D->d;
+  for (int idx = threadIdx.x; idx < k * plow; idx += blockDim.x) {
+    int j = idx / plow, l = idx - j * plow;
+    int64_t o = 0;
+    for (int q = m - 1; q >= m - nlow; q--) {
+      int r = D->radix[q];
+      o += (int64_t)(l % r) * D->stride[j][q];
+      l /= r;
+    }
+    loff[idx] = (int32_t)o;
+  }
+  const int64_t t0 = row_begin / plow, t1 = (row_end - 1) / plow;
+  for (int64_t t = t0 + blockIdx.x; t <= t1; t += gridDim.x) {
+    __syncthreads();
+    if (threadIdx.x < k) {
+      int j = threadIdx.x;
+      int64_t rem = t, o = 0;
+      for (int q = m - nlow - 1; q >= 0; q--) {
+        int r = D->radix[q];
+        o += (rem % r) * D->stride[j][q];
+        rem /= r;
+      }
+      base[j] = o - D->shift[j];
+    }
+    __syncthreads();
+    for (int l = threadIdx.x; l < plow; l += blockDim.x) {
+      int64_t r = t * plow + l;
+      if (r < row_begin || r >= row_end) continue;
+      Acc best = S::zero();
+      double bc = 0.0;
+      int bv = 0;
+      for (int v = 0; v < d; v++) {
+        Acc s = S::zero();
+        double c = 1.0;
+        for (int j = 0; j < k; j++) {
+          const int64_t i = base[j] + loff[j * plow + l] + v;
+          Acc x = S::load((const T *)in.p[j], i);
+          if constexpr (CONS) {
+            if constexpr (sizeof(T) == 4)
+              x = x < kInf ? 0u : kInf;
+            else
+              x = x < Sr<double>::inf() ? 0.0 : Sr<double>::inf();
+          }
+          s = S::add(s, x);
+          if (cin.p[j]) c = c * __ldg((const double *)cin.p[j] + i);
+        }
+        if (v == 0 || s < best) {
+          best = s;
+          bv = v;
+          bc = c;
+        } else if (s == best) {
+          bc = bc + c;
+        }
+      }
+      bool inf;
+      if constexpr (sizeof(T) == 4)
+        inf = (uint32_t)best >= kInf;
+      else
+        inf = !((double)best < Sr<double>::inf());
+      out[r - row_begin] = S::out(best);
+      cnt[r - row_begin] = inf ? 0.0 : bc;
+      if (arg) arg[r - row_begin] = (uint8_t)bv;
+    }
+  }
+}
+
+// number of solutions = product of the constant messages' counts (the
+// components multiply; an original constant counts 1), 0 if the optimum is
+// infinite.  CONS: the reported value is 0 (or INF) -- every finite cost
+// reads as 0.
+template <typename T>
+__global__ void count_total_kernel(const void *const *cptrs, const double *const *cc, int n, int cons,
+                                   T *optimum, double *count) {
+  double c = 1.0;
+  bool inf = false;
+  for (int k = 0; k < n; k++) {
+    if (cc[k]) c = c * cc[k][0];
+    const T x = ((const T *)cptrs[k])[0];
+    if constexpr (sizeof(T) == 4)
+      inf = inf || (uint32_t)x >= kInf;
+    else
+      inf = inf || !(x < Sr<double>::inf());
+  }
+  if (cons) {
+    if constexpr (sizeof(T) == 4)
+      *optimum = inf ? (T)kInf : (T)0;
+    else
+      *optimum = inf ? Sr<double>::inf() : 0.0;
+  }
+  *count = inf ? 0.0 : c;
+}
+
+// ---------------------------------------------------------------------------
 // relayout of the original tables (declared -> ascending position order)
 
 template <typename T>
@@ -276,6 +387,35 @@ cudaError_t value_launch(bool f64, const VStep *steps, int s0, int s1, const VMe
   else
     value_kernel<int32_t><<<1, 32, 0, stream>>>(steps, s0, s1, mems, terms, assign, gathered,
                                                  gvar, W, cptrs, nconst, (int32_t *)optimum);
+  return cudaGetLastError();
+}
+
+cudaError_t bk_count_launch(const gbe_bucket_desc &h, const gbe_bucket_desc *dev_desc, const InPtrs &in,
+                            const InPtrs &cin, void *out, double *cnt, uint8_t *arg, int64_t row_begin,
+                            int64_t row_end, bool consistent, cudaStream_t stream) {
+  if (row_end <= row_begin) return cudaSuccess;
+  const BkLaunchInfo li = bk_plan_launch(h, row_begin, row_end, BK_GENERIC, 148);
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<int64_t>((int64_t)li.grid, (int64_t)nsm * 8);
+#define GBE_CNT(T, C) \
+  bk_count<T, C><<<grid, li.block, li.smem, stream>>>(dev_desc, in, cin, (T *)out, cnt, arg, row_begin, row_end, li.nlow, li.plow)
+  if (h.semiring == GBE_MINSUM_I32) {
+    if (consistent) GBE_CNT(int32_t, true); else GBE_CNT(int32_t, false);
+  } else {
+    if (consistent) GBE_CNT(double, true); else GBE_CNT(double, false);
+  }
+#undef GBE_CNT
+  return cudaGetLastError();
+}
+
+cudaError_t count_total_launch(bool f64, const void *const *cptrs, const double *const *cc, int n,
+                               bool consistent, void *optimum, double *count, cudaStream_t stream) {
+  if (f64)
+    count_total_kernel<double><<<1, 1, 0, stream>>>(cptrs, cc, n, consistent, (double *)optimum, count);
+  else
+    count_total_kernel<int32_t><<<1, 1, 0, stream>>>(cptrs, cc, n, consistent, (int32_t *)optimum, count);
   return cudaGetLastError();
 }
 

@@ -57,6 +57,18 @@ cudaError_t bk_launch(const gbe_bucket_desc &h, const gbe_bucket_desc *dev_desc,
                       const InPtrs &in, void *out, uint8_t *arg, int64_t row_begin,
                       int64_t row_end, const BkLaunchInfo &li, cudaStream_t stream);
 
+// Counting bucket, (min, count) semiring:
+// bk_generic's tiling; cin.p[j] = count table of input j (nullptr: every
+// entry 1).  cnt[r] = number of completions attaining out[r] (0 if infinite);
+// consistent: every finite entry reads as cost 0.
+cudaError_t bk_count_launch(const gbe_bucket_desc &h, const gbe_bucket_desc *dev_desc, const InPtrs &in,
+                            const InPtrs &cin, void *out, double *cnt, uint8_t *arg, int64_t row_begin,
+                            int64_t row_end, bool consistent, cudaStream_t stream);
+// count = prod of the n constant counts cc[k][0] (nullptr: 1), 0 if some
+// constant cptrs[k][0] is infinite; consistent: *optimum = 0 or INF.
+cudaError_t count_total_launch(bool f64, const void *const *cptrs, const double *const *cc, int n,
+                               bool consistent, void *optimum, double *count, cudaStream_t stream);
+
 // Relayout of the original tables from declared to sorted scope order
 // (P:624): for each function f, out[off[f] + i] = in[off[f] + sum_q
 // digit_q(i) * pstride[poff[f] + q]] with digits over radices prad.

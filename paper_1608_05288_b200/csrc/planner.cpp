@@ -143,6 +143,11 @@ std::unique_ptr<Plan> make_plan(std::shared_ptr<const Problem> pp, const int32_t
     if (ibound >= 0) GBE_FAIL(GBE_E_INVALID, "semiring sumprod: exact BE only (ibound < 0)");
     if (plan->ex.retain == 1) plan->ex.retain = 0;  // no value phase: argmins are never read
   }
+  if (ex.count) {
+    if (ex.sumprod) GBE_FAIL(GBE_E_INVALID, "count and semiring sumprod are exclusive");
+    if (ibound >= 0) GBE_FAIL(GBE_E_INVALID, "count: exact BE only (ibound < 0)");
+    if (ex.world_size != 1) GBE_FAIL(GBE_E_INVALID, "count: single-rank plans only");
+  }
   int n = p.n;
   if (ex.world_size < 1 || ex.rank < 0 || ex.rank >= ex.world_size)
     GBE_FAIL(GBE_E_INVALID, "bad world_size/rank (%d/%d)", ex.world_size, ex.rank);

@@ -31,7 +31,7 @@ EXPORTED = [
     "gbe_dpop_util", "gbe_dpop_value", "gbe_run_stats", "gbe_run_table", "gbe_run_destroy",
     "gbe_bucket_kernel", "gbe_set_allocator", "gbe_set_allgather", "gbe_last_error",
     "gbe_version", "gbe_bucket_kernel_variant", "gbe_comm_nccl_id", "gbe_comm_nccl_init",
-    "gbe_comm_finalize",
+    "gbe_comm_finalize", "gbe_solve_count", "gbe_run_count", "gbe_run_count_table",
 ]
 
 
@@ -94,6 +94,9 @@ def lib():
         L.gbe_dpop_value.argtypes = [vp, vp]
         L.gbe_run_stats.argtypes = [vp, ctypes.c_char_p, sz]
         L.gbe_run_table.argtypes = [vp, i32, vp, vp]
+        L.gbe_solve_count.argtypes = [vp, vp, P(Value), P(ctypes.c_double)]
+        L.gbe_run_count.argtypes = [vp, P(ctypes.c_double)]
+        L.gbe_run_count_table.argtypes = [vp, i32, vp]
         L.gbe_run_destroy.argtypes = [vp]
         L.gbe_run_destroy.restype = None
         L.gbe_bucket_kernel.argtypes = [vp, vp, vp, vp, i64, i64, vp]
@@ -254,6 +257,14 @@ class Plan:
         -log_z()).  One value-only solve: -(gbe_solve_be's optimum)."""
         return -self.solve_be(stream, assignment=False)[0]
 
+    def solve_count(self, stream=None):
+        """(optimum, count) of a plan made with count="optimal" (number of
+        optimal assignments) or count="consistent" (number of assignments of
+        finite cost; optimum 0 or INF): solution counting."""
+        v, c = Value(), ctypes.c_double()
+        _check(lib().gbe_solve_count(self._h, _stream_ptr(stream), ctypes.byref(v), ctypes.byref(c)))
+        return _val(v, self.problem.is_f64), c.value
+
     def solve_mbe(self, stream=None, stats=False, assignment=True):
         """(lower, upper, assignment[, stats]); assignment=False: lower bound
         only (no value phase; messages freed once consumed with retain="none")."""
@@ -307,6 +318,19 @@ class Run:
         arg = np.zeros(max(rows, 1), dtype=np.uint8) if want_arg else None
         _check(lib().gbe_run_table(self._h, int(t), _ptr(out), _ptr(arg)))
         return (out[:rows] if out is not None else None), (arg[:rows] if arg is not None else None)
+
+
+    def count(self):
+        """number of optimal / consistent solutions (counting plans)"""
+        c = ctypes.c_double()
+        _check(lib().gbe_run_count(self._h, ctypes.byref(c)))
+        return c.value
+
+    def count_table(self, t, rows):
+        """count table of table t (counting plans with retain="all")"""
+        out = np.zeros(max(rows, 1), dtype=np.float64)
+        _check(lib().gbe_run_count_table(self._h, int(t), _ptr(out)))
+        return out[:rows]
 
 
 def bucket_kernel(desc: BucketDesc, inputs, out, arg, row_begin, row_end, stream=None):

@@ -72,6 +72,39 @@ def measure(name, inst, order, ib, exact_value_only=False, oracle_threads=(), **
     return rec
 
 
+def measure_count(name, inst, order, mode):
+    """Solution counting: kernel cells/s and HBM fraction
+    of the counting bucket kernel (algorithmic bytes include the float64
+    count tables), one-shot solve time, oracle time at all cores."""
+    P = G.Problem.from_instance(inst)
+    plan_t = G.Plan(P, order, count=mode, timing=True)
+    for _ in range(2):
+        run, root = plan_t.dpop_util()
+        st = run.stats()
+        cnt = run.count()
+        run.close()
+    tasks = st["tasks"]
+    ms = sum(t["ms"] for t in tasks)
+    by = sum(t["bytes"] for t in tasks)
+    del plan_t
+    plan = G.Plan(P, order, count=mode)
+    plan.solve_count()
+    walls = []
+    for _ in range(5):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        v, c = plan.solve_count()
+        walls.append((time.perf_counter() - t0) * 1e3)
+    t0 = time.perf_counter()
+    orun = oracle.solve_count(inst, order, mode, keep_tables=False)
+    rec = {"config": name, "count": mode, "cells": st["total_cells"], "kernel_ms": ms,
+           "kernel_cells_per_s": st["total_cells"] / (ms * 1e-3), "hbm_frac": by / (ms * 1e-3) / 1e9 / PEAK,
+           "e2e_solve_ms_median": statistics.median(walls), "value": v, "n_solutions": c,
+           "oracle_n_solutions": orun.count, "oracle_s_all_cores": time.perf_counter() - t0}
+    print(json.dumps(rec), flush=True)
+    return rec
+
+
 def main(which):
     cores = os.cpu_count()
     if "c1" in which:
@@ -80,6 +113,13 @@ def main(which):
     if "c2" in which:
         inst = configs.c2()
         measure("C2", inst, oracle.minfill_order(inst), -1, oracle_threads=(1, cores))
+    if "count" in which:  # solution counting on C2 and C4
+        inst = configs.c2()
+        for mode in ("optimal", "consistent"):
+            measure_count("C2", inst, oracle.minfill_order(inst), mode)
+    if "c4count" in which:
+        inst = configs.c4()
+        measure_count("C4", inst, oracle.minfill_order(inst), "optimal")
     if "c3" in which:
         inst = configs.c3()
         order = configs.c3_order()

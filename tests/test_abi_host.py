@@ -201,3 +201,22 @@ def test_sumprod_plan_validation_host():
     oi, _ = Pi.order()
     with pytest.raises(G.GbeError):
         G.Plan(Pi, oi, semiring="sumprod")
+
+
+def test_count_plan_errors():
+    """Counting plans are exact BE, one rank, min-sum:
+    the planner rejects the rest on the host (GBE_E_INVALID), and a plan
+    without "count" cannot be counted."""
+    inst = gen.random_network(6, 2, 2, 6, 1, 2, 5, 0.0, 1)
+    P = G.Problem.from_instance(inst)
+    order, _ = P.order()
+    for kw in (dict(count="sometimes"), dict(count="optimal", world_size=2, rank=0)):
+        with pytest.raises(G.GbeError):
+            G.Plan(P, order, **kw)
+    with pytest.raises(G.GbeError):
+        G.Plan(P, order, 2, count="optimal")  # MBE: exact BE only
+    with pytest.raises(G.GbeError):
+        G.Plan(P, order).solve_count()        # plan without "count"
+    fp = G.Problem.from_instance(gen.random_network_f64(6, 2, 2, 6, 1, 2, 3.0, 0.0, 1))
+    with pytest.raises(G.GbeError):
+        G.Plan(fp, order, count="optimal", semiring="sumprod")
