@@ -236,6 +236,13 @@ __device__ __forceinline__ void issue_tile(const ProdSmem &ps, const FastHot &f,
   if (bytes) tma_load_1d(sm + s * f.stage_bytes + f.soff[lane], (const void *)a16, bytes, &full[s]);
 }
 
+// in-tile row offset a * rs1 + b * rs2 of register-block row (a, b), formed
+// where it is used (two live registers instead of R * R2)
+struct RowOff {
+  int rs1, rs2;
+  __device__ __forceinline__ int operator()(int a, int b) const { return a * rs1 + b * rs2; }
+};
+
 // cell (a, b, v) = P0[v] (+ P1[a][v]) (+ P2[b][v]) (+ P3[a][b][v]) with the
 // saturating adds of A9; min over v, first minimiser (A8); staged in smem.
 template <typename T, int R, int R2, int DV, bool H1, bool H2, bool H3, bool SP>
@@ -243,7 +250,7 @@ __device__ __forceinline__ void combine(const typename SrF<T>::Acc (&P0)[DV],
                                         const typename SrF<T>::Acc (&P1)[R][DV],
                                         const typename SrF<T>::Acc (&P2)[R2][DV],
                                         const typename SrF<T>::Acc (&P3)[R][R2][DV], T *outs,
-                                        uint8_t *args, const int (&loff)[R][R2],
+                                        uint8_t *args, const RowOff &loff,
                                         typename SrF<T>::Acc &gmax) {
   using S = SrF<T>;
   using Acc = typename S::Acc;
@@ -269,7 +276,7 @@ __device__ __forceinline__ void combine(const typename SrF<T>::Acc (&P0)[DV],
         else
           c[v] = Q[v];
       }
-      const int l = loff[a][b];
+      const int l = loff(a, b);
       if constexpr (SP) {  // -log sum_v exp(-c_v) = m - log sum_v exp(m - c_v)
         Acc m = c[0];
 #pragma unroll
@@ -308,7 +315,7 @@ __device__ __forceinline__ void combine(const typename SrF<T>::Acc (&P0)[DV],
 template <int R, int R2, int DV, bool H1, bool H2, bool H3>
 __device__ __forceinline__ void combine_nf(const uint32_t (&P0)[DV], const uint32_t (&P1)[R][DV],
                                            const uint32_t (&P2)[R2][DV], const uint32_t (&P3)[R][R2][DV],
-                                           int32_t *outs, uint8_t *args, const int (&loff)[R][R2]) {
+                                           int32_t *outs, uint8_t *args, const RowOff &loff) {
   constexpr int SH = DV <= 4 ? 2 : 3;
   constexpr uint32_t MASK = (1u << SH) - 1u;
   auto emit = [&](const uint32_t (&key)[DV], int l) {
@@ -331,7 +338,7 @@ __device__ __forceinline__ void combine_nf(const uint32_t (&P0)[DV], const uint3
         uint32_t key[DV];
 #pragma unroll
         for (int v = 0; v < DV; v++) key[v] = H3 ? B[b][v] + (P3[a][b][v] << SH) : B[b][v];
-        emit(key, loff[a][b]);
+        emit(key, loff(a, b));
       }
   } else {
     uint32_t P2s[R2][DV];
@@ -354,7 +361,7 @@ __device__ __forceinline__ void combine_nf(const uint32_t (&P0)[DV], const uint3
           uint32_t x = H2 ? A[v] + P2s[b][v] : A[v];
           key[v] = H3 ? x + (P3[a][b][v] << SH) : x;
         }
-        emit(key, loff[a][b]);
+        emit(key, loff(a, b));
       }
     }
   }
@@ -499,11 +506,7 @@ __global__ void __launch_bounds__((NG * kGroupWarps + 2) * 32, 1)
   const int ctid = threadIdx.x - g * kGT;  // 0 .. kGT-1 inside the group
   const int c0 = f.cls_off[0], c1 = f.cls_off[1], c2 = f.cls_off[2], c3 = f.cls_off[3], c4 = f.cls_off[4];
   const int sel = (c2 > c1 ? 1 : 0) | (c3 > c2 ? 2 : 0) | (c4 > c3 ? 4 : 0);
-  int loff[R][R2];  // in-tile row offsets of the group digits (tile-invariant)
-#pragma unroll
-  for (int a = 0; a < R; a++)
-#pragma unroll
-    for (int bb = 0; bb < R2; bb++) loff[a][bb] = a * f.rs1 + bb * f.rs2;
+  const RowOff loff{f.rs1, f.rs2};  // in-tile row offsets of the group digits
   unsigned char *const obase = sm + f.off_out + g * nob * f.out_bytes;
   unsigned char *const abase = sm + f.off_arg + g * nob * f.arg_bytes;
   uint32_t oph = 0;  // use round of the group's staging buffers (parity)
@@ -641,7 +644,7 @@ __global__ void __launch_bounds__((NG * kGroupWarps + 2) * 32, 1)
           for (int a = 0; a < R; a++)
 #pragma unroll
             for (int bb = 0; bb < R2; bb++) {
-              const int l = loff[a][bb];
+              const int l = loff(a, bb);
               if ((uint32_t)outq[l] >= kInf) {
                 outq[l] = (T)kInf;
                 argq[l] = 0;

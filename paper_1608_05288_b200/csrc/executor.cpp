@@ -1045,6 +1045,15 @@ static std::string stats_json(const RunImpl &R) {
     o << (ti ? "," : "") << "{\"var\":" << t.var << ",\"mb\":" << t.mb << ",\"rows\":" << local
       << ",\"d\":" << t.d << ",\"k\":" << t.desc.ninputs << ",\"cells\":" << local * t.d
       << ",\"bytes\":" << bytes << ",\"variant\":" << R.D->launch[ti].variant
+      << ",\"k_eff\":" << R.D->h_desc[ti].ninputs << ",\"merges\":" << R.D->task_merges[ti].size();
+    if (R.D->use_fast[ti]) {
+      const FastHot &fh = R.D->h_fast[ti].hot;
+      o << ",\"tile_rows\":" << fh.PL << ",\"stages\":" << fh.nstages << ",\"staging_bufs\":" << fh.nout
+        << ",\"groups\":" << R.D->fl[ti].NG << ",\"classes\":[" << fh.cls_off[1] - fh.cls_off[0] << ","
+        << fh.cls_off[2] - fh.cls_off[1] << "," << fh.cls_off[3] - fh.cls_off[2] << "," << fh.cls_off[4] - fh.cls_off[3]
+        << "]";
+    }
+    o
       << ",\"ms\":" << (ti < R.ms.size() ? R.ms[ti] : -1.0f) << "}";
   }
   o << "]}";
