@@ -41,7 +41,7 @@ constexpr uint32_t kInf = GBE_INF_I32;
 constexpr int kMaxStages = 8;
 constexpr int kOutBufsMax = 3;  // output staging buffers per consumer group (2 or 3)
 constexpr int64_t kMinCells = 1 << 10;  // measured: the tiled kernel beats bk_generic from ~1e3 cells
-constexpr int kGroupWarps = 8;  // warps per consumer group
+constexpr int kGroupWarpsMax = 8;  // warps per consumer group (int32 shapes; f64 and large shapes: 4)
 constexpr int kSmemCap = 200 * 1024;  // dynamic shared memory cap per CTA
 
 template <typename T>
@@ -367,21 +367,21 @@ __device__ __forceinline__ void combine_nf(const uint32_t (&P0)[DV], const uint3
   }
 }
 
-// One CTA = NG consumer groups of kGroupWarps warps + one producer warp.  The
+// One CTA = NG consumer groups of GW warps + one producer warp.  The
 // producer fills ONE ring of f.nstages input stages; tile i of this CTA goes
 // to stage i mod nstages and to consumer group i mod NG, so a group computing
 // one tile never holds back the loads of the next ones (NG = 2: up to
 // nstages - 2 tiles in flight per SM).  Each group stages its rows in its own
 // output buffers and stores them with TMA bulk copies.
-template <typename T, int R, int R2, int DV, bool SP, bool NF, int NG>
-// (registers: 18 warps put 5 on one SM sub-partition, so NG = 2 gets 96 per
-// thread; NG = 1 gets 168)
-__global__ void __launch_bounds__((NG * kGroupWarps + 2) * 32, 1)
+template <typename T, int R, int R2, int DV, bool SP, bool NF, int NG, int GW>
+// (registers: 2 groups of 8 warps + 2 put 5 warps on one SM sub-partition: 96
+// per thread; 2 groups of 4 warps + 2: 3 warps, 168 per thread)
+__global__ void __launch_bounds__((NG * GW + 2) * 32, 1)
     bk_fast_kernel(const FastDesc *__restrict__ Fg, InPtrs in, T *__restrict__ out,
                    uint8_t *__restrict__ arg, int64_t row_begin, int64_t t_begin, int64_t t_end) {
   using S = SrF<T>;
   using Acc = typename S::Acc;
-  constexpr int kGT = kGroupWarps * 32;  // threads per consumer group
+  constexpr int kGT = GW * 32;  // threads per consumer group
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ FastHot f;
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
@@ -407,11 +407,11 @@ __global__ void __launch_bounds__((NG * kGroupWarps + 2) * 32, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kMaxStages; s++) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kGroupWarps);
+      mbar_init(&empty[s], GW);
     }
     for (int g = 0; g < NG; g++)
       for (int b = 0; b < kOutBufsMax; b++) {
-        mbar_init(&ofull[g][b], kGroupWarps);
+        mbar_init(&ofull[g][b], GW);
         mbar_init(&oempty[g][b], 1);
       }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__((NG * kGroupWarps + 2) * 32, 1)
   __syncthreads();
   const int warp = threadIdx.x >> 5;
 
-  if (warp == NG * kGroupWarps) {  // ---- producer warp: TMA ring ----
+  if (warp == NG * GW) {  // ---- producer warp: TMA ring ----
     const int lane = threadIdx.x & 31;
     const char *my_in = lane < k ? (const char *)in.p[f.in_idx[lane]] : nullptr;
     int s = 0, L = 0;
@@ -457,7 +457,7 @@ __global__ void __launch_bounds__((NG * kGroupWarps + 2) * 32, 1)
   const int PL = f.PL, es = (int)sizeof(T);
   const int nob = f.nout;
 
-  if (warp == NG * kGroupWarps + 1) {  // ---- storer warp: TMA bulk stores of staged tiles ----
+  if (warp == NG * GW + 1) {  // ---- storer warp: TMA bulk stores of staged tiles ----
     // tiles in CTA order (tile i: group i mod NG, its buffer (i / NG) mod nob);
     // the buffer of tile i - 1 is released once tile i is committed and at
     // most one store group is still reading shared memory
@@ -502,7 +502,7 @@ __global__ void __launch_bounds__((NG * kGroupWarps + 2) * 32, 1)
   }
 
   // ---- consumer groups ----
-  const int g = warp / kGroupWarps;
+  const int g = warp / GW;
   const int ctid = threadIdx.x - g * kGT;  // 0 .. kGT-1 inside the group
   const int c0 = f.cls_off[0], c1 = f.cls_off[1], c2 = f.cls_off[2], c3 = f.cls_off[3], c4 = f.cls_off[4];
   const int sel = (c2 > c1 ? 1 : 0) | (c3 > c2 ? 2 : 0) | (c4 > c3 ? 4 : 0);
@@ -676,10 +676,10 @@ __global__ void __launch_bounds__((NG * kGroupWarps + 2) * 32, 1)
 // ---------------------------------------------------------------------------
 // dispatch table over (semiring, R, DV)
 
-template <typename T, int R, int R2, int DV, bool SP, bool NF, int NG>
+template <typename T, int R, int R2, int DV, bool SP, bool NF, int NG, int GW>
 cudaError_t launch_one(const FastDesc *d, const InPtrs &in, void *out, uint8_t *arg, int64_t rb,
                        int64_t t0, int64_t t1, int grid, int block, int smem, cudaStream_t s) {
-  auto kern = bk_fast_kernel<T, R, R2, DV, SP, NF, NG>;
+  auto kern = bk_fast_kernel<T, R, R2, DV, SP, NF, NG, GW>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemCap);
@@ -689,10 +689,12 @@ cudaError_t launch_one(const FastDesc *d, const InPtrs &in, void *out, uint8_t *
   return cudaGetLastError();
 }
 
-// consumer groups per CTA: two (one CTA per SM, shared ring) for int32 shapes
-// whose register blocks fit 120 registers per thread; f64 and the large
-// int32 shapes run one group (their register blocks need up to 168).
-constexpr int ng_of(int es, int R, int R2, int DV) { return (es == 4 && R * R2 * DV <= 27) ? 2 : 1; }
+// two consumer groups per CTA (one CTA per SM, shared ring); 8 warps each for
+// int32 shapes whose register blocks fit 96 registers per thread, 4 warps
+// each for f64 and the large int32 shapes (their blocks need up to 168; the
+// smaller groups also keep small f64 tiles' threads busy).
+constexpr int ng_of(int, int, int, int) { return 2; }
+constexpr int gw_of(int es, int R, int R2, int DV) { return (es == 4 && R * R2 * DV <= 27) ? 8 : 4; }
 
 template <typename T, bool SP, bool NF>
 cudaError_t dispatch(int R, int R2, int DV, int NGr, const FastDesc *d, const InPtrs &in, void *out,
@@ -700,9 +702,9 @@ cudaError_t dispatch(int R, int R2, int DV, int NGr, const FastDesc *d, const In
                      int smem, cudaStream_t s) {
 #define GBE_CASE(r, r2, dv)                                                                                  \
   if (R == r && R2 == r2 && DV == dv) {                                                                      \
-    constexpr int ng = ng_of((int)sizeof(T), r, r2, dv);                                                     \
+    constexpr int ng = ng_of((int)sizeof(T), r, r2, dv), gw = gw_of((int)sizeof(T), r, r2, dv);             \
     if (NGr != ng) return cudaErrorInvalidValue;                                                             \
-    return launch_one<T, r, r2, dv, SP, NF, ng>(d, in, out, arg, rb, t0, t1, grid, block, smem, s);          \
+    return launch_one<T, r, r2, dv, SP, NF, ng, gw>(d, in, out, arg, rb, t0, t1, grid, block, smem, s);      \
   }
   GBE_CASE(2, 2, 2) GBE_CASE(2, 2, 3) GBE_CASE(2, 2, 4) GBE_CASE(2, 2, 5) GBE_CASE(3, 3, 2) GBE_CASE(3, 3, 3)
   GBE_CASE(3, 1, 2) GBE_CASE(3, 1, 3) GBE_CASE(3, 1, 4) GBE_CASE(3, 1, 5)
@@ -812,8 +814,8 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     const int R2 = g2 >= 0 ? R : 1;
     const int64_t Pmid = PL / (R * R2);
     if (row_begin % PL || row_end % PL) continue;
-    const int NG = ng_of(es, R, R2, DV);
-    const size_t kSmemMax = (size_t)(smem_env ? std::atoi(smem_env) : (NG == 2 ? 200 : 196)) * 1024;
+    const int NG = ng_of(es, R, R2, DV), GW = gw_of(es, R, R2, DV);
+    const size_t kSmemMax = (size_t)(smem_env ? std::atoi(smem_env) : 200) * 1024;
     const int min_st = pass == 0 ? std::max(kStagesWant, 2 * NG) : NG;
     // classes
     std::memset(&F, 0, sizeof(F));
@@ -926,7 +928,7 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     L.g1 = g1;
     L.g2 = g2;
     L.nf = noinf && es == 4 && h.semiring == GBE_MINSUM_I32;
-    L.block = (NG * kGroupWarps + 2) * 32;
+    L.block = (NG * GW + 2) * 32;
     L.t_begin = row_begin / PL;
     L.t_end = row_end / PL;
     int per_sm = (int)std::min<size_t>(std::max<size_t>(1, (220 * 1024) / (off + 4096)), 2048 / L.block);
