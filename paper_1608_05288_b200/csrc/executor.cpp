@@ -337,7 +337,11 @@ static void plan_merges(const Plan &P, DevPlan *D, size_t ti, gbe_bucket_desc &h
         }
     return c;
   };
-  const int64_t small = C / 64, cap = std::min<int64_t>(C / 32, int64_t(1) << 26);
+  static const int cap_log2 = [] {  // GBE_MERGE_CAP_LOG2: tuning knob
+    const char *e = std::getenv("GBE_MERGE_CAP_LOG2");
+    return e ? std::atoi(e) : 26;
+  }();
+  const int64_t small = C / 64, cap = std::min<int64_t>(C / 32, int64_t(1) << cap_log2);
   std::vector<int> cand[4];
   for (int j = 0; j < k; j++) {
     if (h.shift[j] != 0) continue;
@@ -539,7 +543,7 @@ struct RunImpl {
   std::vector<void *> out, full;
   std::vector<uint8_t *> arg;
   std::vector<cudaEvent_t> ev;
-  std::vector<float> ms;
+  std::vector<float> ms, merge_ms;  // per task: total (merges + bucket) and merges only
   void *d_opt = nullptr;
   int32_t *d_assign = nullptr, *d_gbuf = nullptr;
   gbe_value optimum{};
@@ -713,7 +717,7 @@ static void run_util(RunImpl &R) {
       CK(cudaMallocHost(&A.h_opt, 16));
     }
     if (P.ex.timing && A.ev.empty()) {
-      A.ev.resize(2 * nt);
+      A.ev.resize(3 * nt);
       for (auto &e : A.ev) CK(cudaEventCreate(&e));
     }
     R.d_opt = A.d_opt;
@@ -723,7 +727,7 @@ static void run_util(RunImpl &R) {
     R.d_opt = dalloc(16, s);
     R.d_assign = (int32_t *)dalloc(sizeof(int32_t) * std::max(p.n, 1), s);
     if (P.ex.timing) {
-      R.ev.resize(2 * nt);
+      R.ev.resize(3 * nt);
       for (auto &e : R.ev) CK(cudaEventCreate(&e));
     }
   }
@@ -787,7 +791,7 @@ static void run_util(RunImpl &R) {
       }
       void *out = gathered_src[ti] ? gathered_src[ti] : R.base + R.A->off_out[ti];
       uint8_t *argp = want_arg ? (uint8_t *)(R.base + R.A->off_arg[ti]) : nullptr;
-      if (P.ex.timing) rec(ev[2 * ti]);
+      if (P.ex.timing) rec(ev[3 * ti]);
       for (int32_t mi : D->task_merges[ti]) {
         const DevPlan::Merge &M = D->merges[mi];
         CK(bk_launch(M.h, D->d_mdesc + mi, mins[mi], R.base + R.A->off_merge[mi], nullptr, 0, M.h.rows, M.li, st));
@@ -799,6 +803,7 @@ static void run_util(RunImpl &R) {
                      M.h.ninputs, cudaGetErrorString(e));
         }
       }
+      if (P.ex.timing) rec(ev[3 * ti + 1]);  // merges done
       if (P.ex.count)
         CK(bk_count_launch(D->h_desc[ti], D->d_desc + ti, ins[ti], cins[ti], out,
                            (double *)(R.base + R.A->off_cnt[ti]), argp, sh.lo, sh.hi, P.ex.count == 2, st));
@@ -806,7 +811,7 @@ static void run_util(RunImpl &R) {
         CK(bkf_launch(D->d_fast + ti, D->fl[ti], ins[ti], out, argp, sh.lo, st));
       else
         CK(bk_launch(D->h_desc[ti], D->d_desc + ti, ins[ti], out, argp, sh.lo, sh.hi, D->launch[ti], st));
-      if (P.ex.timing) rec(ev[2 * ti + 1]);
+      if (P.ex.timing) rec(ev[3 * ti + 2]);
       static const bool sync_each = std::getenv("GBE_SYNC_EACH") != nullptr;  // debugging knob
       if (sync_each && !capturing) {
         cudaError_t e = cudaStreamSynchronize(st);
@@ -879,7 +884,11 @@ static void run_util(RunImpl &R) {
   if (P.ex.count) std::memcpy(&R.count, hopt + 8, sizeof(double));
   if (P.ex.timing) {
     R.ms.assign(nt, 0.f);
-    for (size_t ti = 0; ti < nt; ti++) CK(cudaEventElapsedTime(&R.ms[ti], ev[2 * ti], ev[2 * ti + 1]));
+    R.merge_ms.assign(nt, 0.f);
+    for (size_t ti = 0; ti < nt; ti++) {
+      CK(cudaEventElapsedTime(&R.ms[ti], ev[3 * ti], ev[3 * ti + 2]));
+      CK(cudaEventElapsedTime(&R.merge_ms[ti], ev[3 * ti], ev[3 * ti + 1]));
+    }
   }
   R.util_done = true;
 }
@@ -1054,7 +1063,8 @@ static std::string stats_json(const RunImpl &R) {
         << "]";
     }
     o
-      << ",\"ms\":" << (ti < R.ms.size() ? R.ms[ti] : -1.0f) << "}";
+      << ",\"ms\":" << (ti < R.ms.size() ? R.ms[ti] : -1.0f)
+      << ",\"merge_ms\":" << (ti < R.merge_ms.size() ? R.merge_ms[ti] : -1.0f) << "}";
   }
   o << "]}";
   return o.str();

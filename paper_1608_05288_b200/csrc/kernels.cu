@@ -52,6 +52,30 @@ struct Sr<double> {
   __device__ __forceinline__ static double inf() { return __longlong_as_double(0x7ff0000000000000LL); }
 };
 
+// Element offset in input j of the first row of tile t: the mixed-radix
+// digits of t over the high output digits [0, nhigh) times the input's
+// strides.  32-bit division when the tile index fits (every practical
+// launch: the serial 64-bit div/mod chain dominated large d = 1 merges).
+__device__ __forceinline__ int64_t tile_base(const gbe_bucket_desc *__restrict__ D, int j, int64_t t, int nhigh) {
+  int64_t o = 0;
+  if (t < ((int64_t)1 << 32)) {
+    uint32_t rem = (uint32_t)t;
+    for (int q = nhigh - 1; q >= 0 && rem; q--) {
+      const uint32_t r = (uint32_t)D->radix[q], qt = rem / r;
+      o += (int64_t)(rem - qt * r) * D->stride[j][q];
+      rem = qt;
+    }
+  } else {
+    int64_t rem = t;
+    for (int q = nhigh - 1; q >= 0; q--) {
+      const int r = D->radix[q];
+      o += (rem % r) * D->stride[j][q];
+      rem /= r;
+    }
+  }
+  return o - D->shift[j];
+}
+
 // ---------------------------------------------------------------------------
 // BK generic: tiles of `plow` consecutive rows (= all values of the `nlow`
 // least-significant output digits).  Per CTA: the low-digit offsets of every
@@ -81,16 +105,7 @@ __global__ void __launch_bounds__(256) bk_generic(const gbe_bucket_desc *__restr
   const int64_t t0 = row_begin / plow, t1 = (row_end - 1) / plow;
   for (int64_t t = t0 + blockIdx.x; t <= t1; t += gridDim.x) {
     __syncthreads();
-    if (threadIdx.x < k) {
-      int j = threadIdx.x;
-      int64_t rem = t, o = 0;
-      for (int q = m - nlow - 1; q >= 0; q--) {
-        int r = D->radix[q];
-        o += (rem % r) * D->stride[j][q];
-        rem /= r;
-      }
-      base[j] = o - D->shift[j];
-    }
+    if (threadIdx.x < k) base[threadIdx.x] = tile_base(D, threadIdx.x, t, m - nlow);
     __syncthreads();
     for (int l = threadIdx.x; l < plow; l += blockDim.x) {
       int64_t r = t * plow + l;
@@ -156,16 +171,7 @@ __global__ void __launch_bounds__(256) bk_count(const gbe_bucket_desc *__restric
   const int64_t t0 = row_begin / plow, t1 = (row_end - 1) / plow;
   for (int64_t t = t0 + blockIdx.x; t <= t1; t += gridDim.x) {
     __syncthreads();
-    if (threadIdx.x < k) {
-      int j = threadIdx.x;
-      int64_t rem = t, o = 0;
-      for (int q = m - nlow - 1; q >= 0; q--) {
-        int r = D->radix[q];
-        o += (rem % r) * D->stride[j][q];
-        rem /= r;
-      }
-      base[j] = o - D->shift[j];
-    }
+    if (threadIdx.x < k) base[threadIdx.x] = tile_base(D, threadIdx.x, t, m - nlow);
     __syncthreads();
     for (int l = threadIdx.x; l < plow; l += blockDim.x) {
       int64_t r = t * plow + l;

@@ -40,4 +40,4 @@ for label, opts in [("resident", dict(resident_inputs=True, timing=True)), ("e2e
             ti = info["tables"][[i for i, x in enumerate(info["tables"]) if x["var"] == t["var"] and x["mb"] == t["mb"]][0]]
             print(f"   x{t['var']:<4d} k={t['k']:<3d} rows={t['rows']:.3e} ms={t['ms']:.3f} "
                   f"cells/s={t['cells']/t['ms']*1e3:.3e} GB/s={t['bytes']/t['ms']/1e6:.0f} var={t['variant']} in/C={ti['in_cells']/(t['cells']):.3f}"
-                  f" k_eff={t.get('k_eff')} PL={t.get('tile_rows')} st={t.get('stages')} nob={t.get('staging_bufs')} cls={t.get('classes')}")
+                  f" merge_ms={t.get('merge_ms', 0):.3f} k_eff={t.get('k_eff')} PL={t.get('tile_rows')} st={t.get('stages')} nob={t.get('staging_bufs')} cls={t.get('classes')}")
