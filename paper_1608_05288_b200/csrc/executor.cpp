@@ -320,7 +320,11 @@ static void plan_merges(const Plan &P, DevPlan *D, size_t ti, gbe_bucket_desc &h
   for (int j = 0; j < k; j++) map[j] = j;
   if (off || P.ex.kernel == 0 || k < 2) return;
   const int64_t C = (t.shard.hi - t.shard.lo) * d;
-  if (C < (int64_t(1) << 22)) return;  // small buckets: the extra launches cost more than they save
+  static const int min_log2 = [] {  // GBE_MERGE_MIN_LOG2: tuning knob
+    const char *e = std::getenv("GBE_MERGE_MIN_LOG2");
+    return e ? std::atoi(e) : 27;
+  }();
+  if (C < (int64_t(1) << min_log2)) return;  // small buckets: the extra launches cost more than they save
   FastDesc *F = new FastDesc();
   BkfLaunch L;
   const bool ok = bkf_build(h, t.shard.lo, t.shard.hi, D->num_sms, *F, L, noinf);
