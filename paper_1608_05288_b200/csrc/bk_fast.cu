@@ -373,7 +373,10 @@ __device__ __forceinline__ void combine_nf(const uint32_t (&P0)[DV], const uint3
 // one tile never holds back the loads of the next ones (NG = 2: up to
 // nstages - 2 tiles in flight per SM).  Each group stages its rows in its own
 // output buffers and stores them with TMA bulk copies.
-template <typename T, int R, int R2, int DV, bool SP, bool NF, int NG, int GW>
+// CS >= 0 fixes the class structure at compile time (bit 3: class 0 present,
+// bits 0-2: classes 1-3 present), so only that combine and those loads are
+// emitted; CS = -1 reads it from the descriptor.
+template <typename T, int R, int R2, int DV, bool SP, bool NF, int NG, int GW, int CS = -1>
 // (registers: 2 groups of 8 warps + 2 put 5 warps on one SM sub-partition: 96
 // per thread; 2 groups of 4 warps + 2: 3 warps, 168 per thread)
 __global__ void __launch_bounds__((NG * GW + 2) * 32, 1)
@@ -505,7 +508,8 @@ __global__ void __launch_bounds__((NG * GW + 2) * 32, 1)
   const int g = warp / GW;
   const int ctid = threadIdx.x - g * kGT;  // 0 .. kGT-1 inside the group
   const int c0 = f.cls_off[0], c1 = f.cls_off[1], c2 = f.cls_off[2], c3 = f.cls_off[3], c4 = f.cls_off[4];
-  const int sel = (c2 > c1 ? 1 : 0) | (c3 > c2 ? 2 : 0) | (c4 > c3 ? 4 : 0);
+  const int sel = CS >= 0 ? (CS & 7) : ((c2 > c1 ? 1 : 0) | (c3 > c2 ? 2 : 0) | (c4 > c3 ? 4 : 0));
+  const bool has0 = CS >= 0 ? (CS & 8) != 0 : c1 > c0;
   const RowOff loff{f.rs1, f.rs2};  // in-tile row offsets of the group digits
   unsigned char *const obase = sm + f.off_out + g * nob * f.out_bytes;
   unsigned char *const abase = sm + f.off_arg + g * nob * f.arg_bytes;
@@ -526,7 +530,7 @@ __global__ void __launch_bounds__((NG * GW + 2) * 32, 1)
     for (int q = ctid; q < Pmid; q += kGT) {
       Acc P0[DV], P1[R][DV], P2[R2][DV], P3[R][R2][DV];
       // class 0 (no group digit): P0[v]
-      if (c1 > c0) {
+      if (has0) {
         const unsigned char *p = sm + sb[c0] + offtab[c0 * Pmid + q];
 #pragma unroll
         for (int v = 0; v < DV; v++) P0[v] = (Acc)((const T *)p)[v];
@@ -676,10 +680,10 @@ __global__ void __launch_bounds__((NG * GW + 2) * 32, 1)
 // ---------------------------------------------------------------------------
 // dispatch table over (semiring, R, DV)
 
-template <typename T, int R, int R2, int DV, bool SP, bool NF, int NG, int GW>
+template <typename T, int R, int R2, int DV, bool SP, bool NF, int NG, int GW, int CS = -1>
 cudaError_t launch_one(const FastDesc *d, const InPtrs &in, void *out, uint8_t *arg, int64_t rb,
                        int64_t t0, int64_t t1, int grid, int block, int smem, cudaStream_t s) {
-  auto kern = bk_fast_kernel<T, R, R2, DV, SP, NF, NG, GW>;
+  auto kern = bk_fast_kernel<T, R, R2, DV, SP, NF, NG, GW, CS>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemCap);
@@ -696,10 +700,30 @@ cudaError_t launch_one(const FastDesc *d, const InPtrs &in, void *out, uint8_t *
 constexpr int ng_of(int, int, int, int) { return 2; }
 constexpr int gw_of(int es, int R, int R2, int DV) { return (es == 4 && R * R2 * DV <= 27) ? 8 : 4; }
 
+// the hottest shape (C4, C3: d = 3, two radix-3 group digits, infinity-free)
+// with its class structure as a template parameter
+template <int CS>
+cudaError_t launch_333_cs(const FastDesc *d, const InPtrs &in, void *out, uint8_t *arg, int64_t rb, int64_t t0,
+                          int64_t t1, int grid, int block, int smem, cudaStream_t s) {
+  return launch_one<int32_t, 3, 3, 3, false, true, 2, 8, CS>(d, in, out, arg, rb, t0, t1, grid, block, smem, s);
+}
+using Launch333 = cudaError_t (*)(const FastDesc *, const InPtrs &, void *, uint8_t *, int64_t, int64_t, int64_t,
+                                  int, int, int, cudaStream_t);
+constexpr Launch333 kLaunch333[16] = {
+    launch_333_cs<0>, launch_333_cs<1>, launch_333_cs<2>,  launch_333_cs<3>,  launch_333_cs<4>,  launch_333_cs<5>,
+    launch_333_cs<6>, launch_333_cs<-1>, launch_333_cs<8>, launch_333_cs<9>,  launch_333_cs<10>, launch_333_cs<11>,
+    launch_333_cs<12>, launch_333_cs<13>, launch_333_cs<14>, launch_333_cs<-1>};  // 7, 15: all classes
+    // present -- the specialised kernels spill at 96 registers, the generic one does not
+
 template <typename T, bool SP, bool NF>
 cudaError_t dispatch(int R, int R2, int DV, int NGr, const FastDesc *d, const InPtrs &in, void *out,
                      uint8_t *arg, int64_t rb, int64_t t0, int64_t t1, int grid, int block,
-                     int smem, cudaStream_t s) {
+                     int smem, cudaStream_t s, int cs = -1) {
+  if constexpr (sizeof(T) == 4 && NF && !SP) {
+    static const bool cs_off = std::getenv("GBE_FAST_NO_CS") != nullptr;  // A/B knob
+    if (R == 3 && R2 == 3 && DV == 3 && cs >= 0 && !cs_off)
+      return kLaunch333[cs](d, in, out, arg, rb, t0, t1, grid, block, smem, s);
+  }
 #define GBE_CASE(r, r2, dv)                                                                                  \
   if (R == r && R2 == r2 && DV == dv) {                                                                      \
     constexpr int ng = ng_of((int)sizeof(T), r, r2, dv), gw = gw_of((int)sizeof(T), r, r2, dv);             \
@@ -924,6 +948,8 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     off = (off + 127) & ~size_t(127);
     if (off > kSmemMax) continue;
     L.smem = (int)off;
+    L.cs = (f.cls_off[1] > f.cls_off[0] ? 8 : 0) | (f.cls_off[2] > f.cls_off[1] ? 1 : 0) |
+           (f.cls_off[3] > f.cls_off[2] ? 2 : 0) | (f.cls_off[4] > f.cls_off[3] ? 4 : 0);
     L.NG = NG;
     L.g1 = g1;
     L.g2 = g2;
@@ -956,7 +982,7 @@ cudaError_t bkf_launch(const FastDesc *dev_f, const BkfLaunch &L, const InPtrs &
                                           L.t_end, L.grid, L.block, L.smem, s);
   if (L.nf)
     return dispatch<int32_t, false, true>(L.R, L.R2, L.DV, L.NG, dev_f, in, out, arg, row_begin, L.t_begin,
-                                          L.t_end, L.grid, L.block, L.smem, s);
+                                          L.t_end, L.grid, L.block, L.smem, s, L.cs);
   return dispatch<int32_t, false, false>(L.R, L.R2, L.DV, L.NG, dev_f, in, out, arg, row_begin, L.t_begin,
                                          L.t_end, L.grid, L.block, L.smem, s);
 }

@@ -40,6 +40,7 @@ struct BkfLaunch {
   bool nf = false;  // infinity-free int32 tables: packed-key argmin (no clamps)
   int NG = 1;       // consumer groups per CTA
   int g1 = -1, g2 = -1;  // group (register-blocking) digits
+  int cs = -1;           // class structure (bit 3: class 0 present, bits 0-2: classes 1-3)
   int grid = 1, block = 256, smem = 0;
   int64_t t_begin = 0, t_end = 0;
 };
