@@ -143,10 +143,16 @@ gbe_status gbe_pseudotree(const gbe_problem *p, const int32_t *order,
  * generated function, |mini-bucket scope union| <= ibound + 1, reading A5;
  * greedy first-fit partition, reading A6).  json_exec (NULL ok):
  *   {"device":0, "budget_bytes":N, "world_size":W, "rank":r,
- *    "shard_min_rows":N, "retain":"none"|"args"|"all", "timing":true,
+ *    "shard_min_rows":N, "retain":"none"|"args"|"all"|"host", "timing":true,
  *    "kernel":-1|0|1, "resident_inputs":false, "graph":true, "concurrent":true,
- *    "semiring":"minsum"|"sumprod", "count":"none"|"optimal"|"consistent"}
+ *    "semiring":"minsum"|"sumprod", "count":"none"|"optimal"|"consistent",
+ *    "host_arg_chunk":N}
  * "retain":"all" keeps every table on the device for gbe_run_table().
+ * "retain":"host" (exact BE / DPOP, one rank, min-sum; else GBE_E_INVALID)
+ * puts the argmin tables in pinned host memory: buckets run in row chunks of
+ * "host_arg_chunk" rows (default 2^28) whose argmins stream out through a
+ * 2-slot device ring while the next chunk computes (Fig. 8); the
+ * value phase reads them in place.  No CUDA-graph replay for such plans.
  * "kernel" forces the generic (0) or tiled (1) bucket kernel (-1 = auto).
  * "resident_inputs" keeps the uploaded tables on the device between solves.
  * "graph" replays the UTIL phase as a CUDA graph from the second solve on

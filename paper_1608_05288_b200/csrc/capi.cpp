@@ -42,7 +42,10 @@ ExecOptions parse_exec(const char *json) {
   if (r == "none") ex.retain = 0;
   else if (r == "args") ex.retain = 1;
   else if (r == "all") ex.retain = 2;
-  else GBE_FAIL(GBE_E_INVALID, "retain must be none|args|all");
+  else if (r == "host") ex.retain = 1, ex.host_args = true;
+  else GBE_FAIL(GBE_E_INVALID, "retain must be none|args|all|host");
+  ex.host_arg_chunk = j.i("host_arg_chunk", ex.host_arg_chunk);
+  if (ex.host_arg_chunk < 1) GBE_FAIL(GBE_E_INVALID, "host_arg_chunk must be >= 1");
   ex.timing = j.b("timing", false);
   ex.kernel = (int)j.i("kernel", -1);
   ex.resident_inputs = j.b("resident_inputs", false);

@@ -116,6 +116,8 @@ struct ExecOptions {
   bool concurrent = true;       // the graph is the task DAG: sibling subtrees overlap
   bool sumprod = false;         // sum-product semiring (-log Z), f64 exact BE only
   int count = 0;                // (min, count) semiring: 0 off, 1 optimal, 2 consistent solutions
+  bool host_args = false;       // argmin tables in pinned host memory, streamed out chunk by chunk
+  int64_t host_arg_chunk = int64_t(1) << 28;  // rows per streamed chunk (device ring buffer bytes)
 };
 
 struct Plan {

@@ -93,6 +93,26 @@ struct DevPlan {
   std::vector<std::vector<int32_t>> task_merges;  // per task: its merges
   std::vector<std::vector<int32_t>> in_map;       // per task input: member index, or -(1 + merge)
   gbe_bucket_desc *d_mdesc = nullptr;
+  // "retain":"host" (§8(f) row 2, argmin spill): each bucket runs in row
+  // chunks whose argmins land in a 2-slot device ring and stream to mapped
+  // pinned host memory on a copy stream while the next chunk computes (the
+  // host/device concurrency of Fig. 8); the value phase reads them
+  // in place (zero-copy)
+  struct Chunk {
+    int64_t lo = 0, hi = 0;
+    int fidx = -1;        // index into h_cfast / cfl (tiled kernel), -1: generic
+    BkLaunchInfo li{};
+  };
+  std::vector<std::vector<Chunk>> chunks;
+  std::vector<FastDesc> h_cfast;
+  std::vector<BkfLaunch> cfl;
+  FastDesc *d_cfast = nullptr;
+  uint8_t *h_harg = nullptr, *d_harg = nullptr;  // pinned mapped host argmins and their device alias
+  std::vector<size_t> harg_off;
+  uint8_t *d_ring = nullptr;
+  int64_t ring = 0;                               // bytes per ring slot
+  cudaStream_t cp_stream = nullptr;
+  cudaEvent_t k_ev[2] = {nullptr, nullptr}, c_ev[2] = {nullptr, nullptr};
   FastDesc *d_fast = nullptr;
   gbe_bucket_desc *d_desc = nullptr;
   int64_t *d_off = nullptr;
@@ -146,6 +166,12 @@ struct DevPlan {
       }
     cudaFree(d_desc);
     cudaFree(d_mdesc);
+    cudaFree(d_cfast);
+    cudaFree(d_ring);
+    if (h_harg) cudaFreeHost(h_harg);
+    if (cp_stream) cudaStreamDestroy(cp_stream);
+    for (auto e : k_ev) if (e) cudaEventDestroy(e);
+    for (auto e : c_ev) if (e) cudaEventDestroy(e);
     cudaFree(d_fast);
     cudaFree(d_off);
     cudaFree(d_poff);
@@ -207,7 +233,7 @@ static void plan_arena(const Plan &P, DevPlan *D, bool mbe_mode) {
   A.off_raw = fl.alloc(raw);
   A.off_sorted = fl.alloc(raw);
   fl.release(A.off_raw, raw);  // raw tables are dead after the relayout
-  const bool want_arg = (!mbe_mode && P.ex.retain >= 1) || P.ex.retain >= 2;
+  const bool want_arg = ((!mbe_mode && P.ex.retain >= 1) || P.ex.retain >= 2) && !P.ex.host_args;
   std::vector<size_t> out_b(nt, 0), full_b(nt, 0);
   // ranges[t]: the arena ranges task t writes; a later task overwriting any of
   // them must wait for t and for t's consumer (the only reader of t's output)
@@ -486,6 +512,48 @@ static DevPlan *dev_plan(gbe_plan *gp) {
       D->launch[ti].variant = 1;
     }
   }
+  if (P.ex.host_args) {  // row chunks per task, host argmin layout, ring, copy stream
+    D->chunks.assign(P.tasks.size(), {});
+    D->harg_off.assign(P.tasks.size(), 0);
+    size_t off = 0;
+    for (size_t ti = 0; ti < P.tasks.size(); ti++) {
+      const Task &t = P.tasks[ti];
+      D->harg_off[ti] = off;
+      off += (size_t)std::max<int64_t>(t.rows, 1);
+      int64_t step = std::max<int64_t>(1, std::min<int64_t>(t.rows, P.ex.host_arg_chunk));
+      if (D->use_fast[ti]) {
+        const int64_t PL = D->h_fast[ti].hot.PL;
+        step = std::max<int64_t>(PL, step / PL * PL);
+      }
+      for (int64_t lo = 0; lo < t.rows; lo += step) {
+        DevPlan::Chunk c;
+        c.lo = lo;
+        c.hi = std::min<int64_t>(t.rows, lo + step);
+        FastDesc F;
+        BkfLaunch L;
+        if (D->use_fast[ti] && bkf_build(D->h_desc[ti], c.lo, c.hi, D->num_sms, F, L, noinf)) {
+          c.fidx = (int)D->h_cfast.size();
+          D->h_cfast.push_back(F);
+          D->cfl.push_back(L);
+        } else {
+          c.li = bk_plan_launch(D->h_desc[ti], c.lo, c.hi, BK_GENERIC, D->num_sms);
+        }
+        D->ring = std::max<int64_t>(D->ring, c.hi - c.lo);
+        D->chunks[ti].push_back(c);
+      }
+    }
+    CK(cudaHostAlloc((void **)&D->h_harg, std::max<size_t>(off, 1), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer((void **)&D->d_harg, D->h_harg, 0));
+    CK(cudaMalloc(&D->d_ring, 2 * (size_t)std::max<int64_t>(D->ring, 1)));
+    CK(cudaMalloc(&D->d_cfast, sizeof(FastDesc) * std::max<size_t>(D->h_cfast.size(), 1)));
+    if (!D->h_cfast.empty())
+      CK(cudaMemcpy(D->d_cfast, D->h_cfast.data(), sizeof(FastDesc) * D->h_cfast.size(), cudaMemcpyHostToDevice));
+    CK(cudaStreamCreateWithFlags(&D->cp_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; i++) {
+      CK(cudaEventCreateWithFlags(&D->k_ev[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&D->c_ev[i], cudaEventDisableTiming));
+    }
+  }
   CK(cudaMalloc(&D->d_fast, sizeof(FastDesc) * std::max<size_t>(P.tasks.size(), 1)));
   if (!P.tasks.empty())
     CK(cudaMemcpy(D->d_fast, D->h_fast.data(), sizeof(FastDesc) * P.tasks.size(), cudaMemcpyHostToDevice));
@@ -671,12 +739,14 @@ static void run_util(RunImpl &R) {
   }
   R.d_sorted = R.base + R.A->off_sorted;
   const bool want_arg = (!R.mbe && P.ex.retain >= 1) || P.ex.retain >= 2;
+  const bool host_args = P.ex.host_args;
   std::vector<InPtrs> ins(nt), mins(D->merges.size());
   std::vector<void *> gathered_src(nt, nullptr);
   for (size_t ti = 0; ti < nt; ti++) {
     const Task &t = P.tasks[ti];
     R.out[ti] = R.base + R.A->off_out[ti];
-    if (want_arg) R.arg[ti] = (uint8_t *)(R.base + R.A->off_arg[ti]);
+    if (host_args) R.arg[ti] = D->d_harg + D->harg_off[ti];
+    else if (want_arg) R.arg[ti] = (uint8_t *)(R.base + R.A->off_arg[ti]);
     const std::vector<int32_t> &map = D->in_map[ti];
     for (size_t j = 0; j < map.size(); j++)
       ins[ti].p[j] = map[j] >= 0 ? R.member_ptr(t.members[map[j]]) : R.base + R.A->off_merge[-(map[j] + 1)];
@@ -707,7 +777,7 @@ static void run_util(RunImpl &R) {
     for (int j = 0; j < P.tasks[ti].desc.ninputs; j++) cins[ti].p[j] = cnt_ptr(P.tasks[ti].members[j]);
 
   DevPlan::Arena &A = *R.A;
-  const bool graph = P.ex.graph && W == 1 && !g_alloc && !R.arena_own;
+  const bool graph = P.ex.graph && W == 1 && !g_alloc && !R.arena_own && !P.ex.host_args;
   if (graph) {  // persistent per-arena scalars, pinned result slot, events
     if (!A.d_opt) {
       CK(cudaMalloc(&A.d_opt, 16));
@@ -776,6 +846,7 @@ static void run_util(RunImpl &R) {
       last_on.assign(D->side.size(), -2);   // -2: branch not forked yet
     }
     size_t rr = 0;
+    int64_t ring_n = 0;  // argmin chunks streamed so far (host_args)
     for (size_t ti = 0; ti < nt; ti++) {
       const Task &t = P.tasks[ti];
       const Shard &sh = t.shard;
@@ -794,7 +865,7 @@ static void run_util(RunImpl &R) {
         branch_of[ti] = b;
       }
       void *out = gathered_src[ti] ? gathered_src[ti] : R.base + R.A->off_out[ti];
-      uint8_t *argp = want_arg ? (uint8_t *)(R.base + R.A->off_arg[ti]) : nullptr;
+      uint8_t *argp = want_arg && !host_args ? (uint8_t *)(R.base + R.A->off_arg[ti]) : nullptr;
       if (P.ex.timing) rec(ev[3 * ti]);
       for (int32_t mi : D->task_merges[ti]) {
         const DevPlan::Merge &M = D->merges[mi];
@@ -808,7 +879,24 @@ static void run_util(RunImpl &R) {
         }
       }
       if (P.ex.timing) rec(ev[3 * ti + 1]);  // merges done
-      if (P.ex.count)
+      if (host_args) {  // row chunks; argmins through the device ring to host memory
+        for (const DevPlan::Chunk &c : D->chunks[ti]) {
+          const int slot = ring_n & 1;
+          if (ring_n >= 2) CK(cudaStreamWaitEvent(st, D->c_ev[slot], 0));  // slot copied out
+          uint8_t *ra = D->d_ring + (size_t)slot * D->ring;
+          void *oc = (char *)out + (size_t)(c.lo - sh.lo) * el;
+          if (c.fidx >= 0)
+            CK(bkf_launch(D->d_cfast + c.fidx, D->cfl[c.fidx], ins[ti], oc, ra, c.lo, st));
+          else
+            CK(bk_launch(D->h_desc[ti], D->d_desc + ti, ins[ti], oc, ra, c.lo, c.hi, c.li, st));
+          CK(cudaEventRecord(D->k_ev[slot], st));
+          CK(cudaStreamWaitEvent(D->cp_stream, D->k_ev[slot], 0));
+          CK(cudaMemcpyAsync(D->h_harg + D->harg_off[ti] + (c.lo - sh.lo), ra, (size_t)(c.hi - c.lo),
+                             cudaMemcpyDeviceToHost, D->cp_stream));
+          CK(cudaEventRecord(D->c_ev[slot], D->cp_stream));
+          ring_n++;
+        }
+      } else if (P.ex.count)
         CK(bk_count_launch(D->h_desc[ti], D->d_desc + ti, ins[ti], cins[ti], out,
                            (double *)(R.base + R.A->off_cnt[ti]), argp, sh.lo, sh.hi, P.ex.count == 2, st));
       else if (D->use_fast[ti])
@@ -835,6 +923,8 @@ static void run_util(RunImpl &R) {
         st = st0;
       }
     }
+    if (host_args)  // every argmin chunk is in host memory before the value phase
+      for (int i = 0; i < 2 && i < ring_n; i++) CK(cudaStreamWaitEvent(st, D->c_ev[i], 0));
     if (dag)  // join every branch before the constants
       for (size_t q = 0; q < last_on.size(); q++)
         if (last_on[q] >= 0) CK(cudaStreamWaitEvent(st, D->tev[last_on[q]], 0));
@@ -1126,7 +1216,10 @@ void run_table(const RunImpl *R, int32_t t, void *host_out, uint8_t *host_arg) {
       src = (const char *)src + P.prob->elem() * T.shard.lo;
     CK(cudaMemcpyAsync(host_out, src, P.prob->elem() * local, cudaMemcpyDeviceToHost, R->stream));
   }
-  if (host_arg) {
+  if (host_arg && P.ex.host_args) {  // argmins already in (pinned) host memory
+    CK(cudaStreamSynchronize(R->stream));
+    std::memcpy(host_arg, R->D->h_harg + R->D->harg_off[t], (size_t)local);
+  } else if (host_arg) {
     if (!R->arg[t]) GBE_FAIL(GBE_E_INVALID, "argmin table %d not retained", t);
     CK(cudaMemcpyAsync(host_arg, R->arg[t], local, cudaMemcpyDeviceToHost, R->stream));
   }

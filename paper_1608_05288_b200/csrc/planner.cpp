@@ -143,6 +143,11 @@ std::unique_ptr<Plan> make_plan(std::shared_ptr<const Problem> pp, const int32_t
     if (ibound >= 0) GBE_FAIL(GBE_E_INVALID, "semiring sumprod: exact BE only (ibound < 0)");
     if (plan->ex.retain == 1) plan->ex.retain = 0;  // no value phase: argmins are never read
   }
+  if (ex.host_args) {
+    if (ibound >= 0) GBE_FAIL(GBE_E_INVALID, "retain host: exact BE / DPOP only (ibound < 0)");
+    if (ex.world_size != 1) GBE_FAIL(GBE_E_INVALID, "retain host: single-rank plans only");
+    if (ex.sumprod || ex.count) GBE_FAIL(GBE_E_INVALID, "retain host: min-sum plans only");
+  }
   if (ex.count) {
     if (ex.sumprod) GBE_FAIL(GBE_E_INVALID, "count and semiring sumprod are exclusive");
     if (ibound >= 0) GBE_FAIL(GBE_E_INVALID, "count: exact BE only (ibound < 0)");
@@ -396,12 +401,17 @@ std::unique_ptr<Plan> make_plan(std::shared_ptr<const Problem> pp, const int32_t
     int64_t local = t.shard.on ? (t.shard.hi - t.shard.lo) : t.rows;
     int64_t full = t.shard.on && t.shard.gather ? t.shard.per * t.shard.block_rows * W : 0;
     msg_bytes[ti] = el * (local + full);
-    const bool want_arg = (ibound < 0 && plan->ex.retain >= 1) || plan->ex.retain >= 2;
+    const bool want_arg = ((ibound < 0 && plan->ex.retain >= 1) || plan->ex.retain >= 2) && !plan->ex.host_args;
     live += msg_bytes[ti] + (want_arg ? local : 0);  // message + argmin
     peak = std::max(peak, live);
     if (plan->ex.retain < 2 && (ibound < 0 || plan->ex.retain == 0))
       for (auto &m : t.members)
         if (m.kind == 1) live -= msg_bytes[m.index];
+  }
+  if (plan->ex.host_args) {  // + the two device chunk buffers the argmins stream through
+    int64_t big = 0;
+    for (auto &t : plan->tasks) big = std::max(big, t.rows);
+    peak += 2 * std::min(big, plan->ex.host_arg_chunk);
   }
   plan->peak_bytes = peak;
   if (ex.budget_bytes > 0 && peak > ex.budget_bytes) {

@@ -120,6 +120,9 @@ def main(which):
     if "c4count" in which:
         inst = configs.c4()
         measure_count("C4", inst, oracle.minfill_order(inst), "optimal")
+    if "c4host" in which:  # argmin spill: argmins streamed to pinned host memory
+        inst = configs.c4()
+        measure("C4-hostargs", inst, oracle.minfill_order(inst), -1, retain="host")
     if "c3" in which:
         inst = configs.c3()
         order = configs.c3_order()

@@ -220,3 +220,18 @@ def test_count_plan_errors():
     fp = G.Problem.from_instance(gen.random_network_f64(6, 2, 2, 6, 1, 2, 3.0, 0.0, 1))
     with pytest.raises(G.GbeError):
         G.Plan(fp, order, count="optimal", semiring="sumprod")
+
+
+def test_host_args_plan_errors():
+    """"retain":"host" (argmin spill) is exact BE/DPOP on
+    one rank in the min-sum semiring; the planner rejects the rest."""
+    inst = gen.random_network(6, 2, 2, 6, 1, 2, 5, 0.0, 1)
+    P = G.Problem.from_instance(inst)
+    order, _ = P.order()
+    G.Plan(P, order, retain="host", host_arg_chunk=64)  # valid
+    for args, kw in (((2,), dict(retain="host")),
+                     ((), dict(retain="host", world_size=2, rank=0)),
+                     ((), dict(retain="host", count="optimal")),
+                     ((), dict(retain="host", host_arg_chunk=0))):
+        with pytest.raises(G.GbeError):
+            G.Plan(P, order, *args, **kw)
