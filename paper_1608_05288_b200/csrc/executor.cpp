@@ -350,7 +350,10 @@ static void plan_merges(const Plan &P, DevPlan *D, size_t ti, gbe_bucket_desc &h
     const char *e = std::getenv("GBE_MERGE_MIN_LOG2");
     return e ? std::atoi(e) : 27;
   }();
-  if (C < (int64_t(1) << min_log2)) return;  // small buckets: the extra launches cost more than they save
+  // small buckets: the extra launches cost more than they save, unless the
+  // merge removes many inputs (checked once the sets are known, below)
+  if (C < (int64_t(1) << std::min(22, min_log2))) return;
+  const bool big_enough = C >= (int64_t(1) << min_log2);
   FastDesc *F = new FastDesc();
   BkfLaunch L;
   const bool ok = bkf_build(h, t.shard.lo, t.shard.hi, D->num_sms, *F, L, noinf);
@@ -371,7 +374,11 @@ static void plan_merges(const Plan &P, DevPlan *D, size_t ti, gbe_bucket_desc &h
     const char *e = std::getenv("GBE_MERGE_CAP_LOG2");
     return e ? std::atoi(e) : 26;
   }();
-  const int64_t small = C / 64, cap = std::min<int64_t>(C / 32, int64_t(1) << cap_log2);
+  static const int cap_div = [] {  // GBE_MERGE_CAP_DIV: tuning knob (merged table <= C / div)
+    const char *e = std::getenv("GBE_MERGE_CAP_DIV");
+    return e ? std::max(1, std::atoi(e)) : 128;
+  }();
+  const int64_t small = C / 64, cap = std::min<int64_t>(C / cap_div, int64_t(1) << cap_log2);
   std::vector<int> cand[4];
   for (int j = 0; j < k; j++) {
     if (h.shift[j] != 0) continue;
@@ -402,6 +409,9 @@ static void plan_merges(const Plan &P, DevPlan *D, size_t ti, gbe_bucket_desc &h
   for (int c = 0; c < 4; c++)
     if (cand[c].size() >= 2 && union_cells(cand[c]) <= cap) sets.push_back(cand[c]);
   if (sets.empty()) return;
+  size_t removed = 0;
+  for (auto &st : sets) removed += st.size() - 1;
+  if (!big_enough && removed < 4) return;
   std::vector<char> merged(k, 0);
   for (auto &st : sets)
     for (int j : st) merged[j] = 1;

@@ -1,2 +1,2 @@
-# merge-threshold A/B on C3 MBE(16) and C4 (kernel sums, timing mode)
-for m in 22 27 30; do echo "== merge min 2^$m"; GBE_MERGE_MIN_LOG2=$m python scripts/bench_detail.py c3 16 2>&1 | sed -n 1,2p; GBE_MERGE_MIN_LOG2=$m python scripts/bench_detail.py c4 2>&1 | sed -n 1,2p; done
+# merge-policy A/B (kernel sums, timing mode): C4-alt, C3 MBE(16), C4
+for v in 32 128 512; do echo "== cap C/$v"; for w in c4alt "c3 16" c4; do GBE_MERGE_CAP_DIV=$v python scripts/bench_detail.py $w 2>&1 | grep "kernel sum" | head -1; done; done
