@@ -41,7 +41,6 @@ constexpr uint32_t kInf = GBE_INF_I32;
 constexpr int kMaxStages = 8;
 constexpr int kOutBufsMax = 3;  // output staging buffers per consumer group (2 or 3)
 constexpr int64_t kMinCells = 1 << 10;  // measured: the tiled kernel beats bk_generic from ~1e3 cells
-constexpr int kGroupWarpsMax = 8;  // warps per consumer group (int32 shapes; f64 and large shapes: 4)
 constexpr int kSmemCap = 200 * 1024;  // dynamic shared memory cap per CTA
 
 template <typename T>
@@ -377,8 +376,8 @@ __device__ __forceinline__ void combine_nf(const uint32_t (&P0)[DV], const uint3
 // bits 0-2: classes 1-3 present), so only that combine and those loads are
 // emitted; CS = -1 reads it from the descriptor.
 template <typename T, int R, int R2, int DV, bool SP, bool NF, int NG, int GW, int CS = -1>
-// (registers: 2 groups of 8 warps + 2 put 5 warps on one SM sub-partition: 96
-// per thread; 2 groups of 4 warps + 2: 3 warps, 168 per thread)
+// (registers: 2 groups of GW = 4 warps + producer + storer put 3 warps on one
+// SM sub-partition: 168 per thread)
 __global__ void __launch_bounds__((NG * GW + 2) * 32, 1)
     bk_fast_kernel(const FastDesc *__restrict__ Fg, InPtrs in, T *__restrict__ out,
                    uint8_t *__restrict__ arg, int64_t row_begin, int64_t t_begin, int64_t t_end) {
@@ -390,7 +389,7 @@ __global__ void __launch_bounds__((NG * GW + 2) * 32, 1)
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ int32_t sbase[kMaxStages * 32];
   __shared__ int64_t rowstart[kMaxStages];
-  // output staging handshake: ofull[g][b] completes when the 8 warps of group
+  // output staging handshake: ofull[g][b] completes when the GW warps of group
   // g have staged a tile in buffer b; oempty[g][b] when its bulk store has
   // read it; ostart[g][b] = that tile's first output row (relative)
   __shared__ uint64_t ofull[NG][kOutBufsMax], oempty[NG][kOutBufsMax];
@@ -693,27 +692,27 @@ cudaError_t launch_one(const FastDesc *d, const InPtrs &in, void *out, uint8_t *
   return cudaGetLastError();
 }
 
-// two consumer groups per CTA (one CTA per SM, shared ring); 8 warps each for
-// int32 shapes whose register blocks fit 96 registers per thread, 4 warps
-// each for f64 and the large int32 shapes (their blocks need up to 168; the
-// smaller groups also keep small f64 tiles' threads busy).
+// two consumer groups of 4 warps per CTA (one CTA per SM, shared ring; 10
+// warps, 168 registers per thread).  Measured against 8-warp groups at 96
+// registers (int32 shapes): each thread now owns ~2 register blocks per
+// tile, so the per-tile work is amortised, and no shape is register-capped
+// (C4 31.4 -> 29.6 ms, C3 MBE(16) 32.4 -> 31.4 ms; f64 shapes already used 4).
 constexpr int ng_of(int, int, int, int) { return 2; }
-constexpr int gw_of(int es, int R, int R2, int DV) { return (es == 4 && R * R2 * DV <= 27) ? 8 : 4; }
+constexpr int gw_of(int, int, int, int) { return 4; }
 
 // the hottest shape (C4, C3: d = 3, two radix-3 group digits, infinity-free)
 // with its class structure as a template parameter
 template <int CS>
 cudaError_t launch_333_cs(const FastDesc *d, const InPtrs &in, void *out, uint8_t *arg, int64_t rb, int64_t t0,
                           int64_t t1, int grid, int block, int smem, cudaStream_t s) {
-  return launch_one<int32_t, 3, 3, 3, false, true, 2, 8, CS>(d, in, out, arg, rb, t0, t1, grid, block, smem, s);
+  return launch_one<int32_t, 3, 3, 3, false, true, 2, 4, CS>(d, in, out, arg, rb, t0, t1, grid, block, smem, s);
 }
 using Launch333 = cudaError_t (*)(const FastDesc *, const InPtrs &, void *, uint8_t *, int64_t, int64_t, int64_t,
                                   int, int, int, cudaStream_t);
 constexpr Launch333 kLaunch333[16] = {
     launch_333_cs<0>, launch_333_cs<1>, launch_333_cs<2>,  launch_333_cs<3>,  launch_333_cs<4>,  launch_333_cs<5>,
-    launch_333_cs<6>, launch_333_cs<-1>, launch_333_cs<8>, launch_333_cs<9>,  launch_333_cs<10>, launch_333_cs<11>,
-    launch_333_cs<12>, launch_333_cs<13>, launch_333_cs<14>, launch_333_cs<-1>};  // 7, 15: all classes
-    // present -- the specialised kernels spill at 96 registers, the generic one does not
+    launch_333_cs<6>, launch_333_cs<7>, launch_333_cs<8>,  launch_333_cs<9>,  launch_333_cs<10>, launch_333_cs<11>,
+    launch_333_cs<12>, launch_333_cs<13>, launch_333_cs<14>, launch_333_cs<15>};
 
 template <typename T, bool SP, bool NF>
 cudaError_t dispatch(int R, int R2, int DV, int NGr, const FastDesc *d, const InPtrs &in, void *out,
