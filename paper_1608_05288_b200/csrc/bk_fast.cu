@@ -41,7 +41,7 @@ constexpr uint32_t kInf = GBE_INF_I32;
 constexpr int kMaxStages = 8;
 constexpr int kOutBufsMax = 3;  // output staging buffers per consumer group (2 or 3)
 constexpr int64_t kMinCells = 1 << 10;  // measured: the tiled kernel beats bk_generic from ~1e3 cells
-constexpr int kSmemCap = 200 * 1024;  // dynamic shared memory cap per CTA
+constexpr int kSmemCap = 196 * 1024;  // dynamic shared memory cap per CTA
 
 template <typename T>
 struct SrF;
@@ -165,16 +165,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // slice, tb[L][j], and its first output row, trow[L].  One batch serves the
 // next 32 tiles, so the per-tile issue path is a few shared-memory reads.
 constexpr int kMaxH = 32;
-struct ProdSmem {
+struct ProdTiles {      // one producer's decoded batch
   int64_t tb[32][32];    // [tile in batch][class-ordered input] element offset (shift applied)
   int64_t trow[32];      // first output row of the tile
+};
+struct ProdSmem {
+  ProdTiles pt[2];       // per producer warp
   int64_t hstr[kMaxH][32];
   int64_t hrow[kMaxH];
   int64_t shift[32];
   uint32_t hrad[kMaxH];
 };
 
-__device__ __forceinline__ void decode_batch(ProdSmem &ps, const FastHot &f, int64_t t, int64_t step,
+__device__ __forceinline__ void decode_batch(ProdSmem &ps, ProdTiles &pt, const FastHot &f, int64_t t, int64_t step,
                                              int64_t t_end) {
   const int lane = threadIdx.x & 31;
   const int64_t tl = t + (int64_t)lane * step;
@@ -195,13 +198,13 @@ __device__ __forceinline__ void decode_batch(ProdSmem &ps, const FastHot &f, int
 #pragma unroll
     for (int e = 0; e < kMaxH; e++)
       if (e < f.nH) rs += (int64_t)dg[e] * ps.hrow[e];
-    ps.trow[lane] = rs;
+    pt.trow[lane] = rs;
     for (int j = 0; j < f.k; j++) {
       int64_t acc = -ps.shift[j];
 #pragma unroll
       for (int e = 0; e < kMaxH; e++)
         if (e < f.nH) acc += (int64_t)dg[e] * ps.hstr[e][j];
-      ps.tb[lane][j] = acc;
+      pt.tb[lane][j] = acc;
     }
   }
   __syncwarp();
@@ -210,7 +213,7 @@ __device__ __forceinline__ void decode_batch(ProdSmem &ps, const FastHot &f, int
 // The producer warp issues the TMA copies of batch slot L into stage s (one
 // 1-D bulk copy per input: the 16-byte aligned range covering the slice) and
 // publishes the slice bases for the consumers.
-__device__ __forceinline__ void issue_tile(const ProdSmem &ps, const FastHot &f, const char *my_in, int L,
+__device__ __forceinline__ void issue_tile(const ProdTiles &ps, const FastHot &f, const char *my_in, int L,
                                            int s, unsigned char *sm, uint64_t *full, int32_t *sbase,
                                            int64_t *rowstart) {
   const int lane = threadIdx.x & 31;
@@ -378,7 +381,7 @@ __device__ __forceinline__ void combine_nf(const uint32_t (&P0)[DV], const uint3
 template <typename T, int R, int R2, int DV, bool SP, bool NF, int NG, int GW, int CS = -1>
 // (registers: 2 groups of GW = 4 warps + producer + storer put 3 warps on one
 // SM sub-partition: 168 per thread)
-__global__ void __launch_bounds__((NG * GW + 2) * 32, 1)
+__global__ void __launch_bounds__((NG * GW + 1 + NG) * 32, 1)
     bk_fast_kernel(const FastDesc *__restrict__ Fg, InPtrs in, T *__restrict__ out,
                    uint8_t *__restrict__ arg, int64_t row_begin, int64_t t_begin, int64_t t_end) {
   using S = SrF<T>;
@@ -439,17 +442,23 @@ __global__ void __launch_bounds__((NG * GW + 2) * 32, 1)
   __syncthreads();
   const int warp = threadIdx.x >> 5;
 
-  if (warp == NG * GW) {  // ---- producer warp: TMA ring ----
+  if (warp >= NG * GW + 1) {  // ---- producer warps (one per group): TMA ring ----
+    // producer p issues the tiles of group p (CTA tiles i = p mod NG, stages
+    // i mod nst -- the ring length is a multiple of NG), so one producer's
+    // batch decode overlaps the other's issuing
     const int lane = threadIdx.x & 31;
+    const int p = warp - NG * GW - 1;
+    ProdTiles &pt = ps.pt[p];
     const char *my_in = lane < k ? (const char *)in.p[f.in_idx[lane]] : nullptr;
-    int s = 0, L = 0;
-    uint32_t ph = 0;
-    for (int64_t t = t_begin + blockIdx.x; t < t_end; t += gridDim.x) {
-      if (L == 0) decode_batch(ps, f, t, gridDim.x, t_end);
+    int s = p % nst, L = 0;
+    uint32_t ph = (uint32_t)((p / nst) & 1);
+    for (int64_t t = t_begin + blockIdx.x + (int64_t)p * gridDim.x; t < t_end; t += (int64_t)NG * gridDim.x) {
+      if (L == 0) decode_batch(ps, pt, f, t, (int64_t)NG * gridDim.x, t_end);
       mbar_wait(&empty[s], ph ^ 1u);
-      issue_tile(ps, f, my_in, L, s, sm, full, sbase, rowstart);
-      if (++s == nst) {
-        s = 0;
+      issue_tile(pt, f, my_in, L, s, sm, full, sbase, rowstart);
+      s += NG;
+      if (s >= nst) {
+        s -= nst;
         ph ^= 1u;
       }
       L = (L + 1) & 31;
@@ -459,7 +468,7 @@ __global__ void __launch_bounds__((NG * GW + 2) * 32, 1)
   const int PL = f.PL, es = (int)sizeof(T);
   const int nob = f.nout;
 
-  if (warp == NG * GW + 1) {  // ---- storer warp: TMA bulk stores of staged tiles ----
+  if (warp == NG * GW) {  // ---- storer warp: TMA bulk stores of staged tiles ----
     // tiles in CTA order (tile i: group i mod NG, its buffer (i / NG) mod nob);
     // the buffer of tile i - 1 is released once tile i is committed and at
     // most one store group is still reading shared memory
@@ -838,7 +847,7 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     const int64_t Pmid = PL / (R * R2);
     if (row_begin % PL || row_end % PL) continue;
     const int NG = ng_of(es, R, R2, DV), GW = gw_of(es, R, R2, DV);
-    const size_t kSmemMax = (size_t)(smem_env ? std::atoi(smem_env) : 200) * 1024;
+    const size_t kSmemMax = (size_t)(smem_env ? std::atoi(smem_env) : 196) * 1024;
     const int min_st = pass == 0 ? std::max(kStagesWant, 2 * NG) : NG;
     // classes
     std::memset(&F, 0, sizeof(F));
@@ -953,7 +962,7 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     L.g1 = g1;
     L.g2 = g2;
     L.nf = noinf && es == 4 && h.semiring == GBE_MINSUM_I32;
-    L.block = (NG * GW + 2) * 32;
+    L.block = (NG * GW + 1 + NG) * 32;
     L.t_begin = row_begin / PL;
     L.t_end = row_end / PL;
     int per_sm = (int)std::min<size_t>(std::max<size_t>(1, (220 * 1024) / (off + 4096)), 2048 / L.block);
