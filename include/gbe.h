@@ -257,6 +257,11 @@ typedef struct gbe_bucket_desc {
 /* With semiring GBE_SUMPROD_F64: out = -log sum_v exp(-s_v) (m - log sum_v
  * exp(m - s_v), m = min_v s_v; +inf rows stay +inf) and arg = 0.
  * desc: HOST pointer; dev_inputs[k]: device pointers to int32 or double tables;
+ * the tiled variant reads inputs in whole 16-byte-aligned granules (TMA bulk
+ * copies), i.e. up to 15 bytes before the first and after the last element
+ * it needs: every granule that holds an element of an input must lie in
+ * readable device memory (true for any table inside a cudaMalloc / pool
+ * allocation, whose sizes are rounded to >= 256 bytes);
  * dev_out: device array of (row_end - row_begin) int32/double; dev_arg: device
  * uint8 array of the same length or NULL.  Asynchronous on `stream`.
  * Errors: GBE_E_INVALID (sizes, d > 256, k > GBE_MAX_INPUTS), GBE_E_CUDA. */
@@ -284,6 +289,21 @@ gbe_status gbe_set_allocator(void *(*alloc_fn)(size_t, void *stream, void *u),
 gbe_status gbe_set_allgather(int (*ag)(const void *send, void *recv, size_t bytes,
                                        void *stream, void *u),
                              void *u);
+
+/* Table inspection (checksums, parity tests, streaming tables to the host):
+ * fn is called on the host after each (mini-)bucket of a solve / UTIL phase
+ * has been computed on this rank and before its message can be freed, with
+ * task = creation index (gbe_plan_info order), dev_out = its `rows` local
+ * output rows (first global row row_begin) and dev_arg = their argmins (the
+ * executor computes them into a scratch buffer when the plan does not retain
+ * argmins; NULL for sum-product plans).  The pointers are valid only during
+ * the call; `stream` (cudaStream_t) has completed the bucket.  While a hook
+ * is installed solves run the buckets in creation order without a CUDA
+ * graph.  A non-zero return aborts the solve with GBE_E_INTERNAL.  NULL
+ * removes the hook. */
+gbe_status gbe_set_table_hook(int (*fn)(int32_t task, const void *dev_out, const uint8_t *dev_arg,
+                                        int64_t row_begin, int64_t rows, void *stream, void *u),
+                              void *u);
 
 /* Built-in NCCL transport for the all-gather (NVLink 5 / NVSwitch), loaded
  * with dlopen("libnccl.so.2").  Rank 0 calls gbe_comm_nccl_id(id[128]) and

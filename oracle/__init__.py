@@ -55,6 +55,10 @@ def lib():
                                      I32P, F64P, U8P, ctypes.c_int32]
         L.or_solve.argtypes = [PP, I32P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
         L.or_solve.restype = ctypes.c_void_p
+        L.or_bucket_row_sums.argtypes = [I32P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                         ctypes.c_int32, I32P, I64P, I32P,
+                                         ctypes.POINTER(I32P), ctypes.POINTER(F64P),
+                                         ctypes.c_int32, I32P, ctypes.c_int64, I64P, I64P, F64P]
         L.or_bucket_rows_sp.argtypes = [I32P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                         I32P, I64P, I32P, ctypes.POINTER(F64P), ctypes.c_int32,
                                         I32P, ctypes.c_int64, ctypes.c_int64, F64P, ctypes.c_int32]
@@ -91,6 +95,11 @@ def lib():
         L.or_evaluate_f.restype = ctypes.c_double
         L.or_fnv1a.argtypes = [ctypes.c_uint64, ctypes.c_void_p, ctypes.c_int64]
         L.or_fnv1a.restype = ctypes.c_uint64
+        L.or_mixsum.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
+                                ctypes.c_int32]
+        L.or_mixsum.restype = ctypes.c_uint64
+        L.or_set_digest_kind.argtypes = [ctypes.c_int32]
+        L.or_set_digest_kind.restype = None
         _LIB = L
     return _LIB
 
@@ -180,6 +189,22 @@ def fnv1a(*arrays) -> int:
     return int(h)
 
 
+def mixsum(a, salt, nthreads=0) -> int:
+    """or_mixsum: position-keyed sum checksum of a 1/4/8-byte array (mod 2^64)."""
+    a = np.ascontiguousarray(a)
+    return int(lib().or_mixsum(a.ctypes.data, a.itemsize, a.size, salt, nthreads))
+
+
+def mix_digest(out, arg, nthreads=0) -> int:
+    """Table digest of digest kind 1: mixsum(out, 1) + mixsum(arg, 2) mod 2^64."""
+    return (mixsum(out, 1, nthreads) + mixsum(arg, 2, nthreads)) & ((1 << 64) - 1)
+
+
+def set_digest_kind(kind: int):
+    """Digest or_solve records per table: 0 FNV-1a (default), 1 mix_digest."""
+    lib().or_set_digest_kind(int(kind))
+
+
 def bucket_eval(dom, is_f64, x, members, sep, row_begin=0, row_end=None, nthreads=0):
     """Rows [row_begin, row_end) of pi_{-x}(sum members); sep most significant
     first.  members = [(scope, flat table in that scope order)]."""
@@ -212,6 +237,42 @@ def bucket_eval(dom, is_f64, x, members, sep, row_begin=0, row_end=None, nthread
                          _p(out, ctypes.c_double) if is_f64 else None,
                          _p(arg, ctypes.c_uint8), nthreads)
     return out[:nrows], arg[:nrows]
+
+
+def _members_c(members, is_f64):
+    nm = len(members)
+    mar = np.array([len(s) for s, _ in members] + [0], dtype=np.int32)
+    moff = np.zeros(nm + 1, dtype=np.int64)
+    moff[1:] = np.cumsum(mar[:nm]) if nm else []
+    msc = np.array([int(v) for s, _ in members for v in s] + [0], dtype=np.int32)
+    tabs = [np.ascontiguousarray(t, dtype=np.float64 if is_f64 else np.int32) for _, t in members]
+    it = (I32P * (nm + 1))()
+    ft = (F64P * (nm + 1))()
+    for k, t in enumerate(tabs):
+        if is_f64:
+            ft[k] = _p(t, ctypes.c_double)
+        else:
+            it[k] = _p(t, ctypes.c_int32)
+    return nm, mar, moff, msc, tabs, it, ft
+
+
+def bucket_row_sums(dom, is_f64, x, members, sep, rows):
+    """Aggregated sums (before the min over x) of the given output rows:
+    array [len(rows), d] -- or_bucket_row_sums."""
+    dom = np.ascontiguousarray(dom, dtype=np.int32)
+    sep = [int(v) for v in sep]
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    nm, mar, moff, msc, tabs, it, ft = _members_c(members, is_f64)
+    sepa = np.array(sep + [0], dtype=np.int32)
+    d = int(dom[x])
+    si = np.zeros(max(rows.size * d, 1), dtype=np.int64)
+    sf = np.zeros(max(rows.size * d, 1), dtype=np.float64)
+    lib().or_bucket_row_sums(_p(dom, ctypes.c_int32), len(dom), int(is_f64), int(x), nm,
+                             _p(mar, ctypes.c_int32), _p(moff, ctypes.c_int64), _p(msc, ctypes.c_int32),
+                             it, ft, len(sep), _p(sepa, ctypes.c_int32), rows.size, _p(rows, ctypes.c_int64),
+                             _p(si, ctypes.c_int64), _p(sf, ctypes.c_double))
+    s = sf if is_f64 else si
+    return s[:rows.size * d].reshape(rows.size, d)
 
 
 def bucket_eval_sp(dom, x, members, sep, row_begin=0, row_end=None, nthreads=0):

@@ -31,6 +31,40 @@ uint64_t or_fnv1a(uint64_t h, const void *data, int64_t nbytes) {
   return h;
 }
 
+/* Position-keyed checksum of a table (not method arithmetic): element i with
+ * bits x (zero-extended: u8 argmin, uint32 view of an int32, f64 bits) maps
+ * to z = mix(i * 0x9E3779B97F4A7C15 + x + salt * 0xD1B54A32D192ED03) with
+ * mix(z) = ((z ^ z>>31) * 0xBF58476D1CE4E5B9) ^ (... >> 29); the digest is
+ * the sum of z mod 2^64.  Unlike FNV-1a it is a sum, so it parallelises
+ * (tables of 1e10 cells) and a GPU-side test can form it with plain torch
+ * ops.  elem = 1, 4 or 8 bytes. */
+uint64_t or_mixsum(const void *data, int32_t elem, int64_t n, uint64_t salt, int32_t nthreads) {
+  uint64_t h = 0;
+#ifdef _OPENMP
+  if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel for reduction(+ : h) schedule(static) num_threads(nthreads)
+#endif
+  for (int64_t i = 0; i < n; i++) {
+    uint64_t x;
+    if (elem == 1)
+      x = ((const uint8_t *)data)[i];
+    else if (elem == 4)
+      x = ((const uint32_t *)data)[i];
+    else
+      x = ((const uint64_t *)data)[i];
+    uint64_t z = (uint64_t)i * 0x9E3779B97F4A7C15ULL + x + salt * 0xD1B54A32D192ED03ULL;
+    z = (z ^ (z >> 31)) * 0xBF58476D1CE4E5B9ULL;
+    z = z ^ (z >> 29);
+    h += z;
+  }
+  return h;
+}
+
+/* which digest or_solve records per table: 0 FNV-1a over (out bytes, arg
+ * bytes) (default); 1 or_mixsum(out, salt 1) + or_mixsum(arg, salt 2) */
+static int g_digest_kind = 0;
+void or_set_digest_kind(int32_t kind) { g_digest_kind = kind; }
+
 static int32_t *position_of(const int32_t *order, int32_t n) {
   int32_t *pos = (int32_t *)malloc(sizeof(int32_t) * (n ? n : 1));
   for (int i = 0; i < n; i++) pos[order[i]] = i;
@@ -205,6 +239,47 @@ void or_bucket_rows(const int32_t *dom, int32_t n, int32_t is_f64, int32_t x,
     }
     free(a);
   }
+}
+
+/* The aggregation step alone (Alg. 1 line 3 before the projection,
+ * P:204-205) for selected rows: sums[q*d + v] = sum_k f_k(theta_q . v) for
+ * theta_q = the row rows[q] of the output scope sep (int: clamped adds, A9;
+ * f64: IEEE adds in member order).  Used by the tests to decide whether two
+ * argmin choices of a row are a near-tie (reading A10); same decode and
+ * re-rank as or_bucket_rows. */
+void or_bucket_row_sums(const int32_t *dom, int32_t n, int32_t is_f64, int32_t x,
+                        int32_t nmem, const int32_t *mar, const int64_t *moff,
+                        const int32_t *mscope, const int32_t *const *itab,
+                        const double *const *ftab, int32_t nsep, const int32_t *sep,
+                        int64_t nrows, const int64_t *rows, int64_t *sums_i, double *sums_f) {
+  int32_t *a = (int32_t *)calloc(n ? n : 1, sizeof(int32_t));
+  const int d = dom[x];
+  for (int64_t q = 0; q < nrows; q++) {
+    int64_t r = rows[q];
+    for (int p = nsep - 1; p >= 0; p--) {
+      a[sep[p]] = (int32_t)(r % dom[sep[p]]);
+      r /= dom[sep[p]];
+    }
+    for (int v = 0; v < d; v++) {
+      a[x] = v;
+      int64_t s_i = 0;
+      double s_f = 0.0;
+      for (int k = 0; k < nmem; k++) {
+        const int32_t *sc = mscope + moff[k];
+        int64_t idx = 0;
+        for (int p = 0; p < mar[k]; p++) idx = idx * dom[sc[p]] + a[sc[p]];
+        if (is_f64)
+          s_f = s_f + ftab[k][idx];
+        else
+          s_i = add_i(s_i, itab[k][idx]);
+      }
+      if (is_f64)
+        sums_f[q * d + v] = s_f;
+      else
+        sums_i[q * d + v] = s_i;
+    }
+  }
+  free(a);
 }
 
 /* Sum-product bucket (the paper's future work):
@@ -583,12 +658,18 @@ static or_run *or_solve_impl(const or_problem *p, const int32_t *order, int32_t 
       free(msc);
       free(it);
       free(ft);
-      uint64_t h = 0xcbf29ce484222325ULL;
-      if (p->is_f64)
-        h = or_fnv1a(h, t.out_f, t.rows * (int64_t)sizeof(double));
-      else
-        h = or_fnv1a(h, t.out_i, t.rows * (int64_t)sizeof(int32_t));
-      t.digest = or_fnv1a(h, t.arg, t.rows);
+      if (g_digest_kind == 1) {
+        t.digest = or_mixsum(p->is_f64 ? (const void *)t.out_f : (const void *)t.out_i, p->is_f64 ? 8 : 4,
+                             t.rows, 1, nthreads) +
+                   or_mixsum(t.arg, 1, t.rows, 2, nthreads);
+      } else {
+        uint64_t h = 0xcbf29ce484222325ULL;
+        if (p->is_f64)
+          h = or_fnv1a(h, t.out_f, t.rows * (int64_t)sizeof(double));
+        else
+          h = or_fnv1a(h, t.out_i, t.rows * (int64_t)sizeof(int32_t));
+        t.digest = or_fnv1a(h, t.arg, t.rows);
+      }
       if (!keep_tables) {
         free(t.arg);
         t.arg = NULL;

@@ -79,6 +79,12 @@ void or_bucket_rows(const int32_t *dom, int32_t n, int32_t is_f64, int32_t x,
 /* Sum-product variant of the bucket (the
  * sum/product semiring of P:210): out = -log sum_v exp(-sum_k f_k), written
  * as m - log sum_v exp(m - s_v) with m = min_v s_v; f64 only, no argmin. */
+/* aggregation only, for selected rows: sums[q*d + v] (tests: near-ties, A10) */
+void or_bucket_row_sums(const int32_t *dom, int32_t n, int32_t is_f64, int32_t x,
+                        int32_t nmem, const int32_t *mar, const int64_t *moff,
+                        const int32_t *mscope, const int32_t *const *itab,
+                        const double *const *ftab, int32_t nsep, const int32_t *sep,
+                        int64_t nrows, const int64_t *rows, int64_t *sums_i, double *sums_f);
 void or_bucket_rows_sp(const int32_t *dom, int32_t n, int32_t x, int32_t nmem,
                        const int32_t *mar, const int64_t *moff, const int32_t *mscope,
                        const double *const *ftab, int32_t nsep, const int32_t *sep,
@@ -154,6 +160,10 @@ double or_evaluate_f(const or_problem *p, const int32_t *assign);
 
 /* FNV-1a 64 of a byte range, seeded with h (use 0xcbf29ce484222325) */
 uint64_t or_fnv1a(uint64_t h, const void *data, int64_t nbytes);
+/* position-keyed sum checksum (parallel; see oracle.c) and the digest kind
+ * or_solve records: 0 FNV-1a (default), 1 mixsum(out,1) + mixsum(arg,2) */
+uint64_t or_mixsum(const void *data, int32_t elem, int64_t n, uint64_t salt, int32_t nthreads);
+void or_set_digest_kind(int32_t kind);
 
 #ifdef __cplusplus
 }

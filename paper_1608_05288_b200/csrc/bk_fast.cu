@@ -5,28 +5,32 @@
 //  * A tile = all values of the trailing output digits L (P_L rows).  For every
 //    input j the tile's slice is ONE contiguous range of d*prod(L ∩ S_j)
 //    elements (the eliminated variable and the trailing output variables are
-//    the least-significant digits of every input), so each tile
-//    needs one 1-D TMA bulk copy (cp.async.bulk, UBLKCP) per input.  A
-//    dedicated producer warp keeps a 3-stage shared-memory ring full
-//    (full/empty mbarriers); 8 consumer warps never block on a CTA barrier.
-//    Small child tables land in shared memory whole; large ones stream slice
-//    by slice.
-//  * Inside a tile each thread owns R x R x d cells: all values of two
+//    the least-significant digits of every input; bkf_build checks
+//    that the tile digits of every input form a dense stride suffix), so each
+//    tile needs one 1-D TMA bulk copy (cp.async.bulk, UBLKCP) per input.
+//  * One CTA per SM, warp-specialised: NG = 2 consumer groups of GW = 4 warps,
+//    one producer warp per group and one storer warp.  The producers keep ONE
+//    ring of up to 8 input stages full (full/empty mbarriers); CTA tile i goes
+//    to stage i mod nstages and to group i mod 2.  Consumers never block on a
+//    CTA barrier.
+//  * Inside a tile each thread owns R x R2 x d cells: all values of one or two
 //    chosen "group" digits g1, g2 in L and of the eliminated variable.  Inputs
 //    are split by which group digits they contain; an input missing a group
 //    digit is loaded once and reused across that digit's R values, so the
-//    shared-memory loads and saturating adds per cell drop from k to
+//    shared-memory loads and adds per cell drop from k to
 //    sum_j R^-|{g1,g2} \ S_j| (the host picks g1, g2 to minimise this).
-//  * Index math is per tile (one mixed-radix decode by the producer warp) and
-//    per thread group (a shared-memory offset table built once per CTA): no
-//    per-row div/mod.
-//  * Output rows and argmins are stored straight from registers.
+//  * Index math is per tile (a batched mixed-radix decode by the producer
+//    warps) and per thread group (a shared-memory offset table built once per
+//    CTA): no per-row div/mod.
+//  * Output rows and argmins are staged in shared memory (2-3 buffers per
+//    group) and written by TMA bulk stores issued by the storer warp.
 //  * Tile order: the output digits missing from the largest input vary
 //    fastest, so tiles that re-read the same input slice run back to back and
 //    hit L2 instead of HBM.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -692,10 +696,15 @@ template <typename T, int R, int R2, int DV, bool SP, bool NF, int NG, int GW, i
 cudaError_t launch_one(const FastDesc *d, const InPtrs &in, void *out, uint8_t *arg, int64_t rb,
                        int64_t t0, int64_t t1, int grid, int block, int smem, cudaStream_t s) {
   auto kern = bk_fast_kernel<T, R, R2, DV, SP, NF, NG, GW, CS>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemCap);
-    attr_set = true;
+  // the shared-memory opt-in is per device: one bit per device ordinal
+  static std::atomic<uint64_t> attr_set{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  if (!(attr_set.load(std::memory_order_acquire) & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemCap);
+    if (e != cudaSuccess) return e;
+    attr_set.fetch_or(bit, std::memory_order_acq_rel);
   }
   kern<<<grid, block, smem, s>>>(d, in, (T *)out, arg, rb, t0, t1);
   return cudaGetLastError();
@@ -876,7 +885,23 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
       }
     }
     f.cls_off[4] = jj;
-    // mid digits (L minus g1, g2), natural order
+    // every input's tile slice must be ONE contiguous range of slen elements:
+    // the tile digits it has, walked from the least significant, carry the
+    // dense strides DV, DV*r, ... (canonical layouts always do; the bare
+    // primitive accepts arbitrary strides, which go to bk_generic)
+    bool dense = true;
+    for (int j = 0; j < k && dense; j++) {
+      int64_t want = DV;
+      for (int p = m - 1; p >= m - nl; p--) {
+        if (!has(j, p)) continue;
+        if (h.stride[j][p] != want) dense = false;
+        want *= h.radix[p];
+      }
+    }
+    if (!dense) continue;
+    // mid digits (L minus g1, g2), natural order; FastHot holds at most 12
+    // (radix-1 digits would let the count exceed it)
+    if (nl - (g2 >= 0 ? 2 : 1) > 12) continue;
     f.nmid = 0;
     int64_t rowst = 1;
     std::vector<int64_t> rowstride(m);
@@ -965,6 +990,7 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     L.block = (NG * GW + 1 + NG) * 32;
     L.t_begin = row_begin / PL;
     L.t_end = row_end / PL;
+    if (L.t_end >= (int64_t(1) << 32)) return false;  // the producer decodes 32-bit tile indices
     int per_sm = (int)std::min<size_t>(std::max<size_t>(1, (220 * 1024) / (off + 4096)), 2048 / L.block);
     per_sm = std::max(1, std::min(per_sm, NG == 2 ? 1 : 8));
     int64_t tiles = L.t_end - L.t_begin;

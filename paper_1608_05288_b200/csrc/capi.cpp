@@ -304,6 +304,11 @@ gbe_status gbe_set_allgather(int (*ag)(const void *, void *, size_t, void *, voi
   return guard([&] { set_allgather(ag, u); });
 }
 
+gbe_status gbe_set_table_hook(int (*fn)(int32_t, const void *, const uint8_t *, int64_t, int64_t, void *, void *),
+                              void *u) {
+  return guard([&] { set_table_hook(fn, u); });
+}
+
 gbe_status gbe_comm_nccl_id(void *id128) {
   return guard([&] {
     if (!id128) GBE_FAIL(GBE_E_INVALID, "null id");

@@ -36,6 +36,13 @@ static void (*g_free)(void *, void *) = nullptr;
 static void *g_alloc_u = nullptr;
 static int (*g_ag)(const void *, void *, size_t, void *, void *) = nullptr;
 static void *g_ag_u = nullptr;
+static TableHook g_hook = nullptr;
+static void *g_hook_u = nullptr;
+
+void set_table_hook(TableHook fn, void *u) {
+  g_hook = fn;
+  g_hook_u = u;
+}
 
 void set_allocator(void *(*a)(size_t, void *, void *), void (*f)(void *, void *), void *u) {
   g_alloc = a;
@@ -787,7 +794,27 @@ static void run_util(RunImpl &R) {
     for (int j = 0; j < P.tasks[ti].desc.ninputs; j++) cins[ti].p[j] = cnt_ptr(P.tasks[ti].members[j]);
 
   DevPlan::Arena &A = *R.A;
-  const bool graph = P.ex.graph && W == 1 && !g_alloc && !R.arena_own && !P.ex.host_args;
+  // a table hook inspects every bucket on the host: serial, no graph, and an
+  // argmin scratch buffer when the plan does not retain argmins
+  const TableHook hook = g_hook;
+  void *const hook_u = g_hook_u;
+  const bool graph = P.ex.graph && W == 1 && !g_alloc && !R.arena_own && !P.ex.host_args && !hook;
+  uint8_t *hook_arg = nullptr;
+  if (hook && !want_arg && !host_args && !P.ex.sumprod) {
+    int64_t mx = 1;
+    for (auto &t : P.tasks) mx = std::max<int64_t>(mx, t.shard.hi - t.shard.lo);
+    hook_arg = (uint8_t *)dalloc((size_t)mx, s);
+  }
+  struct HookArgFree {
+    uint8_t *p;
+    cudaStream_t s;
+    ~HookArgFree() {
+      if (p) {
+        cudaStreamSynchronize(s);
+        dfree(p, s);
+      }
+    }
+  } hook_arg_free{hook_arg, s};
   if (graph) {  // persistent per-arena scalars, pinned result slot, events
     if (!A.d_opt) {
       CK(cudaMalloc(&A.d_opt, 16));
@@ -875,7 +902,7 @@ static void run_util(RunImpl &R) {
         branch_of[ti] = b;
       }
       void *out = gathered_src[ti] ? gathered_src[ti] : R.base + R.A->off_out[ti];
-      uint8_t *argp = want_arg && !host_args ? (uint8_t *)(R.base + R.A->off_arg[ti]) : nullptr;
+      uint8_t *argp = want_arg && !host_args ? (uint8_t *)(R.base + R.A->off_arg[ti]) : hook_arg;
       if (P.ex.timing) rec(ev[3 * ti]);
       for (int32_t mi : D->task_merges[ti]) {
         const DevPlan::Merge &M = D->merges[mi];
@@ -914,6 +941,12 @@ static void run_util(RunImpl &R) {
       else
         CK(bk_launch(D->h_desc[ti], D->d_desc + ti, ins[ti], out, argp, sh.lo, sh.hi, D->launch[ti], st));
       if (P.ex.timing) rec(ev[3 * ti + 2]);
+      if (hook) {
+        CK(cudaStreamSynchronize(st));
+        const uint8_t *ha = host_args ? nullptr : argp;
+        if (hook((int32_t)ti, out, ha, sh.lo, sh.hi - sh.lo, (void *)st, hook_u) != 0)
+          GBE_FAIL(GBE_E_INTERNAL, "table hook failed on task %zu (x%d)", ti, t.var);
+      }
       static const bool sync_each = std::getenv("GBE_SYNC_EACH") != nullptr;  // debugging knob
       if (sync_each && !capturing) {
         cudaError_t e = cudaStreamSynchronize(st);

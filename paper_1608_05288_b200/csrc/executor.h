@@ -8,6 +8,8 @@ struct RunImpl;
 
 void set_allocator(void *(*a)(size_t, void *, void *), void (*f)(void *, void *), void *u);
 void set_allgather(int (*ag)(const void *, void *, size_t, void *, void *), void *u);
+using TableHook = int (*)(int32_t, const void *, const uint8_t *, int64_t, int64_t, void *, void *);
+void set_table_hook(TableHook fn, void *u);
 void dev_plan_free(void *d);
 void comm_nccl_id(void *id128);
 void comm_nccl_init(const void *id128, int nranks, int rank, int device);

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "kernels.h"
 
@@ -338,8 +339,17 @@ BkLaunchInfo bk_plan_launch(const gbe_bucket_desc &h, int64_t row_begin, int64_t
   const int k = h.ninputs > 0 ? h.ninputs : 1;
   const int plow_max = std::max(1, std::min(1024, 12288 / k));  // <= 48 KB smem
   int nlow = 0, plow = 1;
+  // the per-CTA low-digit offsets are int32: stop before any input's largest
+  // in-tile offset reaches 2^31 (only arbitrary strides of the bare primitive)
+  std::vector<int64_t> maxoff(k, 0);
   while (nlow < h.nsep && (int64_t)plow * h.radix[h.nsep - 1 - nlow] <= plow_max) {
-    plow *= h.radix[h.nsep - 1 - nlow];
+    const int q = h.nsep - 1 - nlow;
+    bool fits = true;
+    for (int j = 0; j < h.ninputs; j++)
+      if (maxoff[j] + (int64_t)(h.radix[q] - 1) * h.stride[j][q] >= (int64_t(1) << 31)) fits = false;
+    if (!fits) break;
+    for (int j = 0; j < h.ninputs; j++) maxoff[j] += (int64_t)(h.radix[q] - 1) * h.stride[j][q];
+    plow *= h.radix[q];
     nlow++;
   }
   li.nlow = nlow;

@@ -32,6 +32,7 @@ EXPORTED = [
     "gbe_bucket_kernel", "gbe_set_allocator", "gbe_set_allgather", "gbe_last_error",
     "gbe_version", "gbe_bucket_kernel_variant", "gbe_comm_nccl_id", "gbe_comm_nccl_init",
     "gbe_comm_finalize", "gbe_solve_count", "gbe_run_count", "gbe_run_count_table",
+    "gbe_set_table_hook",
 ]
 
 
@@ -60,6 +61,8 @@ AG_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.
                          ctypes.c_void_p, ctypes.c_void_p)
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
 FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)
+HOOK_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                           ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p)
 
 _LIB = None
 
@@ -104,6 +107,7 @@ def lib():
         L.gbe_bucket_kernel_variant.restype = i32
         L.gbe_set_allocator.argtypes = [ALLOC_FN, FREE_FN, vp]
         L.gbe_set_allgather.argtypes = [AG_FN, vp]
+        L.gbe_set_table_hook.argtypes = [HOOK_FN, vp]
         L.gbe_comm_nccl_id.argtypes = [vp]
         L.gbe_comm_nccl_init.argtypes = [vp, i32, i32, i32]
         L.gbe_comm_finalize.argtypes = []
@@ -361,6 +365,32 @@ def set_allgather(fn):
     cb = AG_FN(lambda s, r, n, st, u: int(fn(s, r, n, st)))
     _HOOKS["ag"] = cb
     _check(lib().gbe_set_allgather(cb, None))
+
+
+def set_table_hook(fn):
+    """fn(task, dev_out_ptr, dev_arg_ptr, row_begin, rows, stream_ptr) -> 0, called
+    after every bucket of a solve (gbe_set_table_hook); None removes it.  An
+    exception inside fn aborts the solve (GBE_E_INTERNAL)."""
+    if fn is None:
+        _check(lib().gbe_set_table_hook(HOOK_FN(), None))
+        _HOOKS.pop("table", None)
+        return
+
+    def cb(t, o, a, rb, n, st, u):
+        try:
+            return int(fn(int(t), o, a, int(rb), int(n), st) or 0)
+        except Exception as e:  # noqa: BLE001 -- reported through the status
+            _HOOKS["table_error"] = e
+            return 1
+    h = HOOK_FN(cb)
+    _HOOKS["table"] = h
+    _HOOKS.pop("table_error", None)
+    _check(lib().gbe_set_table_hook(h, None))
+
+
+def table_hook_error():
+    """The exception raised inside the last failing table hook (or None)."""
+    return _HOOKS.get("table_error")
 
 
 def set_allocator(alloc, free):

@@ -7,7 +7,10 @@ configs; for the f64 config (C5) the f64 sum / min / max of the finite
 entries and the count of infinite ones (the tiled kernel's f64 summation order
 differs from the oracle's canonical order, so digests would not be stable).
 
-  python scripts/make_golden.py [c2] [c4] [c3] [c5]
+  python scripts/make_golden.py [c2] [c4] [c3] [c5] [c3i18]
+
+c3i18 (MBE i = 18 on the 20x20 grid, 3.8e11 cells, value-only) records
+digests of kind 1 (oracle.mix_digest) instead of FNV-1a.
 """
 import json
 import math
@@ -41,6 +44,24 @@ def int_record(name, inst, order, ib, keep):
            "tables": [{"var": t.var, "mb": t.mb, "rows": t.rows, "digest": f"{t.digest:016x}"} for t in r.tables],
            "oracle_seconds": dt}
     print(f"{name} i={ib}: value {r.value} upper {rec['upper']} tables {len(r.tables)} in {dt:.1f}s", flush=True)
+    return rec
+
+
+def mix_record(name, inst, order, ib, nthreads):
+    """Value-only oracle run (messages freed once consumed, no forward pass)
+    recording per-table digests of kind 1 (oracle.mix_digest: a parallel
+    position-keyed sum, which a GPU test can form on the device)."""
+    oracle.set_digest_kind(1)
+    t0 = time.time()
+    r = oracle.Run(inst, order, ib, keep_tables=False, nthreads=nthreads)
+    dt = time.time() - t0
+    oracle.set_digest_kind(0)
+    assert r.status == 0
+    rec = {"config": name, "ibound": ib, "order": [int(v) for v in order], "value": r.value,
+           "digest_kind": "mix",
+           "tables": [{"var": t.var, "mb": t.mb, "rows": t.rows, "digest": f"{t.digest:016x}"} for t in r.tables],
+           "oracle_seconds": dt, "oracle_threads": nthreads}
+    print(f"{name} i={ib}: value {r.value} tables {len(r.tables)} in {dt:.1f}s", flush=True)
     return rec
 
 
@@ -84,6 +105,11 @@ def main(which):
             recs.append(int_record("C3", inst, order, ib, True))
         recs.append(int_record("C3", inst, order, 16, False))
         json.dump(recs, open(os.path.join(OUT, "c3.json"), "w"))
+    if "c3i18" in which:  # ~3.8e11 cells: hours of oracle time
+        inst = configs.c3()
+        order = configs.c3_order()
+        nthreads = int(os.environ.get("ORACLE_THREADS", "0"))
+        json.dump(mix_record("C3", inst, order, 18, nthreads), open(os.path.join(OUT, "c3_i18.json"), "w"))
     if "c5" in which:
         inst = configs.c5()
         order = oracle.minfill_order(inst)

@@ -235,3 +235,47 @@ def test_host_args_plan_errors():
                      ((), dict(retain="host", host_arg_chunk=0))):
         with pytest.raises(G.GbeError):
             G.Plan(P, order, *args, **kw)
+
+
+def _desc(radix, d, strides, semiring=0):
+    D = G.BucketDesc()
+    D.semiring = semiring
+    D.nsep = len(radix)
+    D.d = d
+    D.ninputs = len(strides)
+    D.rows = int(np.prod(radix, dtype=np.int64)) if radix else 1
+    for q, r in enumerate(radix):
+        D.radix[q] = r
+    for j, st in enumerate(strides):
+        for q, s in enumerate(st):
+            D.stride[j][q] = s
+    return D
+
+
+def test_tiled_kernel_requires_contiguous_tile_slices():
+    """bkf_build takes a descriptor only when every input's
+    tile digits carry dense trailing strides (one contiguous slice per tile).
+    A member stored with its separator digits reversed must not be tiled."""
+    m, d = 10, 3
+    radix = [3] * m
+    canon = [d * 3 ** (m - 1 - q) for q in range(m)]         # ascending scope, x last
+    rev = [d * 3 ** q for q in range(m)]                     # reversed separator order
+    assert G.bucket_kernel_variant(_desc(radix, d, [canon, canon]), 0, 3 ** m) == 1
+    assert G.bucket_kernel_variant(_desc(radix, d, [canon, rev]), 0, 3 ** m) == 0
+    # padded strides (gaps between digits) are not contiguous either
+    pad = [2 * s for s in canon]
+    assert G.bucket_kernel_variant(_desc(radix, d, [canon, pad]), 0, 3 ** m) == 0
+
+
+def test_domain1_digits_do_not_overflow_tile_tables():
+    """radix-1 digits must not push the tiled kernel's
+    middle-digit count past its 12-entry tables (the call must not corrupt
+    memory; it may take either kernel)."""
+    radix = [1, 3] * 15
+    d = 3
+    st, s = [0] * len(radix), d
+    for q in reversed(range(len(radix))):
+        st[q] = s
+        s *= radix[q]
+    v = G.bucket_kernel_variant(_desc(radix, d, [st, st]), 0, int(np.prod(radix)))
+    assert v in (0, 1)

@@ -50,10 +50,24 @@ def close(a, b):
     if not np.array_equal(np.isinf(a), np.isinf(b)): return False
     f = np.isfinite(b)
     return bool(np.all(np.abs(a[f] - b[f]) <= 1e-9 * (1 + np.abs(b[f]))))
+from tests import devtools
+def near_ties_ok(t, ot, arg):
+    bad = np.nonzero(arg != ot.arg)[0]
+    if bad.size == 0:
+        return True
+    mem = []
+    for kind, idx in ot.members:
+        if kind == 0:
+            mem.append(([int(v) for v in inst.scope(idx)], inst.table(idx)))
+        else:
+            mem.append((list(ref.tables[idx].sep), ref.tables[idx].out))
+    sums = oracle.bucket_row_sums([int(v) for v in inst.dom], True, ot.var, mem, ot.sep, bad)
+    res["near_ties"] = res.get("near_ties", 0) + int(bad.size)
+    return bool(devtools.near_tie_ok(sums, arg[bad].astype(np.int64), ot.arg[bad].astype(np.int64)).all())
 for t, (ti, ot) in enumerate(zip(info["tables"], ref.tables)):
     out, arg = run.table(t, ti["rows"])
     if inst.is_f64:
-        ok = close(out, ot.out)
+        ok = close(out, ot.out) and (kind == "sp" or near_ties_ok(t, ot, arg))
     else:
         ok = np.array_equal(out, ot.out) and np.array_equal(arg, ot.arg)
     if not ok:

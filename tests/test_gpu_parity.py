@@ -12,6 +12,7 @@ import pytest
 
 import gen
 import oracle
+from tests import devtools
 import paper_1608_05288_b200 as G
 from gen import configs
 from oracle.brute import brute_force_np
@@ -319,8 +320,13 @@ def test_fast_kernel_shapes(torch_cuda, R, DV, f64):
             np.testing.assert_array_equal(np.isinf(got), np.isinf(exp))
             fin = np.isfinite(exp)
             assert np.allclose(got[fin], exp[fin], rtol=1e-9, atol=0)
-            # argmins may differ only on near-ties (different summation order)
-            assert np.mean(got_arg == exp_arg) > 0.999
+            # argmins may differ only on near-ties (different summation
+            # order): the oracle's own sums of both choices within 1e-9 (A10)
+            bad = np.nonzero(got_arg != exp_arg)[0]
+            if bad.size:
+                sums = oracle.bucket_row_sums(dom, True, x, members, sep, bad)
+                assert devtools.near_tie_ok(sums, got_arg[bad].astype(np.int64),
+                                            exp_arg[bad].astype(np.int64)).all()
         else:
             np.testing.assert_array_equal(got, exp)
             np.testing.assert_array_equal(got_arg, exp_arg)

@@ -1,0 +1,185 @@
+"""The tiled kernel's shared-memory rings wrapped many times (-m gpu).
+
+bk_fast keeps a ring of input stages (full/empty mbarriers, parity flips per
+round) and per-group rings of output staging buffers.  With few tiles per CTA
+the parity never flips, so these buckets are shaped to give every CTA tens of
+tiles: half the members span every output digit, which makes the per-tile
+slices large and the tiles small (a few hundred rows).  Each of the kernel's
+arithmetic paths runs: int32 with INF cells (clamped compare/select), int32
+INF-free (packed-key argmin, taken only when the plan proves the tables
+INF-free -- here through a full solve), f64 min-sum and f64 sum-product.
+Element-wise against the oracle: int32 bit-exact, f64 values within 1e-9
+relative with argmins equal except on oracle-confirmed near-ties (A10).
+"""
+import zlib
+
+import numpy as np
+import pytest
+import torch
+
+import gen
+import oracle
+import paper_1608_05288_b200 as G
+from tests import devtools
+
+pytestmark = pytest.mark.gpu
+INF = G.INF_I32
+
+
+def ring_bucket(rng, R, DV, m, k, kind):
+    dom = [R] * m + [DV]
+    members = []
+    for j in range(k):
+        if j % 2 == 0:
+            sub = list(range(m))
+        else:
+            sub = sorted(q for q in range(m) if rng.random() < 0.6)
+        scope = sub + [m]
+        cells = int(np.prod([dom[v] for v in scope]))
+        if kind == "int":
+            t = rng.integers(0, 1000, cells).astype(np.int64)
+            t[rng.random(cells) < 0.05] = INF
+        else:
+            t = rng.uniform(0, 10, cells)
+            t[rng.random(cells) < 0.03] = np.inf
+        members.append((scope, t))
+    return dom, list(range(m)), m, members
+
+
+def desc_for(dom, sep, x, members, semiring):
+    D = G.BucketDesc()
+    D.semiring = semiring
+    D.nsep = len(sep)
+    D.d = dom[x]
+    D.ninputs = len(members)
+    rows = 1
+    for q, v in enumerate(sep):
+        D.radix[q] = dom[v]
+        rows *= dom[v]
+    D.rows = rows
+    for j, (scope, _) in enumerate(members):
+        st, s = {}, 1
+        for v in reversed(scope):
+            st[v] = s
+            s *= dom[v]
+        for q, v in enumerate(sep):
+            D.stride[j][q] = st.get(v, 0)
+    return D, rows
+
+
+@pytest.mark.parametrize("kind,R,DV,m", [("int", 3, 3, 12), ("int", 2, 4, 17), ("int", 4, 2, 9),
+                                         ("f64", 3, 3, 11), ("f64", 2, 3, 16), ("sp", 3, 3, 11)])
+def test_ring_wraps_bucket_kernel(kind, R, DV, m):
+    rng = np.random.default_rng(zlib.crc32(f"{kind}{R}{DV}{m}".encode()))
+    dom, sep, x, members = ring_bucket(rng, R, DV, m, 8, "int" if kind == "int" else "f64")
+    sr = {"int": G.MINSUM_I32, "f64": G.MINSUM_F64, "sp": G.SUMPROD_F64}[kind]
+    D, rows = desc_for(dom, sep, x, members, sr)
+    assert G.bucket_kernel_variant(D, 0, rows) == 1
+    dt = torch.int32 if kind == "int" else torch.float64
+    ins = [torch.tensor(np.asarray(t), dtype=dt, device="cuda") for _, t in members]
+    out = torch.empty(rows, dtype=dt, device="cuda")
+    arg = torch.empty(rows, dtype=torch.uint8, device="cuda")
+    G.bucket_kernel(D, ins, out, arg, 0, rows)
+    torch.cuda.synchronize()
+    got, got_arg = out.cpu().numpy(), arg.cpu().numpy()
+    if kind == "sp":
+        exp = oracle.bucket_eval_sp(dom, x, members, sep)
+        assert np.array_equal(np.isinf(got), np.isinf(exp))
+        f = np.isfinite(exp)
+        assert np.all(np.abs(got[f] - exp[f]) <= 1e-9 * (1 + np.abs(exp[f])))
+        return
+    exp, exp_arg = oracle.bucket_eval(dom, kind == "f64", x, members, sep)
+    if kind == "int":
+        np.testing.assert_array_equal(got, exp)
+        np.testing.assert_array_equal(got_arg, exp_arg)
+        return
+    assert np.array_equal(np.isinf(got), np.isinf(exp))
+    f = np.isfinite(exp)
+    assert np.all(np.abs(got[f] - exp[f]) <= 1e-9 * np.maximum(1.0, np.abs(exp[f])))
+    bad = np.nonzero(got_arg != exp_arg)[0]
+    if bad.size:
+        sums = oracle.bucket_row_sums(dom, True, x, members, sep, bad)
+        assert devtools.near_tie_ok(sums, got_arg[bad].astype(np.int64), exp_arg[bad].astype(np.int64)).all()
+
+
+@pytest.mark.parametrize("p2,seed", [(0.0, 1), (0.1, 2)])
+def test_ring_wraps_full_solve_int(p2, seed):
+    """A scale-free DCOP whose largest buckets have ~1e7-1e8 cells: the
+    INF-free plan takes the packed-key kernel, the p2 = 0.1 plan the clamped
+    one; every table, argmin and the optimum bit-exact."""
+    inst = gen.scalefree(110, 3, p2, seed)
+    P = G.Problem.from_instance(inst)
+    order, w = P.order()
+    plan = G.Plan(P, order, retain="all")
+    info = plan.info()
+    assert max(t["rows"] * t["d"] for t in info["tables"]) >= 1e6
+    run, root = plan.dpop_util()
+    ref = oracle.solve_be(inst, order)
+    assert root == ref.value
+    for t, (ti, ot) in enumerate(zip(info["tables"], ref.tables)):
+        o, a = run.table(t, ti["rows"])
+        assert np.array_equal(o, ot.out) and np.array_equal(a, ot.arg), t
+    assert list(run.value()) == list(ref.assignment)
+    run.close()
+
+
+def _run(dom, sep, x, members, D, rows, f64=False):
+    dt = torch.float64 if f64 else torch.int32
+    ins = [torch.tensor(np.asarray(t), dtype=dt, device="cuda") for _, t in members]
+    out = torch.empty(rows, dtype=dt, device="cuda")
+    arg = torch.empty(rows, dtype=torch.uint8, device="cuda")
+    G.bucket_kernel(D, ins, out, arg, 0, rows)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), arg.cpu().numpy()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_permuted_member_scopes(seed):
+    """Members stored in a permuted (e.g. reversed) scope order: the bare
+    primitive accepts any strides; the tiled kernel must not take them
+    unless every tile slice is contiguous (bkf_build), and the
+    results are bit-exact either way."""
+    rng = np.random.default_rng(70 + seed)
+    m = 10
+    dom = [3] * m + [3]
+    members = []
+    for j in range(6):
+        sub = sorted(q for q in range(m) if rng.random() < 0.7) + [m]
+        scope = list(reversed(sub)) if j % 2 == 0 else list(rng.permutation(sub))
+        cells = int(np.prod([dom[v] for v in scope]))
+        t = rng.integers(0, 1000, cells).astype(np.int64)
+        t[rng.random(cells) < 0.05] = INF
+        members.append(([int(v) for v in scope], t))
+    sep = list(range(m))
+    D, rows = desc_for(dom, sep, m, members, G.MINSUM_I32)
+    # the eliminated variable must have stride 1: reorder so it is last
+    members2 = []
+    for scope, t in members:
+        arr = np.asarray(t).reshape([dom[v] for v in scope])
+        k = scope.index(m)
+        perm = [i for i in range(len(scope)) if i != k] + [k]
+        members2.append(([scope[i] for i in perm], np.ascontiguousarray(arr.transpose(perm)).reshape(-1)))
+    D, rows = desc_for(dom, sep, m, members2, G.MINSUM_I32)
+    got, ga = _run(dom, sep, m, members2, D, rows)
+    exp, ea = oracle.bucket_eval(dom, False, m, members, sep)
+    np.testing.assert_array_equal(got, exp)
+    np.testing.assert_array_equal(ga, ea)
+
+
+def test_domain1_separator_digits():
+    """Many radix-1 output digits (legal: 1 <= dom) next to real ones: the
+    tiled kernel's middle-digit tables hold 12 entries."""
+    rng = np.random.default_rng(5)
+    dom = [1, 3, 1, 1, 3, 1, 1, 3, 1, 1, 3, 1, 1, 3, 1, 1, 3, 1, 1, 1, 3, 1, 1, 1, 1, 3, 1, 1, 1, 3] + [3]
+    m = len(dom) - 1
+    members = []
+    for j in range(5):
+        sub = sorted(q for q in range(m) if rng.random() < 0.8) + [m]
+        cells = int(np.prod([dom[v] for v in sub]))
+        members.append((sub, rng.integers(0, 500, cells).astype(np.int64)))
+    sep = list(range(m))
+    D, rows = desc_for(dom, sep, m, members, G.MINSUM_I32)
+    got, ga = _run(dom, sep, m, members, D, rows)
+    exp, ea = oracle.bucket_eval(dom, False, m, members, sep)
+    np.testing.assert_array_equal(got, exp)
+    np.testing.assert_array_equal(ga, ea)

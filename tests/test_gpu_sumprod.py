@@ -20,7 +20,7 @@ import oracle
 import paper_1608_05288_b200 as G
 from gen import configs
 
-from test_gpu_parity import FAST_SHAPES, desc_for, random_bucket, uniform_bucket
+from tests.test_gpu_parity import FAST_SHAPES, desc_for, random_bucket, uniform_bucket
 
 pytestmark = pytest.mark.gpu
 

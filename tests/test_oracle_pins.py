@@ -581,3 +581,72 @@ def test_count_tree_closed_form():
     r = oracle.solve_count(ch, oracle.minfill_order(ch), "optimal")
     assert r.value == 0 and r.count == d
     assert oracle.solve_count(ch, oracle.minfill_order(ch), "consistent").count == d ** n
+
+
+# ------------------------------------------- row sums / checksums (test tools)
+
+@pytest.mark.parametrize("is_f64", [False, True])
+def test_bucket_row_sums_against_direct_evaluation(is_f64):
+    """or_bucket_row_sums = Alg. 1 line 3 before the projection:
+    each sum equals the members evaluated directly at theta.v (numpy indexing
+    of the member tables reshaped to their scopes), and min / first minimiser
+    over v equal or_bucket_rows (A8)."""
+    rng = np.random.default_rng(11)
+    dom = [2, 3, 4, 3, 2]
+    x = 2
+    sep = [0, 1, 3, 4]
+    scopes = [(0, 2), (4, 1, 2), (3, 2), (2,), (0, 1, 3, 4, 2)]
+    members = []
+    for sc in scopes:
+        cells = int(np.prod([dom[v] for v in sc]))
+        t = rng.random(cells) * 5 if is_f64 else rng.integers(0, 50, cells).astype(np.int32)
+        if not is_f64:
+            t[rng.random(cells) < 0.2] = INF
+        members.append((list(sc), t))
+    R = int(np.prod([dom[v] for v in sep]))
+    rows = np.arange(R, dtype=np.int64)
+    sums = oracle.bucket_row_sums(dom, is_f64, x, members, sep, rows)
+    out, arg = oracle.bucket_eval(dom, is_f64, x, members, sep)
+    for r in range(R):
+        digits, q = {}, r
+        for v in reversed(sep):
+            digits[v] = q % dom[v]
+            q //= dom[v]
+        for val in range(dom[x]):
+            digits[x] = val
+            tot = 0.0 if is_f64 else 0
+            for sc, t in members:
+                e = t.reshape([dom[v] for v in sc])[tuple(digits[v] for v in sc)]
+                tot = tot + float(e) if is_f64 else min(tot + int(e), INF)
+            assert sums[r, val] == tot
+        assert sums[r].min() == out[r]
+        assert int(np.argmin(sums[r])) == arg[r]
+
+
+def test_mixsum_checksum_properties():
+    """The table checksum (not method arithmetic): equal arrays give equal
+    sums, any single change, swap or shift changes it, and it is the sum of
+    per-element terms (so chunks add up mod 2^64) -- what the GPU tests use
+    to compare 1e10-cell tables without copying them to the host."""
+    rng = np.random.default_rng(3)
+    a = rng.integers(0, 1 << 30, 10001).astype(np.int32)
+    h = oracle.mixsum(a, 1)
+    assert h == oracle.mixsum(a.copy(), 1)
+    b = a.copy(); b[17] += 1
+    assert oracle.mixsum(b, 1) != h
+    b = a.copy(); b[[5, 9]] = b[[9, 5]]
+    assert oracle.mixsum(b, 1) != h
+    assert oracle.mixsum(np.roll(a, 1), 1) != h
+    assert oracle.mixsum(a, 2) != h
+    # pure-Python restatement on a short prefix
+    M = (1 << 64) - 1
+
+    def term(i, x, salt):
+        z = (i * 0x9E3779B97F4A7C15 + x + salt * 0xD1B54A32D192ED03) & M
+        z = ((z ^ (z >> 31)) * 0xBF58476D1CE4E5B9) & M
+        return z ^ (z >> 29)
+    assert oracle.mixsum(a[:50], 1) == sum(term(i, int(x) & 0xFFFFFFFF, 1) for i, x in enumerate(a[:50])) & M
+    u = rng.integers(0, 4, 777).astype(np.uint8)
+    assert oracle.mixsum(u, 2) == sum(term(i, int(x), 2) for i, x in enumerate(u)) & M
+    f = rng.random(99)
+    assert oracle.mixsum(f, 1) == sum(term(i, int(x), 1) for i, x in enumerate(f.view(np.uint64))) & M
