@@ -93,67 +93,108 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def cpu_sample(inst, order, seconds_target=12.0, steps=None):
-    """The oracle (as it stands) on a bounded sample: rows of the largest
-    bucket of this workload, with synthetic member tables of the same shapes."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def oracle_bucket_sampler(inst):
+    """The oracle as it stands on the workload's largest bucket: the bucket
+    structure from oracle/structure.py along the oracle's own min-fill order
+    (no product code on this path), synthetic member tables of the same
+    shapes.  Returns (run(nrows, threads) -> seconds, bucket)."""
     import numpy as np
 
     import oracle
-    import paper_1608_05288_b200 as G
-    P = G.Problem.from_instance(inst)
-    info = G.Plan(P, order).info()
-    t = max(info["tables"], key=lambda t: t["rows"] * t["d"])
+    from oracle.structure import bucket_structure
+    order = oracle.minfill_order(inst)
+    tabs = bucket_structure(inst, order)
+    t = max(tabs, key=lambda t: t["rows"] * t["d"])
     dom = [int(x) for x in inst.dom]
     rng = np.random.default_rng(0)
-    pos = {int(v): i for i, v in enumerate(order)}
     members = []
-    for kind, idx in t["members"]:
-        if kind == 0:
-            sc = sorted([int(v) for v in inst.scope(idx)], key=lambda v: pos[v])
-        else:
-            sc = info["tables"][idx]["sep"]
+    for sc in t["scopes"]:
         cells = int(np.prod([dom[v] for v in sc]))
         members.append((sc, rng.integers(0, 100, cells).astype(np.int32)))
+
+    def run(nrows, threads):
+        t0 = time.perf_counter()
+        oracle.bucket_eval(dom, False, t["var"], members, t["sep"], 0, nrows, nthreads=threads)
+        return time.perf_counter() - t0
+    return run, t
+
+
+def cpu_sample(inst, seconds_target=10.0, seconds_1t=6.0):
+    """cpu_baseline: the oracle on a bounded sample (rows of the largest
+    bucket) at all host cores and at 1 thread (the paper's sequential CPU
+    baseline, P:45, P:908)."""
+    run, t = oracle_bucket_sampler(inst)
     cores = os.cpu_count() or 1
 
-    def run(nrows):
-        t0 = time.perf_counter()
-        oracle.bucket_eval(dom, False, t["var"], members, t["sep"], 0, nrows, nthreads=cores)
-        return time.perf_counter() - t0
-
-    n0 = 20000
-    dt = run(n0)
-    nrows = int(min(t["rows"], max(n0, n0 * seconds_target / max(dt, 1e-6))))
-    dt = run(nrows)
-    return {"cells": nrows * t["d"], "seconds": dt, "cores": cores,
-            "sample": f"rows [0,{nrows}) of the largest bucket (x{t['var']}, {t['rows']} rows, "
-                      f"d={t['d']}, k={len(t['members'])}) with synthetic member tables"}, run, nrows, t["d"]
+    def size(threads, target):
+        n0 = 20000
+        dt = run(n0, threads)
+        return int(min(t["rows"], max(n0, n0 * target / max(dt, 1e-6))))
+    nrows = size(cores, seconds_target)
+    dt = run(nrows, cores)
+    n1 = size(1, seconds_1t)
+    dt1 = run(n1, 1)
+    desc = (f"rows [0,{nrows}) (all cores) and [0,{n1}) (1 thread) of the largest bucket "
+            f"(x{t['var']}, {t['rows']} rows, d={t['d']}, k={len(t['members'])}) with synthetic member "
+            f"tables; bucket structure from oracle/structure.py")
+    return {"value": nrows * t["d"] / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "value_1thread": n1 * t["d"] / dt1, "cpu_model": cpu_model(), "sample": desc,
+            "seconds": dt + dt1}
 
 
 def reference_arm(args, world, rank):
-    """--impl reference: the CPU oracle on the box's host cores."""
+    """--impl reference: the CPU oracle as it stands on the box's host cores
+    (rank 0 only; other ranks exit without work)."""
     if rank != 0:
         return
-    inst, order_none, desc = workload(args.workload)
-    import paper_1608_05288_b200 as G
-    order, w = G.Problem.from_instance(inst).order()
-    base, run, nrows, d = cpu_sample(inst, order, seconds_target=max(2.0, 60.0 / max(args.steps + args.warmup, 1)))
+    inst, _, desc = workload(args.workload)
+    run, t = oracle_bucket_sampler(inst)
+    cores = os.cpu_count() or 1
+    per_step = max(2.0, 60.0 / max(args.steps + args.warmup, 1))
+    n0 = 20000
+    dt0 = run(n0, cores)
+    nrows = int(min(t["rows"], max(n0, n0 * per_step / max(dt0, 1e-6))))
     for _ in range(args.warmup):
-        run(nrows)
+        run(nrows, cores)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        run(nrows)
+        run(nrows, cores)
     dt = (time.perf_counter() - t0) / max(args.steps, 1)
-    val = nrows * d / dt
+    val = nrows * t["d"] / dt
+    sample = (f"rows [0,{nrows}) of the largest bucket (x{t['var']}, {t['rows']} rows, d={t['d']}, "
+              f"k={len(t['members'])}) with synthetic member tables, per step")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
-        "data": "synthetic", "config": {"workload": desc, "sample": base["sample"]},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": base["cores"], "kind": "oracle",
-                         "sample": base["sample"]},
+        "data": "synthetic", "config": {"workload": desc, "sample": sample},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
+
+
+def spawn_ranks(n):
+    """--gpus N without a torchrun environment: launch the same script under
+    torch.distributed.run (one rank per GPU, 127.0.0.1 rendezvous), so the
+    code path is exactly the torchrun one; rank 0 prints the line."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -165,6 +206,8 @@ def main():
     ap.add_argument("--workload", default="c4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -186,7 +229,9 @@ def main():
     P = G.Problem.from_instance(inst)
     order, w = P.order()
     exe = dict(device=local, world_size=world, rank=rank)
+    t0 = time.perf_counter()
     info = G.Plan(P, order, **exe).info()
+    host_plan_ms = (time.perf_counter() - t0) * 1e3
     ntasks = len(info["tables"])
     total_cells = info["total_cells"]
     stream = torch.cuda.current_stream()
@@ -203,7 +248,10 @@ def main():
         sync on both sides; CUDA events on the solve stream; max over ranks.
         Each plan holds one device arena, so plans are measured one at a time."""
         pl = G.Plan(P, order, **opts, **exe)
-        for _ in range(max(args.warmup, 3)):
+        t0 = time.perf_counter()
+        step(pl)  # first solve: device plan, arena, value program (then a graph capture)
+        first_ms = (time.perf_counter() - t0) * 1e3
+        for _ in range(max(args.warmup, 3) - 1):
             step(pl)
         gdist.barrier(pg)
         torch.cuda.synchronize()
@@ -218,16 +266,16 @@ def main():
         ms = e0.elapsed_time(e1) / k
         ms = gdist.max_over_ranks(ms, pg)
         del pl
-        return ms, stats, r
+        return ms, stats, r, first_ms
 
     with ClockSampler(local) as clk:
         # device-resident inputs (the `value` line)
-        ms, _, (root, assign, _) = timed(dict(resident_inputs=True), args.steps)
+        ms, _, (root, assign, _), _ = timed(dict(resident_inputs=True), args.steps)
         # end to end through the C ABI: inputs H2D from pinned host memory and
         # the optimum + assignment D2H inside every step
-        ms_e2e, _, _ = timed(dict(), args.steps)
+        ms_e2e, _, _, first_e2e_ms = timed(dict(), args.steps)
         # roofline pass: same steps with CUDA events around every bucket launch
-        ms_t, stats, _ = timed(dict(resident_inputs=True, timing=True), args.steps)
+        ms_t, stats, _, _ = timed(dict(resident_inputs=True, timing=True), args.steps)
     clocks = clk.summary()
 
     st_last = stats[-1]
@@ -251,9 +299,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        base, _, _, _ = cpu_sample(inst, order)
-        cpu = {"value": base["cells"] / base["seconds"], "unit": UNIT, "cores": base["cores"],
-               "kind": "oracle", "sample": base["sample"]}
+        cpu = cpu_sample(inst)
 
     value = total_cells / (ms * 1e-3)
     line = {
@@ -276,7 +322,10 @@ def main():
         "clocks": clocks,
         "e2e": {"value": total_cells / (ms_e2e * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": int(inst.costs.nbytes),
-                "d2h_bytes_per_step": int(4 * inst.n + 8), "ms_per_step": ms_e2e},
+                "d2h_bytes_per_step": int(4 * inst.n + 8), "ms_per_step": ms_e2e,
+                "planning_ms": {"host_plan": host_plan_ms, "first_solve": first_e2e_ms,
+                                "note": "not in the timed steps: a plan (host planner, then device "
+                                        "descriptors + arena + graph on its first solve) is reused"}},
         # relayout + buckets + input merges + constants (run stats) + the value kernel
         "gpu_launches": args.steps * (int(st_last.get("util_launches", ntasks + 2)) + 1),
         "optimum": root,

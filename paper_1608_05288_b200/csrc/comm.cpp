@@ -83,7 +83,7 @@ void comm_nccl_init(const void *id128, int nranks, int rank, int device) {
   std::memcpy(id.internal, id128, 128);
   ncclResult_t r = n.CommInitRank(&g_comm, nranks, id, rank);
   if (r != 0) GBE_FAIL(GBE_E_COMM, "ncclCommInitRank: %s", n.GetErrorString ? n.GetErrorString(r) : "?");
-  set_allgather(nccl_allgather, nullptr);
+  set_allgather_capturable(nccl_allgather, nullptr);
 }
 
 void comm_finalize() {

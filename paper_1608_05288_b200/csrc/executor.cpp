@@ -49,9 +49,15 @@ void set_allocator(void *(*a)(size_t, void *, void *), void (*f)(void *, void *)
   g_free = f;
   g_alloc_u = u;
 }
+static bool g_ag_graph = false;  // the hook only enqueues stream work (capturable)
 void set_allgather(int (*ag)(const void *, void *, size_t, void *, void *), void *u) {
   g_ag = ag;
   g_ag_u = u;
+  g_ag_graph = false;
+}
+void set_allgather_capturable(int (*ag)(const void *, void *, size_t, void *, void *), void *u) {
+  set_allgather(ag, u);
+  g_ag_graph = ag != nullptr;
 }
 
 static void *dalloc(size_t bytes, cudaStream_t s) {
@@ -145,6 +151,7 @@ struct DevPlan {
     void *vprog = nullptr;  // cached value-phase program (device)
     cudaGraphExec_t exec = nullptr;  // captured UTIL phase
     int runs = 0;
+    bool no_graph = false;  // capture failed (W > 1): eager enqueue
     void *d_opt = nullptr, *d_cp = nullptr, *d_ccp = nullptr, *h_opt = nullptr;
     int32_t *d_assign = nullptr;
     std::vector<cudaEvent_t> ev;
@@ -240,7 +247,8 @@ static void plan_arena(const Plan &P, DevPlan *D, bool mbe_mode) {
   A.off_raw = fl.alloc(raw);
   A.off_sorted = fl.alloc(raw);
   fl.release(A.off_raw, raw);  // raw tables are dead after the relayout
-  const bool want_arg = ((!mbe_mode && P.ex.retain >= 1) || P.ex.retain >= 2) && !P.ex.host_args;
+  // sum-product plans have no argmin (no VALUE phase, A18)
+  const bool want_arg = ((!mbe_mode && P.ex.retain >= 1) || P.ex.retain >= 2) && !P.ex.host_args && !P.ex.sumprod;
   std::vector<size_t> out_b(nt, 0), full_b(nt, 0);
   // ranges[t]: the arena ranges task t writes; a later task overwriting any of
   // them must wait for t and for t's consumer (the only reader of t's output)
@@ -639,6 +647,7 @@ struct RunImpl {
   double count = 0.0;           // counting plans: number of optimal / consistent solutions
   bool util_done = false;
   bool shared_scalars = false;  // d_opt / d_assign belong to the arena (graph path)
+  bool args_written = false;    // the bucket kernels wrote argmin tables (byte accounting)
   ~RunImpl() { release(); }
   void release() {
     if (!D) return;
@@ -755,7 +764,7 @@ static void run_util(RunImpl &R) {
     R.d_raw = R.base + R.A->off_raw;
   }
   R.d_sorted = R.base + R.A->off_sorted;
-  const bool want_arg = (!R.mbe && P.ex.retain >= 1) || P.ex.retain >= 2;
+  const bool want_arg = ((!R.mbe && P.ex.retain >= 1) || P.ex.retain >= 2) && !P.ex.sumprod;
   const bool host_args = P.ex.host_args;
   std::vector<InPtrs> ins(nt), mins(D->merges.size());
   std::vector<void *> gathered_src(nt, nullptr);
@@ -798,7 +807,10 @@ static void run_util(RunImpl &R) {
   // argmin scratch buffer when the plan does not retain argmins
   const TableHook hook = g_hook;
   void *const hook_u = g_hook_u;
-  const bool graph = P.ex.graph && W == 1 && !g_alloc && !R.arena_own && !P.ex.host_args && !hook;
+  // W > 1: the UTIL phase is still one CUDA graph when the all-gather is the
+  // built-in NCCL one (it only enqueues work on the stream; a Python hook
+  // that stages through the host cannot be captured)
+  const bool graph = P.ex.graph && (W == 1 || g_ag_graph) && !g_alloc && !R.arena_own && !P.ex.host_args && !hook;
   uint8_t *hook_arg = nullptr;
   if (hook && !want_arg && !host_args && !P.ex.sumprod) {
     int64_t mx = 1;
@@ -815,6 +827,7 @@ static void run_util(RunImpl &R) {
       }
     }
   } hook_arg_free{hook_arg, s};
+  R.args_written = want_arg || host_args || hook_arg != nullptr;
   if (graph) {  // persistent per-arena scalars, pinned result slot, events
     if (!A.d_opt) {
       CK(cudaMalloc(&A.d_opt, 16));
@@ -884,6 +897,9 @@ static void run_util(RunImpl &R) {
     }
     size_t rr = 0;
     int64_t ring_n = 0;  // argmin chunks streamed so far (host_args)
+    // collectives must run in the same order on every rank: inside the DAG
+    // each all-gathering task also waits for the previous one
+    int last_gather = -1;
     for (size_t ti = 0; ti < nt; ti++) {
       const Task &t = P.tasks[ti];
       const Shard &sh = t.shard;
@@ -898,6 +914,8 @@ static void run_util(RunImpl &R) {
         if (last_on[b] == -2) CK(cudaStreamWaitEvent(st, D->tev[nt], 0));
         for (int32_t k : dp)
           if (branch_of[k] != b) CK(cudaStreamWaitEvent(st, D->tev[k], 0));
+        if (gathered_src[ti] && last_gather >= 0 && branch_of[last_gather] != b)
+          CK(cudaStreamWaitEvent(st, D->tev[last_gather], 0));
         last_on[b] = (int)ti;
         branch_of[ti] = b;
       }
@@ -961,6 +979,7 @@ static void run_util(RunImpl &R) {
         if (g_ag(gathered_src[ti], R.base + R.A->off_full[ti], bytes, (void *)st, g_ag_u) != 0)
           GBE_FAIL(GBE_E_COMM, "all-gather of the message of x%d failed", t.var);
       }
+      if (gathered_src[ti]) last_gather = (int)ti;
       if (dag) {
         CK(cudaEventRecord(D->tev[ti], st));
         st = st0;
@@ -995,26 +1014,39 @@ static void run_util(RunImpl &R) {
     if (!graph) dfree(cp, st);
   };
 
-  if (graph && A.runs > 0) {  // the first run warms up (kernel attributes), later runs replay
+  bool replayed = false;
+  if (graph && A.runs > 0 && !A.no_graph) {  // the first run warms up (kernel attributes), later runs replay
     if (!A.exec) {
       if (!D->cap_stream) CK(cudaStreamCreateWithFlags(&D->cap_stream, cudaStreamNonBlocking));
       cudaGraph_t g = nullptr;
-      CK(cudaStreamBeginCapture(D->cap_stream, cudaStreamCaptureModeThreadLocal));
       try {
-        enqueue(D->cap_stream, true);
-      } catch (...) {
-        cudaStreamEndCapture(D->cap_stream, &g);
-        if (g) cudaGraphDestroy(g);
-        throw;
+        CK(cudaStreamBeginCapture(D->cap_stream, cudaStreamCaptureModeThreadLocal));
+        try {
+          enqueue(D->cap_stream, true);
+        } catch (...) {
+          cudaStreamEndCapture(D->cap_stream, &g);
+          if (g) cudaGraphDestroy(g);
+          g = nullptr;
+          throw;
+        }
+        CK(cudaStreamEndCapture(D->cap_stream, &g));
+        CK(cudaGraphInstantiate(&A.exec, g, 0));
+        CK(cudaGraphDestroy(g));
+      } catch (const Error &) {
+        // a row-sharded plan whose collective cannot be captured runs eagerly
+        // (the collectives then go through the hook stream by stream)
+        if (W == 1) throw;
+        cudaGetLastError();
+        A.exec = nullptr;
+        A.no_graph = true;
       }
-      CK(cudaStreamEndCapture(D->cap_stream, &g));
-      CK(cudaGraphInstantiate(&A.exec, g, 0));
-      CK(cudaGraphDestroy(g));
     }
-    CK(cudaGraphLaunch(A.exec, s));
-  } else {
-    enqueue(s, false);
+    if (A.exec) {
+      CK(cudaGraphLaunch(A.exec, s));
+      replayed = true;
+    }
   }
+  if (!replayed) enqueue(s, false);
   if (graph) A.runs++;
   CK(cudaStreamSynchronize(s));
   R.optimum = read_value(p, hopt);
@@ -1181,7 +1213,9 @@ static std::string stats_json(const RunImpl &R) {
     const Task &t = P.tasks[ti];
     int64_t local = t.shard.hi - t.shard.lo;
     int64_t frac_in = t.rows ? (int64_t)((double)t.in_cells * local / t.rows) : 0;
-    int64_t bytes = (int64_t)p.elem() * (frac_in + local) + ((!R.mbe || P.ex.retain >= 2) ? local : 0);
+    // algorithmic bytes: inputs read once, output written once, and one
+    // argmin byte per row only when the kernel wrote argmins
+    int64_t bytes = (int64_t)p.elem() * (frac_in + local) + (R.args_written ? local : 0);
     if (P.ex.count) {  // + the float64 count tables read (messages) and written
       int64_t msg = 0;
       for (auto &m : t.members)
@@ -1259,7 +1293,9 @@ void run_table(const RunImpl *R, int32_t t, void *host_out, uint8_t *host_arg) {
       src = (const char *)src + P.prob->elem() * T.shard.lo;
     CK(cudaMemcpyAsync(host_out, src, P.prob->elem() * local, cudaMemcpyDeviceToHost, R->stream));
   }
-  if (host_arg && P.ex.host_args) {  // argmins already in (pinned) host memory
+  if (host_arg && P.ex.sumprod) {  // sum-product tables have no argmin
+    std::memset(host_arg, 0, (size_t)local);
+  } else if (host_arg && P.ex.host_args) {  // argmins already in (pinned) host memory
     CK(cudaStreamSynchronize(R->stream));
     std::memcpy(host_arg, R->D->h_harg + R->D->harg_off[t], (size_t)local);
   } else if (host_arg) {

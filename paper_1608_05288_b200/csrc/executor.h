@@ -8,6 +8,9 @@ struct RunImpl;
 
 void set_allocator(void *(*a)(size_t, void *, void *), void (*f)(void *, void *), void *u);
 void set_allgather(int (*ag)(const void *, void *, size_t, void *, void *), void *u);
+// an all-gather that only enqueues stream work (built-in NCCL): the UTIL
+// phase of a row-sharded plan can then be captured as a CUDA graph
+void set_allgather_capturable(int (*ag)(const void *, void *, size_t, void *, void *), void *u);
 using TableHook = int (*)(int32_t, const void *, const uint8_t *, int64_t, int64_t, void *, void *);
 void set_table_hook(TableHook fn, void *u);
 void dev_plan_free(void *d);

@@ -314,13 +314,16 @@ std::unique_ptr<Plan> make_plan(std::shared_ptr<const Problem> pp, const int32_t
     }
   }
 
-  // totals: algorithmic bytes = inputs once + output + argmin
+  // totals: algorithmic bytes = inputs once + output + the
+  // argmin byte when the solve writes argmins (BE / DPOP with retained
+  // argmins, MBE with retained messages, host argmins; never sum-product)
   const int64_t el = (int64_t)p.elem();
+  const bool args = !ex.sumprod && ((ibound < 0 && ex.retain >= 1) || ex.retain >= 2 || ex.host_args);
   plan->total_cells = 0;
   plan->total_bytes = 0;
   for (auto &t : plan->tasks) {
     plan->total_cells += t.rows * t.d;
-    plan->total_bytes += el * t.in_cells + el * t.rows + t.rows;
+    plan->total_bytes += el * t.in_cells + el * t.rows + (args ? t.rows : 0);
   }
 
   // row-shard plan: only tasks with >= shard_min_rows rows.

@@ -199,3 +199,49 @@ def test_c4_sharded_two_ranks_one_gpu(tmp_path):
         assert int(z["root"]) == g["value"] == opt
         assert list(z["assign"]) == list(assign)
         assert int(z["nshard"]) >= 5
+
+
+def _nccl_worker(rank, world, port, out_dir):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE=str(world), RANK=str(rank))
+    import torch
+
+    import paper_1608_05288_b200 as G
+    from gen import configs
+    from paper_1608_05288_b200 import dist as gdist
+    torch.cuda.set_device(rank)
+    pg = gdist.init(rank, "nccl")  # built-in NCCL communicator (bench.py's path)
+    P = G.Problem.from_instance(configs.c4())
+    order, _ = P.order()
+    plan = G.Plan(P, order, device=rank, world_size=world, rank=rank)
+    roots = []
+    for _ in range(3):  # warm-up run, graph capture, replay
+        run, root = plan.dpop_util()
+        assign = run.value()
+        run.close()
+        roots.append(root)
+    np.savez(os.path.join(out_dir, f"nccl{rank}.npz"), roots=np.array(roots), assign=assign)
+    del plan
+    gdist.finish(pg)
+
+
+@pytest.mark.gpu
+def test_c4_sharded_builtin_nccl_two_gpus(tmp_path):
+    """Row-sharded C4 over 2 GPUs with the built-in NCCL all-gather inside
+    the captured UTIL graph (the bench's --gpus 2 path): every run's optimum
+    equals the oracle's golden value and the assignment the 1-GPU one."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    import paper_1608_05288_b200 as G
+    from gen import configs
+    port = _free_port()
+    mp.start_processes(_nccl_worker, args=(2, port, str(tmp_path)), nprocs=2, start_method="spawn")
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "c4.json")))
+    P = G.Problem.from_instance(configs.c4())
+    order, _ = P.order()
+    opt, assign = G.Plan(P, order).solve_be()
+    for r in range(2):
+        z = np.load(tmp_path / f"nccl{r}.npz")
+        assert all(int(x) == g["value"] == opt for x in z["roots"])
+        assert list(z["assign"]) == list(assign)

@@ -650,3 +650,19 @@ def test_mixsum_checksum_properties():
     assert oracle.mixsum(u, 2) == sum(term(i, int(x), 2) for i, x in enumerate(u)) & M
     f = rng.random(99)
     assert oracle.mixsum(f, 1) == sum(term(i, int(x), 1) for i, x in enumerate(f.view(np.uint64))) & M
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_symbolic_bucket_structure_matches_oracle_tables(seed):
+    """oracle/structure.py (the reference arm's planner) gives the same
+    buckets, separators and canonical member lists as the oracle's own BE
+    run (Alg. 1 lines 2-5, A1/A2)."""
+    from oracle.structure import bucket_structure
+    inst = gen.scalefree(30, 3, 0.0, seed) if seed % 2 else gen.random_graph(25, 3, 40, 1, 0.0, seed)
+    order = oracle.minfill_order(inst)
+    ref = oracle.solve_be(inst, order, keep_tables=False)
+    tabs = bucket_structure(inst, order)
+    assert len(tabs) == len(ref.tables)
+    for t, rt in zip(tabs, ref.tables):
+        assert t["var"] == rt.var and t["sep"] == list(rt.sep) and t["rows"] == rt.rows
+        assert t["members"] == rt.members
