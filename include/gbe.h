@@ -144,7 +144,7 @@ gbe_status gbe_pseudotree(const gbe_problem *p, const int32_t *order,
  * greedy first-fit partition, reading A6).  json_exec (NULL ok):
  *   {"device":0, "budget_bytes":N, "world_size":W, "rank":r,
  *    "shard_min_rows":N, "retain":"none"|"args"|"all"|"host", "timing":true,
- *    "kernel":-1|0|1, "resident_inputs":false, "graph":true, "concurrent":true,
+ *    "kernel":-1|0|1|2, "autotune":true, "resident_inputs":false, "graph":true, "concurrent":true,
  *    "semiring":"minsum"|"sumprod", "count":"none"|"optimal"|"consistent",
  *    "host_arg_chunk":N}
  * "retain":"all" keeps every table on the device for gbe_run_table().
@@ -153,7 +153,12 @@ gbe_status gbe_pseudotree(const gbe_problem *p, const int32_t *order,
  * "host_arg_chunk" rows (default 2^28) whose argmins stream out through a
  * 2-slot device ring while the next chunk computes (Fig. 8); the
  * value phase reads them in place.  No CUDA-graph replay for such plans.
- * "kernel" forces the generic (0) or tiled (1) bucket kernel (-1 = auto).
+ * "kernel" forces the generic (0), tiled TMA (1) or streaming (2) bucket
+ * kernel where the bucket fits it (-1 = auto: tiled for int32, streaming for
+ * float64 and for domains d > 5).  With "autotune" (auto only) the first two
+ * solves of a plan time the tiled and the streaming kernel on every bucket
+ * both can run and each bucket keeps the faster one from then on (the
+ * results are the same up to the f64 summation order, reading A10).
  * "resident_inputs" keeps the uploaded tables on the device between solves.
  * "graph" replays the UTIL phase as a CUDA graph from the second solve on
  * (1 GPU); "concurrent" makes that graph the task DAG (a bucket waits only on
@@ -269,9 +274,17 @@ gbe_status gbe_bucket_kernel(const void *desc, const void *const *dev_inputs, vo
                              uint8_t *dev_arg, int64_t row_begin, int64_t row_end,
                              void *stream);
 
+/* The same with the kernel variant chosen by the caller: -1 auto (as
+ * gbe_bucket_kernel), 0 generic, 1 tiled TMA, 2 streaming; GBE_E_INVALID if
+ * the descriptor does not fit the requested variant. */
+gbe_status gbe_bucket_kernel_ex(const void *desc, const void *const *dev_inputs, void *dev_out,
+                                uint8_t *dev_arg, int64_t row_begin, int64_t row_end, void *stream,
+                                int32_t variant);
+
 /* Which kernel variant gbe_bucket_kernel would run for this descriptor and
- * row range: 0 = generic (per-row decode), 1 = tiled TMA + register-blocked
- * (DESIGN.md §5).  Returns -1 for an invalid descriptor. */
+ * row range: 0 = generic (per-row decode), 1 = tiled TMA + register-blocked,
+ * 2 = streaming (lanes over the eliminated domain).  Returns
+ * -1 for an invalid descriptor. */
 int32_t gbe_bucket_kernel_variant(const void *desc, int64_t row_begin, int64_t row_end);
 
 /* ---------------------------------------------------------------------

@@ -1,0 +1,497 @@
+// bk_stream.cu — the streaming bucket kernel (BK, warp-per-row-group).
+//
+// The same operation as every BK variant (Proc. 4 + Proc. 5 fused,
+// P:705-792): out[r] = min_v (+)_j T_j[off_j(r) + v], arg[r] = first
+// minimiser (A8), off_j(r) the index map of Eq. with precomputed
+// strides.  Where the tiled kernel (bk_fast.cu) stages tile slices in shared
+// memory through a TMA ring, this one loads straight from global memory with
+// many warps in flight: it is the variant for buckets whose inputs are few
+// and large (a register-blocked tile saves nothing when every input spans
+// the tile -- e.g. a single input eliminated, C5's k = 1 buckets), for f64
+// tables (whose tile slices leave the ring too few bytes in flight), and for
+// any domain size d up to 256.
+//
+//  * Rows are grouped by LPR lanes ("lanes per row", 1..32): the LPR lanes of
+//    a row split the eliminated variable's domain (lane s takes v = s, s+LPR,
+//    ...) and combine (value, index) pairs with a lexicographic warp-shuffle
+//    min (A8) -- the north star's lanes-over-v mapping; LPR = 1 for d <= 5,
+//    where each lane owns whole rows.  The LPR lanes of a row read
+//    consecutive elements and a warp's row groups are consecutive rows, so a
+//    table spanning the trailing digits is read fully coalesced.
+//  * A warp-tile = all values of the trailing output digits (PL rows); the
+//    in-tile offset of every input is one shared-memory table built once per
+//    CTA (no per-row div/mod).  Warps take warp-tiles round robin; a tile's
+//    base offsets come from one parallel mixed-radix decode (lane q: digit
+//    q; lane j: input j's base).  For a full-range launch the tiles are
+//    enumerated with the digits absent from the largest input varying
+//    fastest, so the tiles that re-read one slice of it are in flight
+//    together and hit L2.
+//  * Loads: each lane issues the loads of UN rows of up to KU inputs before
+//    the first add (memory-level parallelism without the shared-memory ring
+//    of the tiled kernel); vector loads (16 B) where the layout allows.
+//  * int32: saturating adds (A9); f64: IEEE adds in input order (A10);
+//    sum-product: m - log sum_v exp(m - s_v) (A18).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <type_traits>
+#include <vector>
+
+#include "bk_stream.h"
+
+namespace gbe {
+namespace {
+
+constexpr uint32_t kInf = GBE_INF_I32;
+constexpr int kBlock = 256;
+
+template <typename T>
+struct SrS;
+template <>
+struct SrS<int32_t> {
+  using Acc = uint32_t;
+  __device__ __forceinline__ static Acc zero() { return 0u; }
+  __device__ __forceinline__ static Acc inf() { return kInf; }
+  __device__ __forceinline__ static Acc ld(const int32_t *p) { return (uint32_t)__ldg(p); }
+  __device__ __forceinline__ static Acc add(Acc a, Acc b) { return min(a + b, kInf); }
+  __device__ __forceinline__ static int32_t out(Acc a) { return (int32_t)a; }
+};
+template <>
+struct SrS<double> {
+  using Acc = double;
+  __device__ __forceinline__ static Acc zero() { return 0.0; }
+  __device__ __forceinline__ static Acc inf() { return __longlong_as_double(0x7ff0000000000000LL); }
+  __device__ __forceinline__ static Acc ld(const double *p) { return __ldg(p); }
+  __device__ __forceinline__ static Acc add(Acc a, Acc b) { return __dadd_rn(a, b); }
+  __device__ __forceinline__ static double out(Acc a) { return a; }
+};
+
+__device__ __forceinline__ int64_t shfl64(int64_t x, int src) {
+  return (int64_t)__shfl_sync(0xffffffffu, (long long)x, src);
+}
+
+// LPR lanes per row, VPL values per lane, UN row groups per lane per pass.
+// VEC = 1: lane s of a row takes v = s + i * LPR (scalar loads); VEC > 1:
+// lane s takes the VPL = VEC contiguous values v = s * VEC + i with ONE
+// vector load per input (16 or 8 bytes), so the warp's loads of a table that
+// spans the trailing digits are contiguous (needs every offset a multiple of
+// VEC and aligned tables: checked on the host and at launch).  DV > 0: the
+// domain size is that compile-time constant; DV = 0: runtime d, masked.
+template <typename T, int VEC>
+struct VecLd;
+template <>
+struct VecLd<double, 2> {
+  __device__ __forceinline__ static void ld(const double *p, double *v) {
+    const double2 x = __ldg((const double2 *)p);
+    v[0] = x.x;
+    v[1] = x.y;
+  }
+};
+template <>
+struct VecLd<int32_t, 4> {
+  __device__ __forceinline__ static void ld(const int32_t *p, uint32_t *v) {
+    const int4 x = __ldg((const int4 *)p);
+    v[0] = (uint32_t)x.x;
+    v[1] = (uint32_t)x.y;
+    v[2] = (uint32_t)x.z;
+    v[3] = (uint32_t)x.w;
+  }
+};
+template <>
+struct VecLd<int32_t, 2> {
+  __device__ __forceinline__ static void ld(const int32_t *p, uint32_t *v) {
+    const int2 x = __ldg((const int2 *)p);
+    v[0] = (uint32_t)x.x;
+    v[1] = (uint32_t)x.y;
+  }
+};
+
+template <typename T, bool SP, int LPR, int VPL, int DV, int UN, int VEC = 1>
+__global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restrict__ D, InPtrs in,
+                                                    T *__restrict__ out, uint8_t *__restrict__ arg,
+                                                    int64_t row_begin, int64_t row_end, int64_t t0,
+                                                    int64_t ntiles) {
+  using S = SrS<T>;
+  using Acc = typename S::Acc;
+  extern __shared__ int32_t loff[];  // [k][PL] in-tile element offsets
+  const int k = D->k, PL = D->PL, nlow = D->nlow, nhigh = D->nhigh;
+  const int d = DV > 0 ? DV : D->d;
+  for (int idx = threadIdx.x; idx < k * PL; idx += blockDim.x) {
+    const int j = idx / PL;
+    int l = idx - j * PL, o = 0;
+    for (int q = nlow - 1; q >= 0; q--) {
+      const int r = D->lrad[q];
+      o += (l % r) * D->lstr[q][j];
+      l /= r;
+    }
+    loff[idx] = o;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (gw >= ntiles) return;
+  // tile decode: lane q < nhigh computes high digit q of the tile index
+  // (32-bit division when the index fits), lane j < k sums its input's base
+  // offset and every lane the tile's first output row.  Warps take tiles
+  // round robin, so the tiles in flight at any moment form one window of
+  // the enumeration and the tiles re-reading a slice of the largest input
+  // (its absent digits vary fastest) hit L2.
+  int64_t base = 0, row0 = 0;
+  auto decode = [&](int64_t t, int64_t &base, int64_t &row0) {
+    int dig = 0;
+    if (lane < nhigh) {
+      const uint32_t hr = (uint32_t)D->hrad[lane];
+      if (t < (int64_t(1) << 32) && D->hdiv[lane] < (int64_t(1) << 32))
+        dig = (int)(((uint32_t)t / (uint32_t)D->hdiv[lane]) % hr);
+      else
+        dig = (int)((t / D->hdiv[lane]) % hr);
+    }
+    base = 0;
+    row0 = 0;
+    for (int q = 0; q < nhigh; q++) {
+      const int dq = __shfl_sync(0xffffffffu, dig, q);
+      if (lane < k) base += (int64_t)dq * D->hstr[q][lane];
+      row0 += (int64_t)dq * D->hrow[q];
+    }
+    if (lane < k) base -= D->shift[lane];
+  };
+  constexpr int G = 32 / LPR;  // row groups per pass
+  const int grp = lane / LPR, sub = lane % LPR;
+  static_assert(VEC == 1 || (VPL == VEC && DV == LPR * VEC), "vector path: one vector per lane, exact d");
+  // value index of this lane's i-th value
+  auto vix = [&](int i) { return VEC > 1 ? sub * VEC + i : sub + i * LPR; };
+  // inputs in chunks of KU: every load of a chunk is issued before the
+  // first add (the adds keep the input order), so a lane has KU * UN * VPL
+  // loads in flight instead of one input's worth per round trip
+  constexpr int kLaneBytes = UN * VPL * (int)sizeof(T);
+  constexpr int KU = kLaneBytes <= 32 ? 2 : 1;
+  const int lane_off = VEC > 1 ? sub * VEC : sub;
+  const T *pb[KU];  // this tile's first KU input pointers (hoisted per tile)
+  int64_t trow = 0;
+  // one pass = UN row groups of this warp (rows l0 + u * G + grp of the
+  // tile); MASK: rows past the tile or outside [row_begin, row_end) skipped
+  auto pass = [&](auto maskc, int l0) {
+    constexpr bool MASK = decltype(maskc)::value;
+    Acc acc[UN][VPL];
+    bool valid[UN];
+#pragma unroll
+    for (int u = 0; u < UN; u++) {
+      if constexpr (MASK) {
+        const int l = l0 + u * G + grp;
+        const int64_t r = trow + l;
+        valid[u] = l < PL && r >= row_begin && r < row_end;
+      } else {
+        valid[u] = true;
+      }
+#pragma unroll
+      for (int i = 0; i < VPL; i++) acc[u][i] = S::zero();
+    }
+    // input 0 lands straight in the accumulators (0 + x = x: the clamp of A9
+    // and IEEE addition leave it unchanged), later inputs in KU chunks (the
+    // first chunk peeled, so every register array is indexed statically)
+    auto chunk = [&](auto firstc, int j0) {
+      constexpr bool FIRST = decltype(firstc)::value;
+      Acc x[KU][UN][VPL];
+#pragma unroll
+      for (int jj = 0; jj < KU; jj++) {
+        const int j = j0 + jj;
+        if (j >= k) break;
+        const T *pj = FIRST ? pb[jj] : (const T *)in.p[j] + shfl64(base, j) + lane_off;
+        const int32_t *lo = loff + j * PL + l0 + grp;
+#pragma unroll
+        for (int u = 0; u < UN; u++) {
+          if (MASK && !valid[u]) continue;
+          const T *q = pj + lo[u * G];
+          Acc *dst = (FIRST && jj == 0) ? acc[u] : x[jj][u];
+          if constexpr (VEC > 1) {
+            VecLd<T, VEC>::ld(q, dst);
+          } else {
+#pragma unroll
+            for (int i = 0; i < VPL; i++)
+              if (DV > 0 || sub + i * LPR < d) dst[i] = S::ld(q + i * LPR);
+          }
+        }
+      }
+#pragma unroll
+      for (int jj = FIRST ? 1 : 0; jj < KU; jj++) {
+        if (j0 + jj >= k) break;
+#pragma unroll
+        for (int u = 0; u < UN; u++)
+#pragma unroll
+          for (int i = 0; i < VPL; i++)
+            if (DV > 0 || vix(i) < d) acc[u][i] = S::add(acc[u][i], x[jj][u][i]);
+      }
+    };
+    chunk(std::true_type{}, 0);
+    for (int j0 = KU; j0 < k; j0 += KU) chunk(std::false_type{}, j0);
+#pragma unroll
+    for (int u = 0; u < UN; u++) {
+      // this lane's minimum over its values (ascending v: first wins)
+      Acc best = acc[u][0];
+      int bv = vix(0);
+#pragma unroll
+      for (int i = 1; i < VPL; i++)
+        if ((DV > 0 || vix(i) < d) && acc[u][i] < best) {
+          best = acc[u][i];
+          bv = vix(i);
+        }
+      // lexicographic (value, index) min over the row's LPR lanes
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1) {
+        const Acc ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bv, o);
+        if (ob < best || (ob == best && oi < bv)) {
+          best = ob;
+          bv = oi;
+        }
+      }
+      if constexpr (SP) {  // -log sum_v exp(-s_v) = m - log sum_v exp(m - s_v)
+        double z = 0.0;
+        if (best < S::inf()) {
+#pragma unroll
+          for (int i = 0; i < VPL; i++)
+            if (DV > 0 || vix(i) < d) z += exp((double)best - (double)acc[u][i]);
+        }
+#pragma unroll
+        for (int o = LPR / 2; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+        if (best < S::inf()) best = best - log(z);
+        bv = 0;
+      }
+      if (sub == 0 && (!MASK || valid[u])) {
+        const int64_t r = trow + l0 + u * G + grp - row_begin;
+        out[r] = S::out(best);
+        if (arg) arg[r] = (uint8_t)bv;
+      }
+    }
+  };
+  // the NEXT tile of this warp is decoded one tile ahead and its input
+  // slices prefetched into L2 with one bulk (TMA) prefetch per input: the
+  // loads of a tile then find their data in L2, so a warp keeps a whole
+  // tile of bytes in flight without holding registers for them
+  decode(t0 + gw, base, row0);
+  for (int64_t tt = gw; tt < ntiles; tt += nwarps) {
+    int64_t nbase = 0, nrow0 = 0;
+    if (tt + nwarps < ntiles) {
+      decode(t0 + tt + nwarps, nbase, nrow0);
+      if (lane < k && D->pf_bytes[lane] > 0) {
+        const uintptr_t a = (uintptr_t)((const T *)in.p[lane] + nbase);
+        const uintptr_t a16 = a & ~(uintptr_t)15;
+        const uint32_t bytes = (uint32_t)((a + D->pf_bytes[lane] - a16 + 15) & ~(uintptr_t)15);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a16), "r"(bytes) : "memory");
+      }
+    }
+    trow = row0;
+#pragma unroll
+    for (int jj = 0; jj < KU; jj++)
+      if (jj < k) pb[jj] = (const T *)in.p[jj] + shfl64(base, jj) + lane_off;
+    int l0 = 0;
+    if (trow >= row_begin && trow + PL <= row_end)  // whole tile: unmasked passes
+      for (; l0 + G * UN <= PL; l0 += G * UN) pass(std::false_type{}, l0);
+    for (; l0 < PL; l0 += G * UN) pass(std::true_type{}, l0);
+    base = nbase;
+    row0 = nrow0;
+  }
+}
+
+template <typename T, bool SP, int LPR, int VPL, int DV, int UN, int VEC = 1>
+cudaError_t launch(const StreamDesc *dd, const BksLaunch &L, const InPtrs &in, void *out, uint8_t *arg,
+                   int64_t rb, int64_t re, cudaStream_t s) {
+  auto kern = bk_stream<T, SP, LPR, VPL, DV, UN, VEC>;
+  if (L.smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem);
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<L.grid, kBlock, L.smem, s>>>(dd, in, (T *)out, arg, rb, re, L.t0, L.ntiles);
+  return cudaGetLastError();
+}
+
+template <typename T, bool SP>
+cudaError_t dispatch(const StreamDesc *dd, const BksLaunch &L, const InPtrs &in, void *out, uint8_t *arg,
+                     int64_t rb, int64_t re, cudaStream_t s) {
+  // vector path: every input 16-byte aligned (offsets are multiples of VEC,
+  // checked by bks_build)
+  bool aligned = L.vec > 1;
+  for (int j = 0; j < L.k && aligned; j++)
+    if ((uintptr_t)in.p[j] % 16) aligned = false;
+  if (aligned) {
+    if constexpr (sizeof(T) == 8) {
+      if (L.d == 2) return launch<T, SP, 1, 2, 2, 4, 2>(dd, L, in, out, arg, rb, re, s);
+      if (L.d == 8) return launch<T, SP, 4, 2, 8, 4, 2>(dd, L, in, out, arg, rb, re, s);
+    } else {
+      if (L.d == 2) return launch<T, SP, 1, 2, 2, 4, 2>(dd, L, in, out, arg, rb, re, s);
+      if (L.d == 4) return launch<T, SP, 1, 4, 4, 4, 4>(dd, L, in, out, arg, rb, re, s);
+      if (L.d == 8) return launch<T, SP, 2, 4, 8, 4, 4>(dd, L, in, out, arg, rb, re, s);
+      if (L.d == 16) return launch<T, SP, 4, 4, 16, 4, 4>(dd, L, in, out, arg, rb, re, s);
+    }
+  }
+  constexpr bool F = sizeof(T) == 8;
+  static const int un = [] {  // GBE_STREAM_UN: rows per lane per pass for d <= 5 (tuning knob)
+    const char *e = std::getenv("GBE_STREAM_UN");
+    return e ? std::atoi(e) : 0;
+  }();
+#define GBE_UN(DVc, UNdef)                                                                       \
+  {                                                                                              \
+    const int u = un ? un : (UNdef);                                                             \
+    if (u <= 2) return launch<T, SP, 1, DVc, DVc, 2>(dd, L, in, out, arg, rb, re, s);            \
+    if (u <= 4) return launch<T, SP, 1, DVc, DVc, 4>(dd, L, in, out, arg, rb, re, s);            \
+    return launch<T, SP, 1, DVc, DVc, 8>(dd, L, in, out, arg, rb, re, s);                        \
+  }
+  switch (L.d) {
+    case 1: GBE_UN(1, 8)
+    case 2: GBE_UN(2, 8)
+    case 3: GBE_UN(3, F ? 4 : 8)
+    case 4: GBE_UN(4, 4)
+    case 5: GBE_UN(5, F ? 2 : 4)
+    default: break;
+  }
+#undef GBE_UN
+  if (L.d <= 8) return launch<T, SP, 2, 4, 0, 2>(dd, L, in, out, arg, rb, re, s);
+  if (L.d <= 16) return launch<T, SP, 4, 4, 0, 2>(dd, L, in, out, arg, rb, re, s);
+  if (L.d <= 32) return launch<T, SP, 8, 4, 0, 2>(dd, L, in, out, arg, rb, re, s);
+  if (L.d <= 64) return launch<T, SP, 16, 4, 0, 1>(dd, L, in, out, arg, rb, re, s);
+  if (L.d <= 128) return launch<T, SP, 32, 4, 0, 1>(dd, L, in, out, arg, rb, re, s);
+  return launch<T, SP, 32, 8, 0, 1>(dd, L, in, out, arg, rb, re, s);
+}
+
+}  // namespace
+
+int bks_lanes_per_row(int d) {
+  if (d <= 5) return 1;
+  if (d <= 8) return 2;
+  if (d <= 16) return 4;
+  if (d <= 32) return 8;
+  if (d <= 64) return 16;
+  return 32;
+}
+
+bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int num_sms, StreamDesc &S,
+               BksLaunch &L) {
+  const int m = h.nsep, k = h.ninputs, d = h.d;
+  if (k < 1 || k > 32 || d < 1 || d > GBE_MAX_DOMAIN || row_end <= row_begin) return false;
+  // warp-tile: trailing output digits while the CTA's offset table stays
+  // <= 32 KB (k * PL int32) and every in-tile offset fits int32
+  const int pl_max = std::max(1, std::min(4096, 8192 / k));
+  int nlow = 0;
+  int64_t PL = 1;
+  int64_t maxoff[32] = {0};
+  while (nlow < m && PL * h.radix[m - 1 - nlow] <= pl_max) {
+    const int q = m - 1 - nlow;
+    bool fits = true;
+    for (int j = 0; j < k; j++)
+      if (maxoff[j] + (int64_t)(h.radix[q] - 1) * h.stride[j][q] >= (int64_t(1) << 31)) fits = false;
+    if (!fits) break;
+    for (int j = 0; j < k; j++) maxoff[j] += (int64_t)(h.radix[q] - 1) * h.stride[j][q];
+    PL *= h.radix[q];
+    nlow++;
+  }
+  // small buckets: shorter warp-tiles, so that every warp of a full grid
+  // gets one (down to 128 rows)
+  const int64_t want_tiles = (int64_t)num_sms * 2 * (kBlock / 32);
+  while (nlow > 0 && PL > 128 && (row_end - row_begin + PL - 1) / PL < want_tiles) {
+    nlow--;
+    const int q = m - 1 - nlow;
+    PL /= h.radix[q];
+  }
+  std::memset(&S, 0, sizeof(S));
+  S.k = k;
+  S.d = d;
+  S.nlow = nlow;
+  S.PL = (int32_t)PL;
+  for (int q = 0; q < nlow; q++) {  // low digits, most significant first
+    const int p = m - nlow + q;
+    S.lrad[q] = h.radix[p];
+    for (int j = 0; j < k; j++) S.lstr[q][j] = (int32_t)h.stride[j][p];
+  }
+  // high digits (radix-1 digits are always 0 and are dropped).  A launch
+  // over all rows enumerates tiles with the digits absent from the largest
+  // input varying fastest: the tiles re-reading one slice of it then run
+  // back to back in a warp and hit L1/L2 instead of HBM
+  int hd[GBE_MAX_SEP], nh = 0;
+  for (int p = 0; p < m - nlow; p++)
+    if (h.radix[p] > 1) hd[nh++] = p;
+  if (nh > 32) return false;
+  std::vector<int64_t> rowstride(m + 1, 1);
+  for (int p = m - 1; p >= 0; p--) rowstride[p] = rowstride[p + 1] * h.radix[p];
+  for (int p = 0; p < m; p++) rowstride[p] = rowstride[p + 1];
+  const bool full = row_begin == 0 && row_end == h.rows;
+  if (full) {
+    std::vector<int64_t> cells(k, d);
+    int big = 0;
+    for (int j = 0; j < k; j++) {
+      for (int p = 0; p < m; p++)
+        if (h.stride[j][p]) cells[j] *= h.radix[p];
+      if (cells[j] > cells[big]) big = j;
+    }
+    std::stable_sort(hd, hd + nh, [&](int a, int b) { return (h.stride[big][a] != 0) > (h.stride[big][b] != 0); });
+  }
+  L.natural = !full;
+  S.nhigh = nh;
+  int64_t div = 1;
+  for (int e = nh - 1; e >= 0; e--) {
+    const int p = hd[e];
+    S.hrad[e] = h.radix[p];
+    S.hdiv[e] = div;
+    div *= h.radix[p];
+    for (int j = 0; j < k; j++) S.hstr[e][j] = h.stride[j][p];
+    S.hrow[e] = rowstride[p];
+  }
+  for (int j = 0; j < k; j++) S.shift[j] = h.shift[j];
+  // L2 prefetch extent of each input's tile slice: [base, base + maxoff + d)
+  // is the whole slice when the input's in-tile offsets are one dense block
+  // (canonical layouts); otherwise no prefetch.  GBE_STREAM_PF=1 enables it
+  // (A/B knob: C5 18.2 ms with, 17.5 ms without)
+  static const bool no_pf = std::getenv("GBE_STREAM_PF") == nullptr;  // off unless set (measured: k = 1 buckets lose)
+  for (int j = 0; j < k; j++) {
+    int64_t want = d, span = 1;
+    bool dense = true;
+    for (int q = nlow - 1; q >= 0; q--) {
+      const int p = m - nlow + q;
+      if (!h.stride[j][p]) continue;
+      if (h.stride[j][p] != want) dense = false;
+      want *= h.radix[p];
+      span *= h.radix[p];
+    }
+    const int64_t bytes = span * d * (h.semiring == GBE_MINSUM_I32 ? 4 : 8);
+    S.pf_bytes[j] = (dense && !no_pf && bytes >= 256 && bytes < (int64_t(1) << 30)) ? bytes : 0;
+  }
+  // vector loads: one 16-byte (f64 d = 2, 4, 8; int32 d = 4, 8, 16) or
+  // 8-byte (int32 d = 2) load per lane when every offset is a multiple of VEC
+  {
+    const int es = h.semiring == GBE_MINSUM_I32 ? 4 : 8;
+    int vec = 0;
+    if (es == 8 && (d == 2 || d == 4 || d == 8)) vec = 2;
+    if (es == 4 && (d == 4 || d == 8 || d == 16)) vec = 4;
+    if (es == 4 && d == 2) vec = 2;
+    for (int j = 0; j < k && vec; j++) {
+      if (h.shift[j] % vec) vec = 0;
+      for (int p = 0; p < m && vec; p++)
+        if (h.stride[j][p] % vec) vec = 0;
+    }
+    L.vec = vec;
+  }
+  L.k = k;
+  L.d = d;
+  L.f64 = h.semiring != GBE_MINSUM_I32;
+  L.sp = h.semiring == GBE_SUMPROD_F64;
+  L.t0 = row_begin / PL;
+  L.ntiles = (row_end - 1) / PL - L.t0 + 1;
+  L.smem = (int)(sizeof(int32_t) * (size_t)k * PL);
+  // CTAs: as many as fit, at least one warp-tile per warp
+  const int per_sm = std::max(1, std::min(8, (200 * 1024) / std::max(L.smem + 1024, 1)));
+  const int64_t want = (L.ntiles + (kBlock / 32) - 1) / (kBlock / 32);
+  L.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms * per_sm, want));
+  return true;
+}
+
+cudaError_t bks_launch(const StreamDesc *dev_s, const BksLaunch &L, const InPtrs &in, void *out, uint8_t *arg,
+                       int64_t row_begin, int64_t row_end, cudaStream_t s) {
+  if (L.sp) return dispatch<double, true>(dev_s, L, in, out, arg, row_begin, row_end, s);
+  if (L.f64) return dispatch<double, false>(dev_s, L, in, out, arg, row_begin, row_end, s);
+  return dispatch<int32_t, false>(dev_s, L, in, out, arg, row_begin, row_end, s);
+}
+
+}  // namespace gbe

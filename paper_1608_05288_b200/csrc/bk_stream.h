@@ -1,0 +1,40 @@
+// bk_stream.h — descriptor and launcher of the streaming bucket kernel.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace gbe {
+
+// Device descriptor (read through the read-only cache).
+struct StreamDesc {
+  int32_t k, d, nlow, PL, nhigh, pad;
+  int32_t lrad[GBE_MAX_SEP];       // low (in-tile) digits, most significant first
+  int32_t lstr[GBE_MAX_SEP][32];   // their element strides per input
+  int32_t hrad[32];                // high digits (radix > 1), most significant first
+  int64_t hdiv[32];                // tile-index divisor of each high digit
+  int64_t hstr[32][32];            // [digit][input] element stride
+  int64_t hrow[32];                // output-row stride of each high digit
+  int64_t pf_bytes[32];            // bytes of input j's tile slice to prefetch into L2 (0: none)
+  int64_t shift[32];
+};
+
+struct BksLaunch {
+  int d = 1, k = 1, grid = 1, smem = 0;
+  int vec = 0;  // elements per vector load when the layout allows it (0: scalar)
+  bool f64 = false, sp = false;
+  bool natural = true;  // tiles in row order (partial row ranges); else reordered for L2 reuse
+  int64_t t0 = 0, ntiles = 0;
+};
+
+// false when the descriptor does not fit (more than 32 high digits of radix > 1)
+bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int num_sms, StreamDesc &S,
+               BksLaunch &L);
+cudaError_t bks_launch(const StreamDesc *dev_s, const BksLaunch &L, const InPtrs &in, void *out, uint8_t *arg,
+                       int64_t row_begin, int64_t row_end, cudaStream_t s);
+// lanes that split one row's domain (1 for d <= 5, up to 32)
+int bks_lanes_per_row(int d);
+
+}  // namespace gbe

@@ -48,6 +48,8 @@ ExecOptions parse_exec(const char *json) {
   if (ex.host_arg_chunk < 1) GBE_FAIL(GBE_E_INVALID, "host_arg_chunk must be >= 1");
   ex.timing = j.b("timing", false);
   ex.kernel = (int)j.i("kernel", -1);
+  if (ex.kernel < -1 || ex.kernel > 2) GBE_FAIL(GBE_E_INVALID, "kernel must be -1 (auto), 0, 1 or 2");
+  ex.autotune = j.b("autotune", true);
   ex.resident_inputs = j.b("resident_inputs", false);
   ex.graph = j.b("graph", true);
   ex.concurrent = j.b("concurrent", true);
@@ -281,6 +283,15 @@ gbe_status gbe_bucket_kernel(const void *desc, const void *const *dev_inputs, vo
   return guard([&] {
     bucket_kernel((const gbe_bucket_desc *)desc, dev_inputs, dev_out, dev_arg, row_begin, row_end,
                   stream);
+  });
+}
+
+gbe_status gbe_bucket_kernel_ex(const void *desc, const void *const *dev_inputs, void *dev_out,
+                                uint8_t *dev_arg, int64_t row_begin, int64_t row_end, void *stream,
+                                int32_t variant) {
+  return guard([&] {
+    bucket_kernel((const gbe_bucket_desc *)desc, dev_inputs, dev_out, dev_arg, row_begin, row_end,
+                  stream, variant);
   });
 }
 

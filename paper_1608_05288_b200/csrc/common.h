@@ -110,7 +110,8 @@ struct ExecOptions {
   int64_t shard_min_rows = 1ll << 24;
   int retain = 1;              // 0 none, 1 args, 2 all
   bool timing = false;
-  int kernel = -1;             // -1 auto, else force a kernel variant
+  int kernel = -1;             // -1 auto, else force a kernel variant (0 generic, 1 tiled, 2 streaming)
+  bool autotune = true;        // auto: time tiled vs streaming per bucket on the first solves
   bool resident_inputs = false; // keep the uploaded originals on the device between solves
   bool graph = true;            // replay the UTIL phase as a CUDA graph (1 GPU, cached arena)
   bool concurrent = true;       // the graph is the task DAG: sibling subtrees overlap

@@ -18,6 +18,7 @@
 #include "common.h"
 #include "executor.h"
 #include "bk_fast.h"
+#include "bk_stream.h"
 #include "kernels.h"
 
 namespace gbe {
@@ -93,6 +94,18 @@ struct DevPlan {
   std::vector<FastDesc> h_fast;
   std::vector<BkfLaunch> fl;
   std::vector<char> use_fast;
+  std::vector<StreamDesc> h_stream;  // streaming kernel (bk_stream.cu) descriptors
+  std::vector<BksLaunch> sl;
+  std::vector<char> use_stream;
+  StreamDesc *d_stream = nullptr;
+  // autotuning (exec option "autotune", kernel auto): tasks both variants can
+  // run are timed with the tiled kernel on one solve and the streaming
+  // kernel on the next (eager, CUDA events around each launch); then each
+  // keeps the faster one and the graph is captured with the final choice
+  std::vector<char> cand;
+  std::vector<float> t_fast, t_stream;
+  int tune_phase = -1;  // -1: no tuning; 0..3: the next solve times tiled / streaming / tiled / streaming; 4: done
+  std::vector<cudaEvent_t> tune_ev;
   // pre-aggregation of small inputs (DESIGN.md §5 "input merging"): merge mi
   // sums some inputs of task merges[mi].task into one table, a d = 1 bucket
   struct Merge {
@@ -114,6 +127,8 @@ struct DevPlan {
   struct Chunk {
     int64_t lo = 0, hi = 0;
     int fidx = -1;        // index into h_cfast / cfl (tiled kernel), -1: generic
+    bool stream = false;  // streaming kernel over [lo, hi) (the task's StreamDesc)
+    BksLaunch sl{};
     BkLaunchInfo li{};
   };
   std::vector<std::vector<Chunk>> chunks;
@@ -185,8 +200,10 @@ struct DevPlan {
     if (h_harg) cudaFreeHost(h_harg);
     if (cp_stream) cudaStreamDestroy(cp_stream);
     for (auto e : k_ev) if (e) cudaEventDestroy(e);
+    for (auto e : tune_ev) cudaEventDestroy(e);
     for (auto e : c_ev) if (e) cudaEventDestroy(e);
     cudaFree(d_fast);
+    cudaFree(d_stream);
     cudaFree(d_off);
     cudaFree(d_poff);
     cudaFree(d_prad);
@@ -488,6 +505,25 @@ static void plan_merges(const Plan &P, DevPlan *D, size_t ti, gbe_bucket_desc &h
   h = h2;
 }
 
+// Tiled (register-blocked, TMA ring) vs streaming kernel for a bucket both
+// can run.  GBE_KERNEL_POLICY=tiled|stream forces one (A/B knob).
+static int kernel_policy() {
+  static const int pol = [] {
+    const char *e = std::getenv("GBE_KERNEL_POLICY");
+    if (!e) return -1;
+    return std::strcmp(e, "stream") == 0 ? 1 : (std::strcmp(e, "tiled") == 0 ? 0 : -1);
+  }();
+  return pol;
+}
+static bool prefer_stream(const gbe_bucket_desc &h, const BkfLaunch &fl) {
+  const int pol = kernel_policy();
+  if (pol >= 0) return pol == 1;
+  // without timings: float64 buckets stream (C5: 17.5 vs 21.1 ms), int32
+  // buckets take the register-blocked tiled kernel (C4: 28.3 vs 45.4 ms)
+  (void)fl;
+  return h.semiring != GBE_MINSUM_I32;
+}
+
 static DevPlan *dev_plan(gbe_plan *gp) {
   if (gp->dev) return (DevPlan *)gp->dev;
   const Plan &P = *gp->plan;
@@ -510,6 +546,12 @@ static DevPlan *dev_plan(gbe_plan *gp) {
   D->h_fast.resize(P.tasks.size());
   D->fl.resize(P.tasks.size());
   D->use_fast.assign(P.tasks.size(), 0);
+  D->h_stream.resize(P.tasks.size());
+  D->sl.resize(P.tasks.size());
+  D->use_stream.assign(P.tasks.size(), 0);
+  D->cand.assign(P.tasks.size(), 0);
+  D->t_fast.assign(P.tasks.size(), 0.f);
+  D->t_stream.assign(P.tasks.size(), 0.f);
   D->task_merges.assign(P.tasks.size(), {});
   D->in_map.assign(P.tasks.size(), {});
   for (size_t ti = 0; ti < P.tasks.size(); ti++) {
@@ -531,10 +573,20 @@ static DevPlan *dev_plan(gbe_plan *gp) {
     }
     D->h_desc[ti] = h;
     D->launch[ti] = bk_plan_launch(h, t.shard.lo, t.shard.hi, P.ex.kernel, D->num_sms);
-    if (P.ex.kernel != 0 && !P.ex.count &&
-        bkf_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_fast[ti], D->fl[ti], noinf)) {
+    // kernel variant: tiled TMA (1), streaming (2), generic (0)
+    const int want = P.ex.kernel;  // -1 auto
+    const bool fast_ok = (want == -1 || want == 1) && !P.ex.count &&
+                         bkf_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_fast[ti], D->fl[ti], noinf);
+    const bool stream_ok = (want == -1 || want == 2) && !P.ex.count &&
+                           bks_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_stream[ti], D->sl[ti]);
+    D->cand[ti] = want == -1 && P.ex.autotune && kernel_policy() < 0 && !P.ex.host_args && fast_ok && stream_ok;
+    if (D->cand[ti]) D->tune_phase = 0;
+    if (fast_ok && (!stream_ok || !prefer_stream(h, D->fl[ti]))) {
       D->use_fast[ti] = 1;
       D->launch[ti].variant = 1;
+    } else if (stream_ok) {
+      D->use_stream[ti] = 1;
+      D->launch[ti].variant = 2;
     }
   }
   if (P.ex.host_args) {  // row chunks per task, host argmin layout, ring, copy stream
@@ -556,10 +608,13 @@ static DevPlan *dev_plan(gbe_plan *gp) {
         c.hi = std::min<int64_t>(t.rows, lo + step);
         FastDesc F;
         BkfLaunch L;
+        StreamDesc Sd;
         if (D->use_fast[ti] && bkf_build(D->h_desc[ti], c.lo, c.hi, D->num_sms, F, L, noinf)) {
           c.fidx = (int)D->h_cfast.size();
           D->h_cfast.push_back(F);
           D->cfl.push_back(L);
+        } else if (D->use_stream[ti] && bks_build(D->h_desc[ti], c.lo, c.hi, D->num_sms, Sd, c.sl)) {
+          c.stream = true;
         } else {
           c.li = bk_plan_launch(D->h_desc[ti], c.lo, c.hi, BK_GENERIC, D->num_sms);
         }
@@ -579,6 +634,9 @@ static DevPlan *dev_plan(gbe_plan *gp) {
       CK(cudaEventCreateWithFlags(&D->c_ev[i], cudaEventDisableTiming));
     }
   }
+  CK(cudaMalloc(&D->d_stream, sizeof(StreamDesc) * std::max<size_t>(P.tasks.size(), 1)));
+  if (!P.tasks.empty())
+    CK(cudaMemcpy(D->d_stream, D->h_stream.data(), sizeof(StreamDesc) * P.tasks.size(), cudaMemcpyHostToDevice));
   CK(cudaMalloc(&D->d_fast, sizeof(FastDesc) * std::max<size_t>(P.tasks.size(), 1)));
   if (!P.tasks.empty())
     CK(cudaMemcpy(D->d_fast, D->h_fast.data(), sizeof(FastDesc) * P.tasks.size(), cudaMemcpyHostToDevice));
@@ -648,6 +706,8 @@ struct RunImpl {
   bool util_done = false;
   bool shared_scalars = false;  // d_opt / d_assign belong to the arena (graph path)
   bool args_written = false;    // the bucket kernels wrote argmin tables (byte accounting)
+  bool replayed = false;        // this UTIL phase was a CUDA-graph replay
+  bool tuned = false;           // this solve was an autotuning solve
   ~RunImpl() { release(); }
   void release() {
     if (!D) return;
@@ -810,7 +870,22 @@ static void run_util(RunImpl &R) {
   // W > 1: the UTIL phase is still one CUDA graph when the all-gather is the
   // built-in NCCL one (it only enqueues work on the stream; a Python hook
   // that stages through the host cannot be captured)
-  const bool graph = P.ex.graph && (W == 1 || g_ag_graph) && !g_alloc && !R.arena_own && !P.ex.host_args && !hook;
+  // autotuning solve: eager, candidates forced to one variant, timed
+  const bool tuning = D->tune_phase >= 0 && D->tune_phase < 4;
+  if (tuning) {
+    while (D->tune_ev.size() < 2 * nt) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      D->tune_ev.push_back(e);
+    }
+    for (size_t ti = 0; ti < nt; ti++)
+      if (D->cand[ti]) {
+        D->use_fast[ti] = (D->tune_phase & 1) == 0;
+        D->use_stream[ti] = (D->tune_phase & 1) == 1;
+      }
+  }
+  const bool graph = P.ex.graph && (W == 1 || g_ag_graph) && !g_alloc && !R.arena_own && !P.ex.host_args && !hook &&
+                     !tuning;
   uint8_t *hook_arg = nullptr;
   if (hook && !want_arg && !host_args && !P.ex.sumprod) {
     int64_t mx = 1;
@@ -942,6 +1017,8 @@ static void run_util(RunImpl &R) {
           void *oc = (char *)out + (size_t)(c.lo - sh.lo) * el;
           if (c.fidx >= 0)
             CK(bkf_launch(D->d_cfast + c.fidx, D->cfl[c.fidx], ins[ti], oc, ra, c.lo, st));
+          else if (c.stream)
+            CK(bks_launch(D->d_stream + ti, c.sl, ins[ti], oc, ra, c.lo, c.hi, st));
           else
             CK(bk_launch(D->h_desc[ti], D->d_desc + ti, ins[ti], oc, ra, c.lo, c.hi, c.li, st));
           CK(cudaEventRecord(D->k_ev[slot], st));
@@ -951,11 +1028,20 @@ static void run_util(RunImpl &R) {
           CK(cudaEventRecord(D->c_ev[slot], D->cp_stream));
           ring_n++;
         }
+      } else if (tuning && D->cand[ti]) {
+        CK(cudaEventRecord(D->tune_ev[2 * ti], st));
+        if (D->use_fast[ti])
+          CK(bkf_launch(D->d_fast + ti, D->fl[ti], ins[ti], out, argp, sh.lo, st));
+        else
+          CK(bks_launch(D->d_stream + ti, D->sl[ti], ins[ti], out, argp, sh.lo, sh.hi, st));
+        CK(cudaEventRecord(D->tune_ev[2 * ti + 1], st));
       } else if (P.ex.count)
         CK(bk_count_launch(D->h_desc[ti], D->d_desc + ti, ins[ti], cins[ti], out,
                            (double *)(R.base + R.A->off_cnt[ti]), argp, sh.lo, sh.hi, P.ex.count == 2, st));
       else if (D->use_fast[ti])
         CK(bkf_launch(D->d_fast + ti, D->fl[ti], ins[ti], out, argp, sh.lo, st));
+      else if (D->use_stream[ti])
+        CK(bks_launch(D->d_stream + ti, D->sl[ti], ins[ti], out, argp, sh.lo, sh.hi, st));
       else
         CK(bk_launch(D->h_desc[ti], D->d_desc + ti, ins[ti], out, argp, sh.lo, sh.hi, D->launch[ti], st));
       if (P.ex.timing) rec(ev[3 * ti + 2]);
@@ -1047,9 +1133,31 @@ static void run_util(RunImpl &R) {
     }
   }
   if (!replayed) enqueue(s, false);
+  R.replayed = replayed;
+  R.tuned = tuning;
   if (graph) A.runs++;
   CK(cudaStreamSynchronize(s));
   R.optimum = read_value(p, hopt);
+  if (tuning) {  // this solve's candidate times; after both phases keep the faster variant
+    for (size_t ti = 0; ti < nt; ti++)
+      if (D->cand[ti]) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, D->tune_ev[2 * ti], D->tune_ev[2 * ti + 1]));
+        // the first solve of each variant pays lazy module loading: keep the
+        // second (phases 2, 3)
+        if (D->tune_phase >= 2) ((D->tune_phase & 1) == 0 ? D->t_fast : D->t_stream)[ti] = ms;
+      }
+    if (++D->tune_phase == 4) {
+      for (auto &a : D->arena) a.runs = std::max(a.runs, 1);  // every kernel has run: capture next
+      for (size_t ti = 0; ti < nt; ti++)
+        if (D->cand[ti]) {
+          const bool st = D->t_stream[ti] < 0.97f * D->t_fast[ti];
+          D->use_stream[ti] = st;
+          D->use_fast[ti] = !st;
+          D->launch[ti].variant = st ? 2 : 1;
+        }
+    }
+  }
   if (P.ex.count) std::memcpy(&R.count, hopt + 8, sizeof(double));
   if (P.ex.timing) {
     R.ms.assign(nt, 0.f);
@@ -1208,7 +1316,9 @@ static std::string stats_json(const RunImpl &R) {
   // input merge, constants (+ the count product of counting plans)
   const size_t util_launches = 2 + P.tasks.size() + R.D->merges.size() + (P.ex.count ? 1 : 0);
   o << "{\"total_cells\":" << P.total_cells << ",\"total_bytes\":" << P.total_bytes
-    << ",\"merges\":" << R.D->merges.size() << ",\"util_launches\":" << util_launches << ",\"tasks\":[";
+    << ",\"merges\":" << R.D->merges.size() << ",\"util_launches\":" << util_launches
+    << ",\"graph_replay\":" << (R.replayed ? "true" : "false") << ",\"autotune_solve\":" << (R.tuned ? "true" : "false")
+    << ",\"tasks\":[";
   for (size_t ti = 0; ti < P.tasks.size(); ti++) {
     const Task &t = P.tasks[ti];
     int64_t local = t.shard.hi - t.shard.lo;
@@ -1342,17 +1452,27 @@ void solve(gbe_plan *gp, void *stream, bool mbe, gbe_value *opt, gbe_value *uppe
   delete R;
 }
 
+// the variant the bare primitive runs: the same rule as a plan's buckets
+// (tiled when it fits, unless the policy prefers streaming; else streaming;
+// the generic kernel only for descriptors neither takes)
 int bucket_kernel_variant(const gbe_bucket_desc *h, int64_t row_begin, int64_t row_end) {
+  if (row_end <= row_begin) return 0;
   FastDesc *F = new FastDesc();
   BkfLaunch fl;
-  bool ok = bkf_build(*h, row_begin, row_end, 148, *F, fl);
+  const bool fast = bkf_build(*h, row_begin, row_end, 148, *F, fl);
   delete F;
-  return ok ? 1 : 0;
+  StreamDesc *Sd = new StreamDesc();
+  BksLaunch sl;
+  const bool stream = bks_build(*h, row_begin, row_end, 148, *Sd, sl);
+  delete Sd;
+  if (fast && (!stream || !prefer_stream(*h, fl))) return 1;
+  return stream ? 2 : 0;
 }
 
 // the bare hot primitive
 void bucket_kernel(const gbe_bucket_desc *h, const void *const *dev_inputs, void *dev_out,
-                   uint8_t *dev_arg, int64_t row_begin, int64_t row_end, void *stream) {
+                   uint8_t *dev_arg, int64_t row_begin, int64_t row_end, void *stream, int variant) {
+  if (variant < -1 || variant > 2) GBE_FAIL(GBE_E_INVALID, "variant must be -1, 0, 1 or 2");
   if (!h) GBE_FAIL(GBE_E_INVALID, "null descriptor");
   if (h->semiring != GBE_MINSUM_I32 && h->semiring != GBE_MINSUM_F64 && h->semiring != GBE_SUMPROD_F64)
     GBE_FAIL(GBE_E_INVALID, "bad semiring");
@@ -1372,25 +1492,49 @@ void bucket_kernel(const gbe_bucket_desc *h, const void *const *dev_inputs, void
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   cudaStream_t s = (cudaStream_t)stream;
-  gbe_bucket_desc *d_desc = (gbe_bucket_desc *)dalloc(sizeof(gbe_bucket_desc), s);
-  CK(cudaMemcpyAsync(d_desc, h, sizeof(gbe_bucket_desc), cudaMemcpyHostToDevice, s));
   InPtrs in{};
   for (int j = 0; j < h->ninputs; j++) in.p[j] = dev_inputs[j];
-  FastDesc *F = new FastDesc();
-  BkfLaunch fl;
-  if (bkf_build(*h, row_begin, row_end, nsm, *F, fl)) {
-    FastDesc *d_f = (FastDesc *)dalloc(sizeof(FastDesc), s);
-    cudaError_t e = cudaMemcpyAsync(d_f, F, sizeof(FastDesc), cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = bkf_launch(d_f, fl, in, dev_out, dev_arg, row_begin, s);
-    dfree(d_f, s);
+  const int var = variant >= 0 ? variant : bucket_kernel_variant(h, row_begin, row_end);
+  if (var == 2) {  // streaming
+    StreamDesc *Sd = new StreamDesc();
+    BksLaunch sl;
+    const bool ok = bks_build(*h, row_begin, row_end, nsm, *Sd, sl);
+    if (ok) {
+      StreamDesc *d_s = (StreamDesc *)dalloc(sizeof(StreamDesc), s);
+      cudaError_t e = cudaMemcpyAsync(d_s, Sd, sizeof(StreamDesc), cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess) e = bks_launch(d_s, sl, in, dev_out, dev_arg, row_begin, row_end, s);
+      dfree(d_s, s);
+      delete Sd;
+      CK(e);
+      return;
+    }
+    delete Sd;
+    if (variant == 2) GBE_FAIL(GBE_E_INVALID, "the streaming kernel does not fit this descriptor");
+  }
+  if (var == 1) {  // tiled TMA
+    FastDesc *F = new FastDesc();
+    BkfLaunch fl;
+    const bool ok = bkf_build(*h, row_begin, row_end, nsm, *F, fl);
+    if (ok) {
+      FastDesc *d_f = (FastDesc *)dalloc(sizeof(FastDesc), s);
+      cudaError_t e = cudaMemcpyAsync(d_f, F, sizeof(FastDesc), cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess) e = bkf_launch(d_f, fl, in, dev_out, dev_arg, row_begin, s);
+      dfree(d_f, s);
+      delete F;
+      CK(e);
+      return;
+    }
     delete F;
-    CK(e);
-  } else {
-    delete F;
+    if (variant == 1) GBE_FAIL(GBE_E_INVALID, "the tiled kernel does not fit this descriptor");
+  }
+  gbe_bucket_desc *d_desc = (gbe_bucket_desc *)dalloc(sizeof(gbe_bucket_desc), s);
+  cudaError_t e = cudaMemcpyAsync(d_desc, h, sizeof(gbe_bucket_desc), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) {
     BkLaunchInfo li = bk_plan_launch(*h, row_begin, row_end, -1, nsm);
-    CK(bk_launch(*h, d_desc, in, dev_out, dev_arg, row_begin, row_end, li, s));
+    e = bk_launch(*h, d_desc, in, dev_out, dev_arg, row_begin, row_end, li, s);
   }
   dfree(d_desc, s);
+  CK(e);
 }
 
 }  // namespace gbe

@@ -31,7 +31,7 @@ void solve(gbe_plan *gp, void *stream, bool mbe, gbe_value *opt, gbe_value *uppe
            int32_t *assign_out, char *stats, size_t cap);
 int bucket_kernel_variant(const gbe_bucket_desc *h, int64_t row_begin, int64_t row_end);
 void bucket_kernel(const gbe_bucket_desc *h, const void *const *dev_inputs, void *dev_out,
-                   uint8_t *dev_arg, int64_t row_begin, int64_t row_end, void *stream);
+                   uint8_t *dev_arg, int64_t row_begin, int64_t row_end, void *stream, int variant = -1);
 
 }  // namespace gbe
 

@@ -32,7 +32,7 @@ EXPORTED = [
     "gbe_bucket_kernel", "gbe_set_allocator", "gbe_set_allgather", "gbe_last_error",
     "gbe_version", "gbe_bucket_kernel_variant", "gbe_comm_nccl_id", "gbe_comm_nccl_init",
     "gbe_comm_finalize", "gbe_solve_count", "gbe_run_count", "gbe_run_count_table",
-    "gbe_set_table_hook",
+    "gbe_set_table_hook", "gbe_bucket_kernel_ex",
 ]
 
 
@@ -103,6 +103,7 @@ def lib():
         L.gbe_run_destroy.argtypes = [vp]
         L.gbe_run_destroy.restype = None
         L.gbe_bucket_kernel.argtypes = [vp, vp, vp, vp, i64, i64, vp]
+        L.gbe_bucket_kernel_ex.argtypes = [vp, vp, vp, vp, i64, i64, vp, i32]
         L.gbe_bucket_kernel_variant.argtypes = [vp, i64, i64]
         L.gbe_bucket_kernel_variant.restype = i32
         L.gbe_set_allocator.argtypes = [ALLOC_FN, FREE_FN, vp]
@@ -337,15 +338,20 @@ class Run:
         return out[:rows]
 
 
-def bucket_kernel(desc: BucketDesc, inputs, out, arg, row_begin, row_end, stream=None):
-    """The hot primitive on device pointers (ints) or torch tensors."""
+def bucket_kernel(desc: BucketDesc, inputs, out, arg, row_begin, row_end, stream=None, variant=-1):
+    """The hot primitive on device pointers (ints) or torch tensors; variant
+    -1 auto, 0 generic, 1 tiled TMA, 2 streaming (gbe_bucket_kernel_ex)."""
     def p(x):
         if x is None:
             return None
         return ctypes.c_void_p(x if isinstance(x, int) else x.data_ptr())
     arr = (ctypes.c_void_p * max(len(inputs), 1))(*[p(x) for x in inputs])
-    _check(lib().gbe_bucket_kernel(ctypes.byref(desc), arr, p(out), p(arg), int(row_begin),
-                                   int(row_end), _stream_ptr(stream)))
+    if variant < 0:
+        _check(lib().gbe_bucket_kernel(ctypes.byref(desc), arr, p(out), p(arg), int(row_begin),
+                                       int(row_end), _stream_ptr(stream)))
+    else:
+        _check(lib().gbe_bucket_kernel_ex(ctypes.byref(desc), arr, p(out), p(arg), int(row_begin),
+                                          int(row_end), _stream_ptr(stream), int(variant)))
 
 
 def bucket_kernel_variant(desc: BucketDesc, row_begin, row_end):

@@ -28,7 +28,8 @@ for _ in range(a.steps):
         assign = run.value()
     st = run.stats()
     run.close()
-fast = [t for t in st["tasks"] if t["variant"] == 1]
+want = int(os.environ.get("PROF_VARIANT", "1"))  # 1 tiled (bk_fast), 2 streaming (bk_stream)
+fast = [t for t in st["tasks"] if t["variant"] == want]
 big = max(range(len(fast)), key=lambda i: fast[i]["cells"]) if a.var < 0 else [i for i, t in enumerate(fast) if t["var"] == a.var][0]
 if a.which_fast:
     print(big)

@@ -77,14 +77,14 @@ def desc_for(dom, sep, x, members, f64):
     return D, rows
 
 
-def run_bucket(torch, dom, sep, x, members, f64, rb, re):
+def run_bucket(torch, dom, sep, x, members, f64, rb, re, variant=-1):
     D, rows = desc_for(dom, sep, x, members, f64)
     dt = torch.float64 if f64 else torch.int32
     ins = [torch.tensor(np.asarray(t), dtype=dt, device="cuda") for _, t in members]
     n = max(re - rb, 1)
     out = torch.empty(n, dtype=dt, device="cuda")
     arg = torch.empty(n, dtype=torch.uint8, device="cuda")
-    G.bucket_kernel(D, ins, out, arg, rb, re)
+    G.bucket_kernel(D, ins, out, arg, rb, re, variant=variant)
     torch.cuda.synchronize()
     return out.cpu().numpy()[:re - rb], arg.cpu().numpy()[:re - rb]
 
@@ -310,26 +310,26 @@ def test_fast_kernel_shapes(torch_cuda, R, DV, f64):
         k = int(rng.integers(1, 12))
         dom, sep, x, members = uniform_bucket(rng, R, DV, m, k, f64)
         D, rows = desc_for(dom, sep, x, members, f64)
-        if f64 and R == 5 and DV == 5:  # no f64 shape fits the register budget
-            assert G.bucket_kernel_variant(D, 0, rows) == 0
-            continue
-        assert G.bucket_kernel_variant(D, 0, rows) == 1
+        # auto: tiled for int32, streaming for f64; both variants run explicitly
+        assert G.bucket_kernel_variant(D, 0, rows) == (2 if f64 else 1)
+        variants = [2] if (f64 and R == 5 and DV == 5) else [1, 2]  # no f64 tiled 5x5x5 shape
         exp, exp_arg = oracle.bucket_eval(dom, f64, x, members, sep)
-        got, got_arg = run_bucket(torch_cuda, dom, sep, x, members, f64, 0, rows)
-        if f64:
-            np.testing.assert_array_equal(np.isinf(got), np.isinf(exp))
-            fin = np.isfinite(exp)
-            assert np.allclose(got[fin], exp[fin], rtol=1e-9, atol=0)
-            # argmins may differ only on near-ties (different summation
-            # order): the oracle's own sums of both choices within 1e-9 (A10)
-            bad = np.nonzero(got_arg != exp_arg)[0]
-            if bad.size:
-                sums = oracle.bucket_row_sums(dom, True, x, members, sep, bad)
-                assert devtools.near_tie_ok(sums, got_arg[bad].astype(np.int64),
-                                            exp_arg[bad].astype(np.int64)).all()
-        else:
-            np.testing.assert_array_equal(got, exp)
-            np.testing.assert_array_equal(got_arg, exp_arg)
+        for var in variants:
+            got, got_arg = run_bucket(torch_cuda, dom, sep, x, members, f64, 0, rows, variant=var)
+            if f64:
+                np.testing.assert_array_equal(np.isinf(got), np.isinf(exp))
+                fin = np.isfinite(exp)
+                assert np.allclose(got[fin], exp[fin], rtol=1e-9, atol=0)
+                # argmins may differ only on near-ties (different summation
+                # order): the oracle's own sums of both choices within 1e-9 (A10)
+                bad = np.nonzero(got_arg != exp_arg)[0]
+                if bad.size:
+                    sums = oracle.bucket_row_sums(dom, True, x, members, sep, bad)
+                    assert devtools.near_tie_ok(sums, got_arg[bad].astype(np.int64),
+                                                exp_arg[bad].astype(np.int64)).all()
+            else:
+                np.testing.assert_array_equal(got, exp)
+                np.testing.assert_array_equal(got_arg, exp_arg)
 
 
 def test_fast_kernel_partial_ranges(torch_cuda):

@@ -41,14 +41,14 @@ def close(got, exp, tol=1e-9):
     assert err.size == 0 or err.max() <= tol, f"max scaled error {err.max():.3g}"
 
 
-def run_sp(torch, dom, sep, x, members, rb, re):
+def run_sp(torch, dom, sep, x, members, rb, re, variant=-1):
     D, rows = desc_for(dom, sep, x, members, True)
     D.semiring = G.SUMPROD_F64
     ins = [torch.tensor(np.asarray(t), dtype=torch.float64, device="cuda") for _, t in members]
     n = max(re - rb, 1)
     out = torch.empty(n, dtype=torch.float64, device="cuda")
     arg = torch.full((n,), 77, dtype=torch.uint8, device="cuda")
-    G.bucket_kernel(D, ins, out, arg, rb, re)
+    G.bucket_kernel(D, ins, out, arg, rb, re, variant=variant)
     torch.cuda.synchronize()
     return D, out.cpu().numpy()[:re - rb], arg.cpu().numpy()[:re - rb]
 
@@ -78,12 +78,12 @@ def test_sumprod_fast_kernel_shapes(torch_cuda, R, DV):
         dom, sep, x, members = uniform_bucket(rng, R, DV, m, k, True)
         D, rows = desc_for(dom, sep, x, members, True)
         D.semiring = G.SUMPROD_F64
-        variant = G.bucket_kernel_variant(D, 0, rows)
-        assert variant in (0, 1)
+        assert G.bucket_kernel_variant(D, 0, rows) == 2  # auto: f64 streams
         exp = oracle.bucket_eval_sp(dom, x, members, sep)
-        _, got, arg = run_sp(torch_cuda, dom, sep, x, members, 0, rows)
-        close(got, exp)
-        assert not arg.any()
+        for var in (1, 2):  # the tiled and the streaming kernel, explicitly
+            _, got, arg = run_sp(torch_cuda, dom, sep, x, members, 0, rows, variant=var)
+            close(got, exp)
+            assert not arg.any()
 
 
 def test_sumprod_edge_cases(torch_cuda):
