@@ -74,12 +74,14 @@ def test_ring_wraps_bucket_kernel(kind, R, DV, m):
     dom, sep, x, members = ring_bucket(rng, R, DV, m, 8, "int" if kind == "int" else "f64")
     sr = {"int": G.MINSUM_I32, "f64": G.MINSUM_F64, "sp": G.SUMPROD_F64}[kind]
     D, rows = desc_for(dom, sep, x, members, sr)
-    assert G.bucket_kernel_variant(D, 0, rows) == 1
+    # the auto policy may pick the streaming kernel for f64; the ring is the
+    # tiled kernel's, so it is forced (variant 1) here
+    assert G.bucket_kernel_variant(D, 0, rows) in (1, 2)
     dt = torch.int32 if kind == "int" else torch.float64
     ins = [torch.tensor(np.asarray(t), dtype=dt, device="cuda") for _, t in members]
     out = torch.empty(rows, dtype=dt, device="cuda")
     arg = torch.empty(rows, dtype=torch.uint8, device="cuda")
-    G.bucket_kernel(D, ins, out, arg, 0, rows)
+    G.bucket_kernel(D, ins, out, arg, 0, rows, variant=1)
     torch.cuda.synchronize()
     got, got_arg = out.cpu().numpy(), arg.cpu().numpy()
     if kind == "sp":
