@@ -46,6 +46,9 @@ ExecOptions parse_exec(const char *json) {
   else GBE_FAIL(GBE_E_INVALID, "retain must be none|args|all|host");
   ex.host_arg_chunk = j.i("host_arg_chunk", ex.host_arg_chunk);
   if (ex.host_arg_chunk < 1) GBE_FAIL(GBE_E_INVALID, "host_arg_chunk must be >= 1");
+  ex.spill = j.b("spill", false);
+  ex.stage_bytes = j.i("stage_bytes", 0);
+  if (ex.stage_bytes < 0) GBE_FAIL(GBE_E_INVALID, "stage_bytes must be >= 0");
   ex.timing = j.b("timing", false);
   ex.kernel = (int)j.i("kernel", -1);
   if (ex.kernel < -1 || ex.kernel > 2) GBE_FAIL(GBE_E_INVALID, "kernel must be -1 (auto), 0, 1 or 2");

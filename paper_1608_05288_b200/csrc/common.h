@@ -101,6 +101,13 @@ struct Task {                  // one (mini-)bucket: Alg. 1 line 3 / Alg. 2 line
   gbe_bucket_desc desc{};      // radices + per-input stride maps (shift = 0)
   int64_t in_cells = 0;        // sum of input table sizes
   Shard shard;
+  // out-of-core plans ("spill"): the message lives in
+  // pinned host memory; the task runs in row chunks of `chunk_rows` rows
+  // (whole blocks of its leading output digits), each chunk's host-resident
+  // input slices staged into a device slot (Fig. 8)
+  bool host = false;
+  int32_t chunk_digits = 0;    // chunk = chunk_blocks consecutive blocks of these leading digits
+  int64_t chunk_blocks = 1, chunk_rows = 0;
 };
 
 struct ExecOptions {
@@ -119,6 +126,8 @@ struct ExecOptions {
   int count = 0;                // (min, count) semiring: 0 off, 1 optimal, 2 consistent solutions
   bool host_args = false;       // argmin tables in pinned host memory, streamed out chunk by chunk
   int64_t host_arg_chunk = int64_t(1) << 28;  // rows per streamed chunk (device ring buffer bytes)
+  bool spill = false;           // out-of-core: messages beyond budget_bytes live in host memory
+  int64_t stage_bytes = 0;      // spill: device staging (two slots); 0 = budget / 4, clamped
 };
 
 struct Plan {
@@ -135,6 +144,8 @@ struct Plan {
   int64_t total_cells = 0;                     // sum over tasks of rows*d
   int64_t total_bytes = 0;                     // algorithmic bytes
   int64_t peak_bytes = 0;                      // estimated device peak
+  int64_t host_bytes = 0;                      // spill: pinned host bytes of the host messages
+  int64_t slot_bytes = 0;                      // spill: bytes of each of the two device staging slots
   ExecOptions ex;
 };
 
@@ -146,6 +157,13 @@ int32_t induced_width(const Problem &p, const std::vector<int32_t> &order);
 std::unique_ptr<Plan> make_plan(std::shared_ptr<const Problem> p, const int32_t *order,
                                 int32_t ibound, const ExecOptions &ex);
 std::string plan_json(const Plan &plan);
+// out-of-core plans: device staging bytes of task ti's chunk over blocks
+// [b0, b1) of its c leading output digits, and input j's element range there
+struct SpillChunk {
+  int64_t lo = 0, n = 0;
+};
+int64_t spill_chunk_bytes(const Plan &P, size_t ti, int c, int64_t b0, int64_t b1);
+SpillChunk spill_chunk_input(const Plan &P, size_t ti, int c, int64_t b0, int64_t b1, int j);
 
 // problem.cpp
 std::shared_ptr<Problem> problem_create(int32_t n, const int32_t *dom, int32_t nf,

@@ -130,7 +130,24 @@ struct DevPlan {
     bool stream = false;  // streaming kernel over [lo, hi) (the task's StreamDesc)
     BksLaunch sl{};
     BkLaunchInfo li{};
+    // out-of-core plans ("spill"): staging-slot layout of this chunk
+    size_t out_off = 0, arg_off = 0;
+    struct HostIn {
+      int j;            // task input (after merging)
+      int32_t src;      // producing task (a host message)
+      int64_t lo, n;    // element range of that message the chunk reads
+      size_t off;       // byte offset in the slot (16-byte phase of lo * el added at use)
+    };
+    std::vector<HostIn> hin;
   };
+  // "spill" (out-of-core, §8(f) row 2): host messages in pinned host memory,
+  // two device staging slots, an H2D stream beside the D2H copy stream
+  char *h_msg = nullptr;
+  std::vector<size_t> msg_off;
+  char *d_slot = nullptr;
+  cudaStream_t h2d_stream = nullptr;
+  cudaEvent_t h_ev[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> done_ev;  // per host-message task: its last chunk copied out
   std::vector<std::vector<Chunk>> chunks;
   std::vector<FastDesc> h_cfast;
   std::vector<BkfLaunch> cfl;
@@ -198,6 +215,11 @@ struct DevPlan {
     cudaFree(d_cfast);
     cudaFree(d_ring);
     if (h_harg) cudaFreeHost(h_harg);
+    if (h_msg) cudaFreeHost(h_msg);
+    cudaFree(d_slot);
+    if (h2d_stream) cudaStreamDestroy(h2d_stream);
+    for (auto e : h_ev) if (e) cudaEventDestroy(e);
+    for (auto e : done_ev) if (e) cudaEventDestroy(e);
     if (cp_stream) cudaStreamDestroy(cp_stream);
     for (auto e : k_ev) if (e) cudaEventDestroy(e);
     for (auto e : tune_ev) cudaEventDestroy(e);
@@ -285,9 +307,11 @@ static void plan_arena(const Plan &P, DevPlan *D, bool mbe_mode) {
       A.off_merge[mi] = fl.alloc(D->merges[mi].bytes);
       put(ti, A.off_merge[mi], D->merges[mi].bytes);
     }
-    out_b[ti] = el * (size_t)cap;
-    A.off_out[ti] = fl.alloc(out_b[ti]);
-    put(ti, A.off_out[ti], out_b[ti]);
+    if (!t.host) {  // (a host message of an out-of-core plan has no device range)
+      out_b[ti] = el * (size_t)cap;
+      A.off_out[ti] = fl.alloc(out_b[ti]);
+      put(ti, A.off_out[ti], out_b[ti]);
+    }
     if (P.ex.count) {  // (min, count) semiring: a float64 count per row
       cnt_b[ti] = 8 * (size_t)cap;
       A.off_cnt[ti] = fl.alloc(cnt_b[ti]);
@@ -414,6 +438,7 @@ static void plan_merges(const Plan &P, DevPlan *D, size_t ti, gbe_bucket_desc &h
   std::vector<int> cand[4];
   for (int j = 0; j < k; j++) {
     if (h.shift[j] != 0) continue;
+    if (t.members[j].kind == 1 && P.tasks[t.members[j].index].host) continue;  // staged per chunk
     if (union_cells({j}) > small) continue;
     const int cls = (has(j, L.g1) ? 1 : 0) + (L.g2 >= 0 && has(j, L.g2) ? 2 : 0);
     cand[cls].push_back(j);
@@ -524,6 +549,90 @@ static bool prefer_stream(const gbe_bucket_desc &h, const BkfLaunch &fl) {
   return h.semiring != GBE_MINSUM_I32;
 }
 
+// Out-of-core chunks (planner.cpp plan_spill): every task runs in chunks of
+// t.chunk_rows rows; a chunk's slot holds its output rows when the message
+// lives on the host, its argmins (streamed to host memory), and the slices of
+// its host-resident inputs (copied in on the H2D stream while the previous
+// chunk computes: Fig. 8).
+static void plan_spill_chunks(const Plan &P, DevPlan *D, bool noinf) {
+  const size_t el = P.prob->elem();
+  const size_t nt = P.tasks.size();
+  D->chunks.assign(nt, {});
+  D->harg_off.assign(nt, 0);
+  D->msg_off.assign(nt, SIZE_MAX);
+  size_t aoff = 0, moff = 0;
+  auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+  for (size_t ti = 0; ti < nt; ti++) {
+    const Task &t = P.tasks[ti];
+    D->harg_off[ti] = aoff;
+    aoff += (size_t)std::max<int64_t>(t.rows, 1);
+    if (t.host) {
+      D->msg_off[ti] = moff;
+      moff += up(el * (size_t)t.rows);
+    }
+    int64_t blocks = 1;
+    for (int q = 0; q < t.chunk_digits; q++) blocks *= t.desc.radix[q];
+    const int64_t brows = t.rows / blocks;
+    for (int64_t b0 = 0; b0 < blocks; b0 += t.chunk_blocks) {
+      const int64_t b1 = std::min(blocks, b0 + t.chunk_blocks);
+      DevPlan::Chunk c;
+      c.lo = b0 * brows;
+      c.hi = b1 * brows;
+      size_t off = 0;
+      if (t.host) {
+        c.out_off = off;
+        off += up(el * (size_t)(c.hi - c.lo));
+      }
+      c.arg_off = off;
+      off += up((size_t)(c.hi - c.lo));
+      const std::vector<int32_t> &map = D->in_map[ti];
+      for (size_t j = 0; j < map.size(); j++) {
+        if (map[j] < 0) continue;  // a merged table (device)
+        const Member &m = t.members[map[j]];
+        if (m.kind != 1 || !P.tasks[m.index].host) continue;
+        const SpillChunk r = spill_chunk_input(P, ti, t.chunk_digits, b0, b1, map[j]);
+        c.hin.push_back({(int)j, m.index, r.lo, r.n, off});
+        off += up(el * (size_t)r.n + 64);
+      }
+      if ((int64_t)off > P.slot_bytes)
+        GBE_FAIL(GBE_E_INTERNAL, "spill chunk of x%d needs %zu bytes > slot %lld", t.var, off,
+                 (long long)P.slot_bytes);
+      FastDesc F;
+      BkfLaunch L;
+      StreamDesc Sd;
+      if (D->use_fast[ti] && bkf_build(D->h_desc[ti], c.lo, c.hi, D->num_sms, F, L, noinf)) {
+        c.fidx = (int)D->h_cfast.size();
+        D->h_cfast.push_back(F);
+        D->cfl.push_back(L);
+      } else if (D->use_stream[ti] && bks_build(D->h_desc[ti], c.lo, c.hi, D->num_sms, Sd, c.sl)) {
+        c.stream = true;
+      } else {
+        c.li = bk_plan_launch(D->h_desc[ti], c.lo, c.hi, BK_GENERIC, D->num_sms);
+      }
+      D->chunks[ti].push_back(std::move(c));
+    }
+  }
+  if (P.ex.host_args) {
+    CK(cudaHostAlloc((void **)&D->h_harg, std::max<size_t>(aoff, 1), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer((void **)&D->d_harg, D->h_harg, 0));
+  }
+  if (moff) CK(cudaHostAlloc((void **)&D->h_msg, moff, cudaHostAllocDefault));
+  CK(cudaMalloc(&D->d_slot, 2 * (size_t)P.slot_bytes));
+  CK(cudaMalloc(&D->d_cfast, sizeof(FastDesc) * std::max<size_t>(D->h_cfast.size(), 1)));
+  if (!D->h_cfast.empty())
+    CK(cudaMemcpy(D->d_cfast, D->h_cfast.data(), sizeof(FastDesc) * D->h_cfast.size(), cudaMemcpyHostToDevice));
+  CK(cudaStreamCreateWithFlags(&D->cp_stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&D->h2d_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; i++) {
+    CK(cudaEventCreateWithFlags(&D->k_ev[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&D->c_ev[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&D->h_ev[i], cudaEventDisableTiming));
+  }
+  D->done_ev.assign(nt, nullptr);
+  for (size_t ti = 0; ti < nt; ti++)
+    if (P.tasks[ti].host) CK(cudaEventCreateWithFlags(&D->done_ev[ti], cudaEventDisableTiming));
+}
+
 static DevPlan *dev_plan(gbe_plan *gp) {
   if (gp->dev) return (DevPlan *)gp->dev;
   const Plan &P = *gp->plan;
@@ -589,7 +698,9 @@ static DevPlan *dev_plan(gbe_plan *gp) {
       D->launch[ti].variant = 2;
     }
   }
-  if (P.ex.host_args) {  // row chunks per task, host argmin layout, ring, copy stream
+  if (P.ex.spill) {
+    plan_spill_chunks(P, D, noinf);
+  } else if (P.ex.host_args) {  // row chunks per task, host argmin layout, ring, copy stream
     D->chunks.assign(P.tasks.size(), {});
     D->harg_off.assign(P.tasks.size(), 0);
     size_t off = 0;
@@ -830,7 +941,7 @@ static void run_util(RunImpl &R) {
   std::vector<void *> gathered_src(nt, nullptr);
   for (size_t ti = 0; ti < nt; ti++) {
     const Task &t = P.tasks[ti];
-    R.out[ti] = R.base + R.A->off_out[ti];
+    R.out[ti] = t.host ? (void *)(D->h_msg + D->msg_off[ti]) : (void *)(R.base + R.A->off_out[ti]);
     if (host_args) R.arg[ti] = D->d_harg + D->harg_off[ti];
     else if (want_arg) R.arg[ti] = (uint8_t *)(R.base + R.A->off_arg[ti]);
     const std::vector<int32_t> &map = D->in_map[ti];
@@ -884,8 +995,8 @@ static void run_util(RunImpl &R) {
         D->use_stream[ti] = (D->tune_phase & 1) == 1;
       }
   }
-  const bool graph = P.ex.graph && (W == 1 || g_ag_graph) && !g_alloc && !R.arena_own && !P.ex.host_args && !hook &&
-                     !tuning;
+  const bool graph = P.ex.graph && (W == 1 || g_ag_graph) && !g_alloc && !R.arena_own && !P.ex.host_args &&
+                     !P.ex.spill && !hook && !tuning;
   uint8_t *hook_arg = nullptr;
   if (hook && !want_arg && !host_args && !P.ex.sumprod) {
     int64_t mx = 1;
@@ -994,7 +1105,9 @@ static void run_util(RunImpl &R) {
         last_on[b] = (int)ti;
         branch_of[ti] = b;
       }
-      void *out = gathered_src[ti] ? gathered_src[ti] : R.base + R.A->off_out[ti];
+      void *out = gathered_src[ti] ? gathered_src[ti]
+                  : t.host            ? (void *)(D->h_msg + D->msg_off[ti])
+                                      : (void *)(R.base + R.A->off_out[ti]);
       uint8_t *argp = want_arg && !host_args ? (uint8_t *)(R.base + R.A->off_arg[ti]) : hook_arg;
       if (P.ex.timing) rec(ev[3 * ti]);
       for (int32_t mi : D->task_merges[ti]) {
@@ -1009,7 +1122,52 @@ static void run_util(RunImpl &R) {
         }
       }
       if (P.ex.timing) rec(ev[3 * ti + 1]);  // merges done
-      if (host_args) {  // row chunks; argmins through the device ring to host memory
+      if (P.ex.spill) {  // out-of-core: chunks through the two staging slots
+        bool waited = false;
+        for (const DevPlan::Chunk &c : D->chunks[ti]) {
+          const int slot = ring_n & 1;
+          char *sb = D->d_slot + (size_t)slot * P.slot_bytes;
+          InPtrs in = ins[ti];
+          if (!c.hin.empty()) {  // H2D of the host-resident input slices
+            if (!waited) {
+              for (const auto &hi : c.hin) CK(cudaStreamWaitEvent(D->h2d_stream, D->done_ev[hi.src], 0));
+              waited = true;
+            }
+            if (ring_n >= 2) CK(cudaStreamWaitEvent(D->h2d_stream, D->k_ev[slot], 0));  // slot inputs read
+            for (const auto &hi : c.hin) {
+              // the slice keeps the 16-byte phase it has in the full table, so
+              // the kernel's aligned (TMA / vector) reads see the same layout
+              const size_t ph = (size_t)(hi.lo * (int64_t)el) & 15;
+              char *dst = sb + hi.off + ph;
+              CK(cudaMemcpyAsync(dst, D->h_msg + D->msg_off[hi.src] + (size_t)hi.lo * el, (size_t)hi.n * el,
+                                 cudaMemcpyHostToDevice, D->h2d_stream));
+              in.p[hi.j] = (const void *)((uintptr_t)dst - (uintptr_t)hi.lo * el);
+            }
+            CK(cudaEventRecord(D->h_ev[slot], D->h2d_stream));
+            CK(cudaStreamWaitEvent(st, D->h_ev[slot], 0));
+          }
+          if (ring_n >= 2) CK(cudaStreamWaitEvent(st, D->c_ev[slot], 0));  // slot outputs copied out
+          void *oc = t.host ? (void *)(sb + c.out_off) : (void *)((char *)out + (size_t)c.lo * el);
+          uint8_t *ra = host_args ? (uint8_t *)(sb + c.arg_off) : nullptr;
+          if (c.fidx >= 0)
+            CK(bkf_launch(D->d_cfast + c.fidx, D->cfl[c.fidx], in, oc, ra, c.lo, st));
+          else if (c.stream)
+            CK(bks_launch(D->d_stream + ti, c.sl, in, oc, ra, c.lo, c.hi, st));
+          else
+            CK(bk_launch(D->h_desc[ti], D->d_desc + ti, in, oc, ra, c.lo, c.hi, c.li, st));
+          CK(cudaEventRecord(D->k_ev[slot], st));
+          CK(cudaStreamWaitEvent(D->cp_stream, D->k_ev[slot], 0));
+          if (t.host)
+            CK(cudaMemcpyAsync(D->h_msg + D->msg_off[ti] + (size_t)c.lo * el, oc, (size_t)(c.hi - c.lo) * el,
+                               cudaMemcpyDeviceToHost, D->cp_stream));
+          if (ra)
+            CK(cudaMemcpyAsync(D->h_harg + D->harg_off[ti] + c.lo, ra, (size_t)(c.hi - c.lo),
+                               cudaMemcpyDeviceToHost, D->cp_stream));
+          CK(cudaEventRecord(D->c_ev[slot], D->cp_stream));
+          ring_n++;
+        }
+        if (t.host) CK(cudaEventRecord(D->done_ev[ti], D->cp_stream));
+      } else if (host_args) {  // row chunks; argmins through the device ring to host memory
         for (const DevPlan::Chunk &c : D->chunks[ti]) {
           const int slot = ring_n & 1;
           if (ring_n >= 2) CK(cudaStreamWaitEvent(st, D->c_ev[slot], 0));  // slot copied out
@@ -1071,7 +1229,7 @@ static void run_util(RunImpl &R) {
         st = st0;
       }
     }
-    if (host_args)  // every argmin chunk is in host memory before the value phase
+    if (host_args || P.ex.spill)  // every argmin / message chunk is in host memory before the value phase
       for (int i = 0; i < 2 && i < ring_n; i++) CK(cudaStreamWaitEvent(st, D->c_ev[i], 0));
     if (dag)  // join every branch before the constants
       for (size_t q = 0; q < last_on.size(); q++)
@@ -1398,10 +1556,16 @@ void run_table(const RunImpl *R, int32_t t, void *host_out, uint8_t *host_arg) {
   CK(cudaSetDevice(R->D->device));
   if (host_out) {
     const void *src = R->out[t] ? R->out[t] : R->full[t];
-    if (!src) GBE_FAIL(GBE_E_INVALID, "table %d not retained (plan needs \"retain\":\"all\")", t);
-    if (R->full[t] && !R->out[t])  // gathered: this rank's rows start at lo
-      src = (const char *)src + P.prob->elem() * T.shard.lo;
-    CK(cudaMemcpyAsync(host_out, src, P.prob->elem() * local, cudaMemcpyDeviceToHost, R->stream));
+    if (T.host) {  // out-of-core plan: the message is in pinned host memory
+      CK(cudaStreamSynchronize(R->stream));
+      std::memcpy(host_out, R->D->h_msg + R->D->msg_off[t], P.prob->elem() * local);
+      src = nullptr;
+    } else if (!src) GBE_FAIL(GBE_E_INVALID, "table %d not retained (plan needs \"retain\":\"all\")", t);
+    if (src) {
+      if (R->full[t] && !R->out[t])  // gathered: this rank's rows start at lo
+        src = (const char *)src + P.prob->elem() * T.shard.lo;
+      CK(cudaMemcpyAsync(host_out, src, P.prob->elem() * local, cudaMemcpyDeviceToHost, R->stream));
+    }
   }
   if (host_arg && P.ex.sumprod) {  // sum-product tables have no argmin
     std::memset(host_arg, 0, (size_t)local);

@@ -131,6 +131,131 @@ int64_t mul_sat(int64_t a, int64_t b) {
 
 }  // namespace
 
+// Out-of-core plan (the chunked host<->device pipeline of
+// Fig. 8, generalised to messages): the largest messages move to
+// pinned host memory until the device peak plus two staging slots fits
+// budget_bytes.  Every task then runs in row chunks = runs of whole blocks of
+// its leading output digits: inside one block every input's slice is ONE
+// contiguous range (an input's scope is a subsequence of sep + x in the same
+// order, so the block's fixed digits are its most significant ones), and a
+// chunk's slice of input j is [base_j(first block), base_j(last block) +
+// span_j).  A chunk's staging = its output rows (host message) + argmins +
+// the slices of its host-resident inputs, within one slot.
+namespace {
+// element range of input j over the blocks [b0, b1) of the c leading output
+// digits: the run splits into aligned pieces (a prefix of digits fixed, the
+// rest free); a piece's offsets span [base, base + sum of its free digits'
+// strides * (radix - 1)], plus the in-block extent of the trailing digits
+SpillChunk spill_span(const gbe_bucket_desc &h, int j, int c, int64_t b0, int64_t b1) {
+  int64_t span = h.d;
+  for (int p = c; p < h.nsep; p++) span += h.stride[j][p] * (h.radix[p] - 1);
+  auto base = [&](int64_t b) {
+    int64_t o = 0;
+    for (int p = c - 1; p >= 0; p--) {
+      o += h.stride[j][p] * (b % h.radix[p]);
+      b /= h.radix[p];
+    }
+    return o;
+  };
+  int64_t mn = INT64_MAX, mx = INT64_MIN;
+  int64_t lo = b0;
+  while (lo < b1) {
+    int k = 0;  // free trailing prefix digits of the piece starting at lo
+    int64_t size = 1, ext = 0;
+    while (k < c) {
+      const int p = c - 1 - k;
+      const int64_t nsize = size * h.radix[p];
+      if (lo % nsize != 0 || lo + nsize > b1) break;
+      ext += h.stride[j][p] * (h.radix[p] - 1);
+      size = nsize;
+      k++;
+    }
+    const int64_t o = base(lo);
+    mn = std::min(mn, o);
+    mx = std::max(mx, o + ext);
+    lo += size;
+  }
+  if (mn > mx) return {0, 0};
+  return {mn, mx - mn + span};
+}
+}  // namespace
+
+int64_t spill_chunk_bytes(const Plan &P, size_t ti, int c, int64_t b0, int64_t b1) {
+  const Task &t = P.tasks[ti];
+  const int64_t el = (int64_t)P.prob->elem();
+  int64_t blocks = 1;
+  for (int q = 0; q < c; q++) blocks *= t.desc.radix[q];
+  const int64_t rows = (b1 - b0) * (t.rows / std::max<int64_t>(blocks, 1));
+  int64_t b = ((t.host ? el * rows : 0) + 255) / 256 * 256 + (rows + 255) / 256 * 256;
+  for (int j = 0; j < t.desc.ninputs; j++) {
+    const Member &m = t.members[j];
+    if (m.kind != 1 || !P.tasks[m.index].host) continue;
+    b += (el * spill_span(t.desc, j, c, b0, b1).n + 64 + 255) / 256 * 256;
+  }
+  return b;
+}
+
+SpillChunk spill_chunk_input(const Plan &P, size_t ti, int c, int64_t b0, int64_t b1, int j) {
+  return spill_span(P.tasks[ti].desc, j, c, b0, b1);
+}
+
+static void plan_spill(Plan &P) {
+  const Problem &p = *P.prob;
+  const int64_t el = (int64_t)p.elem();
+  const size_t nt = P.tasks.size();
+  const int64_t B = P.ex.budget_bytes;
+  const int64_t S = P.ex.stage_bytes > 0 ? P.ex.stage_bytes
+                                          : std::min<int64_t>(std::max<int64_t>(B / 4, int64_t(1) << 24),
+                                                              int64_t(4) << 30);
+  P.slot_bytes = S / 2 / 256 * 256;
+  auto dev_peak = [&]() {  // executor allocation sequence with host messages off the device
+    int64_t live = 2 * el * p.table_off[p.nf], peak = live;
+    for (size_t ti = 0; ti < nt; ti++) {
+      const Task &t = P.tasks[ti];
+      live += t.host ? 0 : el * t.rows;
+      peak = std::max(peak, live);
+      if (P.ex.retain < 2)
+        for (auto &m : t.members)
+          if (m.kind == 1 && !P.tasks[m.index].host) live -= el * P.tasks[m.index].rows;
+    }
+    return peak;
+  };
+  std::vector<size_t> by_size(nt);
+  for (size_t i = 0; i < nt; i++) by_size[i] = i;
+  std::stable_sort(by_size.begin(), by_size.end(),
+                   [&](size_t a, size_t b) { return P.tasks[a].rows > P.tasks[b].rows; });
+  size_t next = 0;
+  while (dev_peak() + S > B && next < nt) P.tasks[by_size[next++]].host = true;
+  P.host_bytes = 0;
+  for (auto &t : P.tasks)
+    if (t.host) P.host_bytes += el * t.rows;
+  P.peak_bytes = dev_peak() + S;
+  // chunks: the fewest leading digits whose blocks each fit a slot, then the
+  // largest power-of-two run of consecutive blocks for which every chunk fits
+  constexpr int64_t kMaxChunks = int64_t(1) << 20;
+  for (size_t ti = 0; ti < nt; ti++) {
+    Task &t = P.tasks[ti];
+    auto fits = [&](int c, int64_t blocks, int64_t per) {
+      if ((blocks + per - 1) / per > kMaxChunks) return false;
+      for (int64_t b0 = 0; b0 < blocks; b0 += per)
+        if (spill_chunk_bytes(P, ti, c, b0, std::min(blocks, b0 + per)) > P.slot_bytes) return false;
+      return true;
+    };
+    int c = 0;
+    int64_t blocks = 1;
+    while (c < t.desc.nsep && blocks <= kMaxChunks && !fits(c, blocks, 1)) blocks *= t.desc.radix[c++];
+    if (!fits(c, blocks, 1)) {
+      P.peak_bytes = INT64_MAX / 2;  // even the smallest chunks exceed a slot: over budget
+      return;
+    }
+    int64_t per = 1;
+    while (per < blocks && fits(c, blocks, std::min(blocks, 2 * per))) per = std::min(blocks, 2 * per);
+    t.chunk_digits = c;
+    t.chunk_blocks = per;
+    t.chunk_rows = per * (t.rows / blocks);
+  }
+}
+
 std::unique_ptr<Plan> make_plan(std::shared_ptr<const Problem> pp, const int32_t *order_in,
                                 int32_t ibound, const ExecOptions &ex) {
   const Problem &p = *pp;
@@ -147,6 +272,14 @@ std::unique_ptr<Plan> make_plan(std::shared_ptr<const Problem> pp, const int32_t
     if (ibound >= 0) GBE_FAIL(GBE_E_INVALID, "retain host: exact BE / DPOP only (ibound < 0)");
     if (ex.world_size != 1) GBE_FAIL(GBE_E_INVALID, "retain host: single-rank plans only");
     if (ex.sumprod || ex.count) GBE_FAIL(GBE_E_INVALID, "retain host: min-sum plans only");
+  }
+  if (ex.spill) {
+    if (ibound >= 0) GBE_FAIL(GBE_E_INVALID, "spill: exact BE / DPOP only (ibound < 0)");
+    if (ex.world_size != 1) GBE_FAIL(GBE_E_INVALID, "spill: single-rank plans only");
+    if (ex.count) GBE_FAIL(GBE_E_INVALID, "spill: not with count");
+    if (ex.budget_bytes <= 0) GBE_FAIL(GBE_E_INVALID, "spill needs budget_bytes > 0");
+    // argmins of an out-of-core plan always stream to host memory
+    plan->ex.host_args = ex.retain >= 1 && !ex.sumprod;
   }
   if (ex.count) {
     if (ex.sumprod) GBE_FAIL(GBE_E_INVALID, "count and semiring sumprod are exclusive");
@@ -417,6 +550,10 @@ std::unique_ptr<Plan> make_plan(std::shared_ptr<const Problem> pp, const int32_t
     peak += 2 * std::min(big, plan->ex.host_arg_chunk);
   }
   plan->peak_bytes = peak;
+  if (ex.spill) {
+    plan_spill(*plan);
+    peak = plan->peak_bytes;
+  }
   if (ex.budget_bytes > 0 && peak > ex.budget_bytes) {
     // name the largest bucket
     const Task *big = &plan->tasks[0];
@@ -433,7 +570,8 @@ std::string plan_json(const Plan &plan) {
   o << "{\"n\":" << plan.prob->n << ",\"ibound\":" << plan.ibound << ",\"width\":" << plan.width
     << ",\"total_cells\":" << plan.total_cells << ",\"total_bytes\":" << plan.total_bytes
     << ",\"peak_bytes\":" << plan.peak_bytes << ",\"world_size\":" << plan.ex.world_size
-    << ",\"rank\":" << plan.ex.rank << ",\"order\":[";
+    << ",\"rank\":" << plan.ex.rank << ",\"spill\":" << (plan.ex.spill ? "true" : "false")
+    << ",\"host_bytes\":" << plan.host_bytes << ",\"slot_bytes\":" << plan.slot_bytes << ",\"order\":[";
   for (size_t i = 0; i < plan.order.size(); i++) o << (i ? "," : "") << plan.order[i];
   o << "],\"constants\":[";
   for (size_t i = 0; i < plan.constants.size(); i++)
@@ -452,6 +590,9 @@ std::string plan_json(const Plan &plan) {
       << t.shard.key_digits << ",\"blocks\":" << t.shard.blocks << ",\"per\":" << t.shard.per
       << ",\"lo\":" << t.shard.lo << ",\"hi\":" << t.shard.hi
       << ",\"gather\":" << (t.shard.gather ? "true" : "false") << "}";
+    if (plan.ex.spill)
+      o << ",\"host\":" << (t.host ? "true" : "false") << ",\"chunk_rows\":" << t.chunk_rows
+        << ",\"chunk_digits\":" << t.chunk_digits;
     {
       FastDesc *F = new FastDesc();
       BkfLaunch L;

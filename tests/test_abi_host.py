@@ -279,3 +279,89 @@ def test_domain1_digits_do_not_overflow_tile_tables():
         s *= radix[q]
     v = G.bucket_kernel_variant(_desc(radix, d, [st, st]), 0, int(np.prod(radix)))
     assert v in (0, 1)
+
+
+def test_spill_plan_errors():
+    """"spill" (out-of-core): exact BE/DPOP on one rank,
+    a positive budget; a budget no chunking can meet is GBE_E_BUDGET."""
+    inst = gen.scalefree(40, 3, 0.0, 3)
+    P = G.Problem.from_instance(inst)
+    order, _ = P.order()
+    G.Plan(P, order, spill=True, budget_bytes=1 << 30)  # valid
+    for args, kw in (((2,), dict(spill=True, budget_bytes=1 << 30)),
+                     ((), dict(spill=True, budget_bytes=1 << 30, world_size=2, rank=0)),
+                     ((), dict(spill=True, budget_bytes=1 << 30, count="optimal")),
+                     ((), dict(spill=True)),
+                     ((), dict(spill=True, budget_bytes=1 << 30, stage_bytes=-1))):
+        with pytest.raises(G.GbeError) as e:
+            G.Plan(P, order, *args, **kw)
+        assert e.value.status == 1
+    with pytest.raises(G.GbeError) as e:
+        G.Plan(P, order, spill=True, budget_bytes=4096)
+    assert e.value.status == 3
+
+
+def _input_layout(inst, info, pos, t):
+    """(scope, stride per variable) of every input of table t: originals and
+    messages in the canonical layout (scope ascending by order position,
+    first variable most significant, P:553-554 / P:751-753)."""
+    tab = info["tables"][t]
+    out = []
+    for kind, idx in tab["members"]:
+        scope = [int(v) for v in inst.scope(idx)] if kind == 0 else list(info["tables"][idx]["sep"])
+        scope = sorted(scope, key=lambda v: pos[v])
+        st, s = {}, 1
+        for v in reversed(scope):
+            st[v] = s
+            s *= int(inst.dom[v])
+        out.append((kind, idx, st))
+    return out
+
+
+@pytest.mark.parametrize("seed,budget_frac,stage_div", [(3, 0.6, 16), (4, 0.5, 8), (5, 0.7, 64)])
+def test_spill_plan_chunks_fit_their_slot(seed, budget_frac, stage_div):
+    """Every chunk of an out-of-core plan fits one staging slot: its output
+    rows (host message), argmins and, for each host-resident input, the
+    element range the chunk's rows read -- recomputed here by enumerating the
+    rows of each chunk and applying the index map (Eq. P:673-697) directly."""
+    inst = gen.scalefree(60, 3, 0.0, seed)
+    P = G.Problem.from_instance(inst)
+    order, _ = P.order()
+    pos = {int(v): i for i, v in enumerate(order)}
+    peak = G.Plan(P, order).info()["peak_bytes"]
+    info = G.Plan(P, order, spill=True, budget_bytes=int(peak * budget_frac),
+                  stage_bytes=peak // stage_div).info()
+    assert info["peak_bytes"] <= int(peak * budget_frac)
+    tabs = info["tables"]
+    host = [t["host"] for t in tabs]
+    assert any(host)
+    # greedy by size: no device message is larger than a host one
+    assert min(t["rows"] for t in tabs if t["host"]) >= max([t["rows"] for t in tabs if not t["host"]] + [0])
+    slot = info["slot_bytes"]
+    up = lambda b: (b + 255) // 256 * 256  # noqa: E731
+    nmulti = 0
+    for t, tab in enumerate(tabs):
+        sep, d, rows, cr = tab["sep"], tab["d"], tab["rows"], tab["chunk_rows"]
+        assert 1 <= cr <= rows
+        nmulti += cr < rows
+        dom = [int(inst.dom[v]) for v in sep]
+        layouts = _input_layout(inst, info, pos, t)
+        for lo in range(0, rows, cr):
+            hi = min(rows, lo + cr)
+            need = (up(4 * (hi - lo)) if tab["host"] else 0) + up(hi - lo)
+            r = np.arange(lo, hi, dtype=np.int64)
+            digits = []
+            for q in range(len(sep) - 1, -1, -1):
+                digits.append(r % dom[q])
+                r //= dom[q]
+            digits = digits[::-1]
+            for kind, idx, st in layouts:
+                if kind != 1 or not host[idx]:
+                    continue
+                off = np.zeros(hi - lo, dtype=np.int64)
+                for q, v in enumerate(sep):
+                    off += digits[q] * st.get(v, 0)
+                n = int(off.max() - off.min()) + d
+                need += up(4 * n + 64)
+            assert need <= slot, (t, lo, need, slot)
+    assert nmulti > 0
