@@ -23,6 +23,7 @@ C2_SEED = 2       # min-fill w* = 10
 C4_SEED = 5       # min-fill w* = 20
 C4_ALT_SEED = 9   # n=200, d=3, min-fill w* = 16 (smaller variant for tests)
 C5_SEED = 2       # min-fill w* = 18
+C4D4_SEED = 12    # SURVEY's C4 alternative: n=150, d=4, min-fill w* = 16 (4^16 = 4.29e9 rows)
 
 
 def c1(seed=0, literal=False, p2=0.0):
@@ -44,6 +45,11 @@ def c3_order(rows=20, cols=20):
 
 def c4(seed=C4_SEED, n=200, d=3):
     return scalefree(n, d, 0.0, seed)
+
+
+def c4d4(seed=C4D4_SEED):
+    """The BA DCOP at the BASELINE domain d = 4 (n = 150, w* = 16)."""
+    return scalefree(150, 4, 0.0, seed)
 
 
 def c5(seed=C5_SEED):

@@ -319,7 +319,15 @@ cudaError_t dispatch(const StreamDesc *dd, const BksLaunch &L, const InPtrs &in,
     if ((uintptr_t)in.p[j] % 16) aligned = false;
   if (aligned) {
     if constexpr (sizeof(T) == 8) {
+      // d = 4: two lanes per row, one 16-byte load each (a warp's load of a
+      // dense input covers 16 consecutive rows); GBE_STREAM_V4=0: A/B knob
+      static const int v4 = [] {
+        const char *e = std::getenv("GBE_STREAM_V4");
+        return e ? std::atoi(e) : 4;
+      }();
       if (L.d == 2) return launch<T, SP, 1, 2, 2, 4, 2>(dd, L, in, out, arg, rb, re, s);
+      if (L.d == 4 && v4 == 4) return launch<T, SP, 2, 2, 4, 4, 2>(dd, L, in, out, arg, rb, re, s);
+      if (L.d == 4 && v4 == 8) return launch<T, SP, 2, 2, 4, 8, 2>(dd, L, in, out, arg, rb, re, s);
       if (L.d == 8) return launch<T, SP, 4, 2, 8, 4, 2>(dd, L, in, out, arg, rb, re, s);
     } else {
       if (L.d == 2) return launch<T, SP, 1, 2, 2, 4, 2>(dd, L, in, out, arg, rb, re, s);

@@ -127,7 +127,8 @@ struct DevPlan {
   struct Chunk {
     int64_t lo = 0, hi = 0;
     int fidx = -1;        // index into h_cfast / cfl (tiled kernel), -1: generic
-    bool stream = false;  // streaming kernel over [lo, hi) (the task's StreamDesc)
+    bool stream = false;  // streaming kernel over [lo, hi)
+    int sidx = -1;        // its descriptor: index into h_cstream
     BksLaunch sl{};
     BkLaunchInfo li{};
     // out-of-core plans ("spill"): staging-slot layout of this chunk
@@ -152,6 +153,10 @@ struct DevPlan {
   std::vector<FastDesc> h_cfast;
   std::vector<BkfLaunch> cfl;
   FastDesc *d_cfast = nullptr;
+  // the streaming kernel's descriptor depends on the row range (warp-tile
+  // length, tile order): one per chunk
+  std::vector<StreamDesc> h_cstream;
+  StreamDesc *d_cstream = nullptr;
   uint8_t *h_harg = nullptr, *d_harg = nullptr;  // pinned mapped host argmins and their device alias
   std::vector<size_t> harg_off;
   uint8_t *d_ring = nullptr;
@@ -213,6 +218,7 @@ struct DevPlan {
     cudaFree(d_desc);
     cudaFree(d_mdesc);
     cudaFree(d_cfast);
+    cudaFree(d_cstream);
     cudaFree(d_ring);
     if (h_harg) cudaFreeHost(h_harg);
     if (h_msg) cudaFreeHost(h_msg);
@@ -606,6 +612,8 @@ static void plan_spill_chunks(const Plan &P, DevPlan *D, bool noinf) {
         D->cfl.push_back(L);
       } else if (D->use_stream[ti] && bks_build(D->h_desc[ti], c.lo, c.hi, D->num_sms, Sd, c.sl)) {
         c.stream = true;
+        c.sidx = (int)D->h_cstream.size();
+        D->h_cstream.push_back(Sd);
       } else {
         c.li = bk_plan_launch(D->h_desc[ti], c.lo, c.hi, BK_GENERIC, D->num_sms);
       }
@@ -621,6 +629,10 @@ static void plan_spill_chunks(const Plan &P, DevPlan *D, bool noinf) {
   CK(cudaMalloc(&D->d_cfast, sizeof(FastDesc) * std::max<size_t>(D->h_cfast.size(), 1)));
   if (!D->h_cfast.empty())
     CK(cudaMemcpy(D->d_cfast, D->h_cfast.data(), sizeof(FastDesc) * D->h_cfast.size(), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&D->d_cstream, sizeof(StreamDesc) * std::max<size_t>(D->h_cstream.size(), 1)));
+  if (!D->h_cstream.empty())
+    CK(cudaMemcpy(D->d_cstream, D->h_cstream.data(), sizeof(StreamDesc) * D->h_cstream.size(),
+                  cudaMemcpyHostToDevice));
   CK(cudaStreamCreateWithFlags(&D->cp_stream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&D->h2d_stream, cudaStreamNonBlocking));
   for (int i = 0; i < 2; i++) {
@@ -726,6 +738,8 @@ static DevPlan *dev_plan(gbe_plan *gp) {
           D->cfl.push_back(L);
         } else if (D->use_stream[ti] && bks_build(D->h_desc[ti], c.lo, c.hi, D->num_sms, Sd, c.sl)) {
           c.stream = true;
+          c.sidx = (int)D->h_cstream.size();
+          D->h_cstream.push_back(Sd);
         } else {
           c.li = bk_plan_launch(D->h_desc[ti], c.lo, c.hi, BK_GENERIC, D->num_sms);
         }
@@ -739,6 +753,10 @@ static DevPlan *dev_plan(gbe_plan *gp) {
     CK(cudaMalloc(&D->d_cfast, sizeof(FastDesc) * std::max<size_t>(D->h_cfast.size(), 1)));
     if (!D->h_cfast.empty())
       CK(cudaMemcpy(D->d_cfast, D->h_cfast.data(), sizeof(FastDesc) * D->h_cfast.size(), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&D->d_cstream, sizeof(StreamDesc) * std::max<size_t>(D->h_cstream.size(), 1)));
+    if (!D->h_cstream.empty())
+      CK(cudaMemcpy(D->d_cstream, D->h_cstream.data(), sizeof(StreamDesc) * D->h_cstream.size(),
+                    cudaMemcpyHostToDevice));
     CK(cudaStreamCreateWithFlags(&D->cp_stream, cudaStreamNonBlocking));
     for (int i = 0; i < 2; i++) {
       CK(cudaEventCreateWithFlags(&D->k_ev[i], cudaEventDisableTiming));
@@ -1133,7 +1151,10 @@ static void run_util(RunImpl &R) {
               for (const auto &hi : c.hin) CK(cudaStreamWaitEvent(D->h2d_stream, D->done_ev[hi.src], 0));
               waited = true;
             }
-            if (ring_n >= 2) CK(cudaStreamWaitEvent(D->h2d_stream, D->k_ev[slot], 0));  // slot inputs read
+            if (ring_n >= 2) {  // the slot's previous chunk: inputs read, outputs / argmins copied out
+              CK(cudaStreamWaitEvent(D->h2d_stream, D->k_ev[slot], 0));
+              CK(cudaStreamWaitEvent(D->h2d_stream, D->c_ev[slot], 0));
+            }
             for (const auto &hi : c.hin) {
               // the slice keeps the 16-byte phase it has in the full table, so
               // the kernel's aligned (TMA / vector) reads see the same layout
@@ -1152,7 +1173,7 @@ static void run_util(RunImpl &R) {
           if (c.fidx >= 0)
             CK(bkf_launch(D->d_cfast + c.fidx, D->cfl[c.fidx], in, oc, ra, c.lo, st));
           else if (c.stream)
-            CK(bks_launch(D->d_stream + ti, c.sl, in, oc, ra, c.lo, c.hi, st));
+            CK(bks_launch(D->d_cstream + c.sidx, c.sl, in, oc, ra, c.lo, c.hi, st));
           else
             CK(bk_launch(D->h_desc[ti], D->d_desc + ti, in, oc, ra, c.lo, c.hi, c.li, st));
           CK(cudaEventRecord(D->k_ev[slot], st));
@@ -1176,7 +1197,7 @@ static void run_util(RunImpl &R) {
           if (c.fidx >= 0)
             CK(bkf_launch(D->d_cfast + c.fidx, D->cfl[c.fidx], ins[ti], oc, ra, c.lo, st));
           else if (c.stream)
-            CK(bks_launch(D->d_stream + ti, c.sl, ins[ti], oc, ra, c.lo, c.hi, st));
+            CK(bks_launch(D->d_cstream + c.sidx, c.sl, ins[ti], oc, ra, c.lo, c.hi, st));
           else
             CK(bk_launch(D->h_desc[ti], D->d_desc + ti, ins[ti], oc, ra, c.lo, c.hi, c.li, st));
           CK(cudaEventRecord(D->k_ev[slot], st));
@@ -1499,7 +1520,16 @@ static std::string stats_json(const RunImpl &R) {
       o << ",\"tile_rows\":" << fh.PL << ",\"stages\":" << fh.nstages << ",\"staging_bufs\":" << fh.nout
         << ",\"groups\":" << R.D->fl[ti].NG << ",\"classes\":[" << fh.cls_off[1] - fh.cls_off[0] << ","
         << fh.cls_off[2] - fh.cls_off[1] << "," << fh.cls_off[3] - fh.cls_off[2] << "," << fh.cls_off[4] - fh.cls_off[3]
-        << "]";
+        << "],\"g\":[" << R.D->fl[ti].g1 << "," << R.D->fl[ti].g2 << "],\"slen\":[";
+      for (int q = 0; q < fh.k; q++) o << (q ? "," : "") << fh.slen[q];
+      o << "],\"in_scope\":[";  // per class-ordered input: the output digits it has
+      const gbe_bucket_desc &hd = R.D->h_desc[ti];
+      for (int q = 0; q < fh.k; q++) {
+        o << (q ? "," : "") << "\"";
+        for (int pp = 0; pp < hd.nsep; pp++) o << (hd.stride[fh.in_idx[q]][pp] ? 'X' : '.');
+        o << "\"";
+      }
+      o << "]";
     }
     o
       << ",\"ms\":" << (ti < R.ms.size() ? R.ms[ti] : -1.0f)

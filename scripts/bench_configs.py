@@ -134,6 +134,9 @@ def main(which):
     if "c4" in which:
         inst = configs.c4()
         measure("C4", inst, oracle.minfill_order(inst), -1)
+    if "c4d4" in which:  # SURVEY's alternative C4: n=150, d=4, w*=16
+        inst = configs.c4d4()
+        measure("C4-d4", inst, oracle.minfill_order(inst), -1)
     if "c5" in which:
         inst = configs.c5()
         order = oracle.minfill_order(inst)
@@ -146,4 +149,4 @@ def main(which):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5"])
+    main(sys.argv[1:] or ["c1", "c2", "c3", "c4", "c4d4", "c5"])

@@ -8,7 +8,7 @@ from gen import configs
 wl = sys.argv[1] if len(sys.argv) > 1 else "c4"
 ib = int(sys.argv[2]) if len(sys.argv) > 2 else -1
 inst = {"c4": configs.c4, "c2": configs.c2, "c5": configs.c5, "c3": configs.c3,
-        "c4alt": lambda: configs.c4(seed=configs.C4_ALT_SEED)}[wl]()
+        "c4alt": lambda: configs.c4(seed=configs.C4_ALT_SEED), "c4d4": configs.c4d4}[wl]()
 P = G.Problem.from_instance(inst)
 order = configs.c3_order() if wl == "c3" else P.order()[0]
 info = G.Plan(P, order, ib).info()

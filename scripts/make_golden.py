@@ -7,7 +7,7 @@ configs; for the f64 config (C5) the f64 sum / min / max of the finite
 entries and the count of infinite ones (the tiled kernel's f64 summation order
 differs from the oracle's canonical order, so digests would not be stable).
 
-  python scripts/make_golden.py [c2] [c4] [c3] [c5] [c3i18]
+  python scripts/make_golden.py [c2] [c4] [c4d4] [c3] [c5] [c3i18]
 
 c3i18 (MBE i = 18 on the 20x20 grid, 3.8e11 cells, value-only) records
 digests of kind 1 (oracle.mix_digest) instead of FNV-1a.
@@ -97,6 +97,10 @@ def main(which):
         inst = configs.c4()
         order = oracle.minfill_order(inst)
         json.dump(int_record("C4", inst, order, -1, False), open(os.path.join(OUT, "c4.json"), "w"))
+    if "c4d4" in which:  # SURVEY's alternative C4 (n=150, d=4, w*=16): 3.4e10 cells
+        inst = configs.c4d4()
+        order = oracle.minfill_order(inst)
+        json.dump(int_record("C4-d4", inst, order, -1, False), open(os.path.join(OUT, "c4d4.json"), "w"))
     if "c3" in which:
         inst = configs.c3()
         order = configs.c3_order()

@@ -73,6 +73,13 @@ def test_c4_full_dpop_digests():
     _dpop_against("c4.json", configs.c4())
 
 
+def test_c4d4_full_dpop_digests():
+    """SURVEY's alternative C4 at the BASELINE domain d = 4 (n = 150, min-fill
+    w* = 16): the largest table 4^16 = 4.29e9 rows, so the tiled kernel's
+    R = 4 register-block shapes run at full size."""
+    _dpop_against("c4d4.json", configs.c4d4())
+
+
 def test_c3_grid_mbe_sweep_and_exact():
     """MBE / ADPOP i-bound sweep on the 20x20 grid: lower bounds, tables,
     upper bounds and assignments against the oracle; then i = 18 and the

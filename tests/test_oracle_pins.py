@@ -397,6 +397,9 @@ def test_pinned_config_widths():
     c5 = configs.c5()
     assert oracle.induced_width(c5, oracle.minfill_order(c5)) == 18
     assert oracle.induced_width(configs.c3(), configs.c3_order()) == 20
+    c4d4 = configs.c4d4()  # SURVEY's alternative C4: n=150, d=4, w*=16
+    assert oracle.induced_width(c4d4, oracle.minfill_order(c4d4)) == 16
+    assert len(c4d4.dom) == 150 and set(int(v) for v in c4d4.dom) == {4}
 
 
 # ------------------------------------------------ sum-product (§8(f) row 3)
