@@ -430,8 +430,10 @@ __global__ void __launch_bounds__((NG * GW + 1 + NG) * 32, 1)
   int32_t *offtab = (int32_t *)(sm + f.off_tab);
   int32_t *mrowoff = (int32_t *)(sm + f.off_mrow);
   // per-CTA tables: slice offset of every thread group, per input; row offset
+  const bool qperm = Fg->qperm_on != 0;
   for (int idx = threadIdx.x; idx < (k + 1) * Pmid; idx += blockDim.x) {
     int jj = idx / Pmid, q = idx - jj * Pmid;
+    if (qperm) q = Fg->qperm[q];
     int off = 0;
     for (int e = f.nmid - 1; e >= 0; e--) {
       int r = f.mrad[e], dg = q % r;
@@ -778,6 +780,81 @@ bool supported(int R, int R2, int DV, int es) {
 // host: choose L (tile digits), the group digits, the tile order, the smem
 // layout; false when the bucket does not fit this kernel (-> bk_generic)
 
+namespace {
+// Shared-memory bank conflicts of the consumers' loads and staging stores
+// depend on which 32 mid-digit combinations a warp handles together: the
+// natural order puts combinations whose offsets agree mod 32 banks in one
+// warp (radix-3 strides: 2 wavefronts per LDS / STS on C4's largest
+// buckets).  Greedy assignment: combinations in order of how crowded their
+// residues are, each to the warp where it adds the fewest same-bank
+// collisions, weighted by how many loads (stores) per register block the
+// input (the output) issues.
+void build_qperm(FastDesc &F, int es, int R, int R2, int Pmid, int64_t rows) {
+  F.qperm_on = 0;
+  static const bool off = std::getenv("GBE_FAST_NO_QPERM") != nullptr;  // A/B knob
+  const FastHot &f = F.hot;
+  if (off || es != 4 || Pmid < 64 || Pmid > kMaxPmid || rows < (int64_t(1) << 22)) return;
+  const int nw = (Pmid + 31) / 32;
+  const int ns = f.k + 1;  // streams: inputs, then the output rows
+  std::vector<int> res((size_t)Pmid * ns);
+  std::vector<int> w(ns);
+  for (int q = 0; q < Pmid; q++) {
+    int x = q;
+    std::vector<int> dg(f.nmid);
+    for (int e = f.nmid - 1; e >= 0; e--) {
+      dg[e] = x % f.mrad[e];
+      x /= f.mrad[e];
+    }
+    for (int j = 0; j < ns; j++) {
+      int64_t o = 0;
+      for (int e = 0; e < f.nmid; e++) o += (int64_t)dg[e] * (j < f.k ? f.mstr[e][j] : f.mrow[e]);
+      res[(size_t)q * ns + j] = (int)(o & 31);
+    }
+  }
+  for (int j = 0; j < ns; j++) {  // loads (stores) per register block
+    if (j == f.k) {
+      w[j] = 2 * R * R2;  // outputs + argmins
+      continue;
+    }
+    const bool h1 = f.sg1[j] != 0, h2 = f.sg2[j] != 0;
+    w[j] = f.DV * (h1 ? R : 1) * (h2 ? R2 : 1);
+  }
+  std::vector<int> freq((size_t)ns * 32, 0);
+  for (int q = 0; q < Pmid; q++)
+    for (int j = 0; j < ns; j++) freq[(size_t)j * 32 + res[(size_t)q * ns + j]] += w[j];
+  std::vector<int> order(Pmid);
+  for (int q = 0; q < Pmid; q++) order[q] = q;
+  std::vector<int> crowd(Pmid, 0);
+  for (int q = 0; q < Pmid; q++)
+    for (int j = 0; j < ns; j++) crowd[q] += freq[(size_t)j * 32 + res[(size_t)q * ns + j]];
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return crowd[a] > crowd[b]; });
+  std::vector<int> cnt((size_t)nw * ns * 32, 0), fill(nw, 0);
+  std::vector<std::vector<int>> slots(nw);
+  for (int q : order) {
+    int best = -1;
+    int64_t bc = INT64_MAX;
+    for (int wi = 0; wi < nw; wi++) {
+      const int cap = wi == nw - 1 ? Pmid - 32 * (nw - 1) : 32;
+      if (fill[wi] >= cap) continue;
+      int64_t c = 0;
+      for (int j = 0; j < ns; j++) c += (int64_t)w[j] * cnt[((size_t)wi * ns + j) * 32 + res[(size_t)q * ns + j]];
+      c = c * 64 + fill[wi];  // ties: the emptier warp
+      if (c < bc) {
+        bc = c;
+        best = wi;
+      }
+    }
+    fill[best]++;
+    slots[best].push_back(q);
+    for (int j = 0; j < ns; j++) cnt[((size_t)best * ns + j) * 32 + res[(size_t)q * ns + j]]++;
+  }
+  int pos = 0;
+  for (int wi = 0; wi < nw; wi++)
+    for (int q : slots[wi]) F.qperm[pos++] = (uint16_t)q;
+  F.qperm_on = 1;
+}
+}  // namespace
+
 bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int num_sms,
                FastDesc &F, BkfLaunch &L, bool noinf) {
   const int m = h.nsep, k = h.ninputs, DV = h.d;
@@ -918,6 +995,7 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     }
     f.rs1 = (int32_t)rowstride[g1];
     f.rs2 = g2 >= 0 ? (int32_t)rowstride[g2] : 0;
+    build_qperm(F, es, R, R2, (int)Pmid, row_end - row_begin);
     // H digits: natural order; for a full-range launch, digits absent from
     // the largest input go last (fastest) so their re-reads hit L2
     std::vector<int> hd;

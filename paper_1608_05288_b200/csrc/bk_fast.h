@@ -8,6 +8,8 @@
 
 namespace gbe {
 
+constexpr int kMaxPmid = 8192;  // PL <= 16384 rows, R * R2 >= 2
+
 // Fields every CTA copies into shared memory (all int32).
 struct FastHot {
   int32_t k, es, PL, Pmid, R, DV, nmid, nH;  // R: radix of g1 (g2 has R or is absent)
@@ -32,6 +34,12 @@ struct FastDesc {
   int64_t hrow[32];      // output row stride of each high digit
   int64_t hstr[32][32];  // element stride per high digit, per (class-ordered) input
   int64_t shift[32];
+  // thread-block slot q -> mid-digit combination (the in-tile offsets of slot
+  // q are those of combination qperm[q]); chosen on the host so that the 32
+  // combinations a warp handles together hit distinct shared-memory banks
+  // (qperm_on = 0: identity)
+  int32_t qperm_on, pad3;
+  uint16_t qperm[kMaxPmid];
 };
 
 struct BkfLaunch {

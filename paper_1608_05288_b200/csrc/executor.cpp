@@ -700,7 +700,8 @@ static DevPlan *dev_plan(gbe_plan *gp) {
                          bkf_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_fast[ti], D->fl[ti], noinf);
     const bool stream_ok = (want == -1 || want == 2) && !P.ex.count &&
                            bks_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_stream[ti], D->sl[ti]);
-    D->cand[ti] = want == -1 && P.ex.autotune && kernel_policy() < 0 && !P.ex.host_args && fast_ok && stream_ok;
+    D->cand[ti] = want == -1 && P.ex.autotune && kernel_policy() < 0 && !P.ex.host_args && !P.ex.spill && fast_ok &&
+                  stream_ok;
     if (D->cand[ti]) D->tune_phase = 0;
     if (fast_ok && (!stream_ok || !prefer_stream(h, D->fl[ti]))) {
       D->use_fast[ti] = 1;
