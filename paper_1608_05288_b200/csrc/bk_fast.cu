@@ -45,7 +45,7 @@ constexpr uint32_t kInf = GBE_INF_I32;
 constexpr int kMaxStages = 8;
 constexpr int kOutBufsMax = 3;  // output staging buffers per consumer group (2 or 3)
 constexpr int64_t kMinCells = 1 << 10;  // measured: the tiled kernel beats bk_generic from ~1e3 cells
-constexpr int kSmemCap = 196 * 1024;  // dynamic shared memory cap per CTA
+constexpr int kSmemCap = 220 * 1024;  // dynamic shared memory cap per CTA (static use ~5 KB of the 227 KB)
 
 template <typename T>
 struct SrF;
@@ -169,21 +169,24 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // slice, tb[L][j], and its first output row, trow[L].  One batch serves the
 // next 32 tiles, so the per-tile issue path is a few shared-memory reads.
 constexpr int kMaxH = 32;
-struct ProdTiles {      // one producer's decoded batch
-  int64_t tb[32][32];    // [tile in batch][class-ordered input] element offset (shift applied)
-  int64_t trow[32];      // first output row of the tile
+// Decode tables live in dynamic shared memory sized by the input count k
+// (f.off_prod): hstr[nH][k], then per producer warp trow[32] and tb[32][k]
+// (a static [32][32] layout cost 25 KB, a ring stage's worth, on every bucket)
+struct ProdTiles {      // one producer's decoded batch (views into dynamic smem)
+  int64_t *tb;          // [tile in batch][class-ordered input] element offset (shift applied)
+  int64_t *trow;        // [tile in batch] first output row of the tile
 };
 struct ProdSmem {
-  ProdTiles pt[2];       // per producer warp
-  int64_t hstr[kMaxH][32];
   int64_t hrow[kMaxH];
   int64_t shift[32];
   uint32_t hrad[kMaxH];
+  int64_t *hstr;        // [high digit][class-ordered input]
 };
 
 __device__ __forceinline__ void decode_batch(ProdSmem &ps, ProdTiles &pt, const FastHot &f, int64_t t, int64_t step,
                                              int64_t t_end) {
   const int lane = threadIdx.x & 31;
+  const int k = f.k;
   const int64_t tl = t + (int64_t)lane * step;
   if (tl < t_end) {
     uint32_t x = (uint32_t)tl;
@@ -203,12 +206,12 @@ __device__ __forceinline__ void decode_batch(ProdSmem &ps, ProdTiles &pt, const 
     for (int e = 0; e < kMaxH; e++)
       if (e < f.nH) rs += (int64_t)dg[e] * ps.hrow[e];
     pt.trow[lane] = rs;
-    for (int j = 0; j < f.k; j++) {
+    for (int j = 0; j < k; j++) {
       int64_t acc = -ps.shift[j];
 #pragma unroll
       for (int e = 0; e < kMaxH; e++)
-        if (e < f.nH) acc += (int64_t)dg[e] * ps.hstr[e][j];
-      pt.tb[lane][j] = acc;
+        if (e < f.nH) acc += (int64_t)dg[e] * ps.hstr[e * k + j];
+      pt.tb[lane * k + j] = acc;
     }
   }
   __syncwarp();
@@ -224,7 +227,7 @@ __device__ __forceinline__ void issue_tile(const ProdTiles &ps, const FastHot &f
   uintptr_t a16 = 0;
   uint32_t bytes = 0, skew = 0;
   if (lane < f.k) {
-    const char *p = my_in + ps.tb[L][lane] * f.es;
+    const char *p = my_in + ps.tb[L * f.k + lane] * f.es;
     a16 = (uintptr_t)p & ~(uintptr_t)15;
     const uintptr_t e16 = ((uintptr_t)p + (uintptr_t)f.slen[lane] * f.es + 15) & ~(uintptr_t)15;
     bytes = (uint32_t)(e16 - a16);
@@ -401,8 +404,12 @@ __global__ void __launch_bounds__((NG * GW + 1 + NG) * 32, 1)
   // read it; ostart[g][b] = that tile's first output row (relative)
   __shared__ uint64_t ofull[NG][kOutBufsMax], oempty[NG][kOutBufsMax];
   __shared__ int64_t ostart[NG][kOutBufsMax];
-  __shared__ ProdSmem ps;  // producer's decode tables
-  for (int i = threadIdx.x; i < kMaxH * 32; i += blockDim.x) ps.hstr[i / 32][i % 32] = Fg->hstr[i / 32][i % 32];
+  __shared__ ProdSmem ps;  // producer's decode tables (the large ones in dynamic smem)
+  {
+    const int kk = Fg->hot.k, nh = Fg->hot.nH;
+    ps.hstr = (int64_t *)(sm + Fg->hot.off_prod);
+    for (int i = threadIdx.x; i < nh * kk; i += blockDim.x) ps.hstr[i] = Fg->hstr[i / kk][i % kk];
+  }
   if (threadIdx.x < kMaxH) {
     ps.hrow[threadIdx.x] = Fg->hrow[threadIdx.x];
     ps.hrad[threadIdx.x] = (uint32_t)Fg->hrad[threadIdx.x];
@@ -454,7 +461,12 @@ __global__ void __launch_bounds__((NG * GW + 1 + NG) * 32, 1)
     // batch decode overlaps the other's issuing
     const int lane = threadIdx.x & 31;
     const int p = warp - NG * GW - 1;
-    ProdTiles &pt = ps.pt[p];
+    ProdTiles pt;
+    {
+      int64_t *pb = (int64_t *)(sm + f.off_prod) + f.nH * k + p * 32 * (k + 1);
+      pt.trow = pb;
+      pt.tb = pb + 32;
+    }
     const char *my_in = lane < k ? (const char *)in.p[f.in_idx[lane]] : nullptr;
     int s = p % nst, L = 0;
     uint32_t ph = (uint32_t)((p / nst) & 1);
@@ -791,7 +803,10 @@ namespace {
 // input (the output) issues.
 void build_qperm(FastDesc &F, int es, int R, int R2, int Pmid, int64_t rows) {
   F.qperm_on = 0;
-  static const bool off = std::getenv("GBE_FAST_NO_QPERM") != nullptr;  // A/B knob
+  // measured SLOWER on C4 (kernel sum 28.0 -> 29.2 ms: x57 7.09 -> 7.48,
+  // x9 6.13 -> 6.47; the scattered argmin byte stores it causes are not in
+  // its model), so it is off unless GBE_FAST_QPERM=1 (A/B knob)
+  static const bool off = std::getenv("GBE_FAST_QPERM") == nullptr;
   const FastHot &f = F.hot;
   if (off || es != 4 || Pmid < 64 || Pmid > kMaxPmid || rows < (int64_t(1) << 22)) return;
   const int nw = (Pmid + 31) / 32;
@@ -933,7 +948,7 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     const int64_t Pmid = PL / (R * R2);
     if (row_begin % PL || row_end % PL) continue;
     const int NG = ng_of(es, R, R2, DV), GW = gw_of(es, R, R2, DV);
-    const size_t kSmemMax = (size_t)(smem_env ? std::atoi(smem_env) : 196) * 1024;
+    const size_t kSmemMax = (size_t)(smem_env ? std::atoi(smem_env) : 220) * 1024;
     const int min_st = pass == 0 ? std::max(kStagesWant, 2 * NG) : NG;
     // classes
     std::memset(&F, 0, sizeof(F));
@@ -1028,14 +1043,14 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     f.arg_bytes = (int32_t)(((size_t)PL + 16 + 127) & ~size_t(127));
     // 3 staging buffers when they fit beside the wanted ring (the store of
     // a tile then has a whole tile of compute to drain), else 2
-    const size_t tabs = (size_t)(k + 1) * Pmid * 4 + 256;
+    const size_t tabs = (size_t)(k + 1) * Pmid * 4 + 256 + 8 * ((size_t)f.nH * k + 64 * (size_t)(k + 1)) + 256;
     const size_t obuf = (size_t)NG * ((size_t)f.out_bytes + f.arg_bytes);
     static const int kNob = [] {  // GBE_FAST_NOUT: tuning knob (2 or 3)
       const char *e = std::getenv("GBE_FAST_NOUT");
-      return e ? std::max(2, std::min(kOutBufsMax, std::atoi(e))) : kOutBufsMax;
+      return e ? std::max(1, std::min(kOutBufsMax, std::atoi(e))) : kOutBufsMax;
     }();
     int nob = kNob;
-    while (nob > 2 && obuf * nob + tabs + (size_t)min_st * off > kSmemMax) nob--;
+    while (nob > std::min(2, kNob) && obuf * nob + tabs + (size_t)min_st * off > kSmemMax) nob--;
     f.nout = nob;
     size_t fixed = obuf * nob + tabs;
     // the ring length is a multiple of NG: stage s then always serves group
@@ -1056,6 +1071,9 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     off += (size_t)k * Pmid * 4;
     f.off_mrow = (int32_t)off;
     off += (size_t)Pmid * 4;
+    off = (off + 127) & ~size_t(127);
+    f.off_prod = (int32_t)off;  // producer decode tables: hstr[nH][k], 2 x (trow[32], tb[32][k])
+    off += 8 * ((size_t)f.nH * k + 2 * 32 * (size_t)(k + 1));
     off = (off + 127) & ~size_t(127);
     if (off > kSmemMax) continue;
     L.smem = (int)off;

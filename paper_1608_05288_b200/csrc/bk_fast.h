@@ -22,7 +22,7 @@ struct FastHot {
   int32_t rs1, rs2;      // in-tile row strides of g1, g2
   int32_t mrad[12], mrow[12];  // middle digits (L minus group), most significant first
   int32_t mstr[12][32];  // their element strides per input
-  int32_t off_out, off_arg, off_tab, off_mrow;
+  int32_t off_out, off_arg, off_tab, off_mrow, off_prod;
   int32_t nstages, out_bytes, arg_bytes, nout;
 };
 

@@ -109,7 +109,7 @@ struct VecLd<int32_t, 2> {
   }
 };
 
-template <typename T, bool SP, int LPR, int VPL, int DV, int UN, int VEC = 1>
+template <typename T, bool SP, int LPR, int VPL, int DV, int UN, int VEC = 1, bool BD = false>
 __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restrict__ D, InPtrs in,
                                                     T *__restrict__ out, uint8_t *__restrict__ arg,
                                                     int64_t row_begin, int64_t row_end, int64_t t0,
@@ -162,6 +162,13 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
   constexpr int G = 32 / LPR;  // row groups per pass
   const int grp = lane / LPR, sub = lane % LPR;
   static_assert(VEC == 1 || (VPL == VEC && DV == LPR * VEC), "vector path: one vector per lane, exact d");
+  static_assert(!BD || (LPR == 1 && VEC == 1), "broadcast digit: one lane per row, scalar loads");
+  // broadcast digit: pass rows are i = l0 + grp (i < PL / UN enumerates the
+  // rows whose digit b is 0) and the lane's UN rows lb(i) + u * bs
+  const int bs = BD ? D->bd_stride : 0;
+  const uint32_t bhas = BD ? D->bd_has : 0u;
+  const int64_t brs = BD ? (D->bd_rowstride ? D->bd_rowstride : (int64_t)bs) : 0;  // output-row stride of b
+  const int PLi = BD ? PL / UN : PL;
   // value index of this lane's i-th value
   auto vix = [&](int i) { return VEC > 1 ? sub * VEC + i : sub + i * LPR; };
   // inputs in chunks of KU: every load of a chunk is issued before the
@@ -178,12 +185,26 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
     constexpr bool MASK = decltype(maskc)::value;
     Acc acc[UN][VPL];
     bool valid[UN];
+    int lrow[UN];      // in-tile row (offset-table index) of each of this lane's UN rows
+    int64_t grow[UN];  // its output row relative to the tile's first row
+    if constexpr (BD) {
+      const int i = l0 + grp;
+      const int lb = (i / bs) * bs * UN + i % bs;
+#pragma unroll
+      for (int u = 0; u < UN; u++) {
+        lrow[u] = lb + u * bs;
+        grow[u] = lb + u * brs;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < UN; u++) grow[u] = lrow[u] = l0 + u * G + grp;
+    }
 #pragma unroll
     for (int u = 0; u < UN; u++) {
       if constexpr (MASK) {
-        const int l = l0 + u * G + grp;
-        const int64_t r = trow + l;
-        valid[u] = l < PL && r >= row_begin && r < row_end;
+        const int l = lrow[u];
+        const int64_t r = trow + grow[u];
+        valid[u] = (BD ? l0 + grp < PLi : l < PL) && r >= row_begin && r < row_end;
       } else {
         valid[u] = true;
       }
@@ -201,12 +222,22 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
         const int j = j0 + jj;
         if (j >= k) break;
         const T *pj = FIRST ? pb[jj] : (const T *)in.p[j] + shfl64(base, j) + lane_off;
-        const int32_t *lo = loff + j * PL + l0 + grp;
+        const int32_t *lo = loff + j * PL;
+        // an input without the broadcast digit: one load serves all UN rows
+        const bool once = BD && !((bhas >> j) & 1u);
 #pragma unroll
         for (int u = 0; u < UN; u++) {
           if (MASK && !valid[u]) continue;
-          const T *q = pj + lo[u * G];
           Acc *dst = (FIRST && jj == 0) ? acc[u] : x[jj][u];
+          if (BD && u > 0 && once) {
+            const Acc *src = (FIRST && jj == 0) ? acc[0] : x[jj][0];
+            if (!MASK || valid[0]) {
+#pragma unroll
+              for (int i = 0; i < VPL; i++) dst[i] = src[i];
+              continue;
+            }
+          }
+          const T *q = pj + lo[lrow[u]];
           if constexpr (VEC > 1) {
             VecLd<T, VEC>::ld(q, dst);
           } else {
@@ -262,7 +293,7 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
         bv = 0;
       }
       if (sub == 0 && (!MASK || valid[u])) {
-        const int64_t r = trow + l0 + u * G + grp - row_begin;
+        const int64_t r = trow + grow[u] - row_begin;
         out[r] = S::out(best);
         if (arg) arg[r] = (uint8_t)bv;
       }
@@ -289,18 +320,22 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
     for (int jj = 0; jj < KU; jj++)
       if (jj < k) pb[jj] = (const T *)in.p[jj] + shfl64(base, jj) + lane_off;
     int l0 = 0;
-    if (trow >= row_begin && trow + PL <= row_end)  // whole tile: unmasked passes
-      for (; l0 + G * UN <= PL; l0 += G * UN) pass(std::false_type{}, l0);
-    for (; l0 < PL; l0 += G * UN) pass(std::true_type{}, l0);
+    constexpr int kStep = BD ? G : G * UN;  // pass rows (BD: rows with digit b = 0)
+    // whole tile: unmasked passes (a tile with a high broadcast digit spans
+    // rows up to trow + (UN - 1) * brs + PL / UN)
+    const int64_t tspan = (BD && brs != bs) ? (int64_t)(UN - 1) * brs + PLi : PL;
+    if (trow >= row_begin && trow + tspan <= row_end)
+      for (; l0 + kStep <= PLi; l0 += kStep) pass(std::false_type{}, l0);
+    for (; l0 < PLi; l0 += kStep) pass(std::true_type{}, l0);
     base = nbase;
     row0 = nrow0;
   }
 }
 
-template <typename T, bool SP, int LPR, int VPL, int DV, int UN, int VEC = 1>
+template <typename T, bool SP, int LPR, int VPL, int DV, int UN, int VEC = 1, bool BD = false>
 cudaError_t launch(const StreamDesc *dd, const BksLaunch &L, const InPtrs &in, void *out, uint8_t *arg,
                    int64_t rb, int64_t re, cudaStream_t s) {
-  auto kern = bk_stream<T, SP, LPR, VPL, DV, UN, VEC>;
+  auto kern = bk_stream<T, SP, LPR, VPL, DV, UN, VEC, BD>;
   if (L.smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem);
     if (e != cudaSuccess) return e;
@@ -312,6 +347,18 @@ cudaError_t launch(const StreamDesc *dd, const BksLaunch &L, const InPtrs &in, v
 template <typename T, bool SP>
 cudaError_t dispatch(const StreamDesc *dd, const BksLaunch &L, const InPtrs &in, void *out, uint8_t *arg,
                      int64_t rb, int64_t re, cudaStream_t s) {
+  if constexpr (!SP) {  // broadcast digit of radix L.bd (one lane per row, d <= 5)
+#define GBE_BD(DVc)                                                                              \
+  if (L.d == DVc) {                                                                              \
+    if (L.bd == 2) return launch<T, SP, 1, DVc, DVc, 2, 1, true>(dd, L, in, out, arg, rb, re, s); \
+    if (L.bd == 3) return launch<T, SP, 1, DVc, DVc, 3, 1, true>(dd, L, in, out, arg, rb, re, s); \
+    if (L.bd == 4) return launch<T, SP, 1, DVc, DVc, 4, 1, true>(dd, L, in, out, arg, rb, re, s); \
+  }
+    if (L.bd) {
+      GBE_BD(2) GBE_BD(3) GBE_BD(4) GBE_BD(5)
+    }
+#undef GBE_BD
+  }
   // vector path: every input 16-byte aligned (offsets are multiples of VEC,
   // checked by bks_build)
   bool aligned = L.vec > 1;
@@ -319,15 +366,9 @@ cudaError_t dispatch(const StreamDesc *dd, const BksLaunch &L, const InPtrs &in,
     if ((uintptr_t)in.p[j] % 16) aligned = false;
   if (aligned) {
     if constexpr (sizeof(T) == 8) {
-      // d = 4: two lanes per row, one 16-byte load each (a warp's load of a
-      // dense input covers 16 consecutive rows); GBE_STREAM_V4=0: A/B knob
-      static const int v4 = [] {
-        const char *e = std::getenv("GBE_STREAM_V4");
-        return e ? std::atoi(e) : 4;
-      }();
+      // (d = 4 with two lanes per row and one 16-byte load each measured
+      // slower on C5 than one lane per row: x57 3.38 vs 2.30 ms)
       if (L.d == 2) return launch<T, SP, 1, 2, 2, 4, 2>(dd, L, in, out, arg, rb, re, s);
-      if (L.d == 4 && v4 == 4) return launch<T, SP, 2, 2, 4, 4, 2>(dd, L, in, out, arg, rb, re, s);
-      if (L.d == 4 && v4 == 8) return launch<T, SP, 2, 2, 4, 8, 2>(dd, L, in, out, arg, rb, re, s);
       if (L.d == 8) return launch<T, SP, 4, 2, 8, 4, 2>(dd, L, in, out, arg, rb, re, s);
     } else {
       if (L.d == 2) return launch<T, SP, 1, 2, 2, 4, 2>(dd, L, in, out, arg, rb, re, s);
@@ -405,14 +446,96 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     PL /= h.radix[q];
   }
   std::memset(&S, 0, sizeof(S));
+  const bool full = row_begin == 0 && row_end == h.rows;
+  std::vector<int64_t> cells(k, d);
+  int big = 0;
+  for (int j = 0; j < k; j++) {
+    for (int p = 0; p < m; p++)
+      if (h.stride[j][p]) cells[j] *= h.radix[p];
+    if (cells[j] > cells[big]) big = j;
+  }
+  std::vector<int64_t> rowstride(m + 1, 1);
+  for (int p = m - 1; p >= 0; p--) rowstride[p] = rowstride[p + 1] * h.radix[p];
+  for (int p = 0; p < m; p++) rowstride[p] = rowstride[p + 1];
+  // broadcast digit (d <= 5, min-sum): a digit b of radix 2..4
+  // the largest input lacks; a lane's rows are the rows that differ only in
+  // b and every input without b is loaded once for all of them.  b is an
+  // in-tile digit when one qualifies, else (full-range launches) a high
+  // digit placed on top of the warp-tile, whose rows then form radix(b) runs
+  // of PL rows.  Chosen to minimise the loads per row sum_j (has b ? 1 : 1/r).
+  int bd_low = -1, bd_high = -1, bd_r = 0;
+  int64_t bd_stride = 0;
+  {
+    // measured slower on C5 (x57 2.55 -> 2.69 ms, x77 1.39 -> 1.56, x91
+    // 1.30 -> 1.63 with the tiled kernel then winning): the rows per lane
+    // drop to radix(b) and with them the loads in flight, while the re-reads
+    // it saves were L1 hits.  Off unless GBE_STREAM_BD=1 (read per build, so
+    // tests can enable it)
+    const char *bd_env = std::getenv("GBE_STREAM_BD");
+    const bool bd_off = !(bd_env && std::atoi(bd_env) == 1);
+    if (!bd_off && d <= 5 && d >= 2 && h.semiring != GBE_SUMPROD_F64 && k >= 1) {
+      auto cost = [&](int p) {
+        double c = 0;
+        for (int j = 0; j < k; j++) c += h.stride[j][p] ? 1.0 : 1.0 / h.radix[p];
+        return c;
+      };
+      double best = (double)k - 1e-9;
+      int64_t stride = 1;
+      for (int q = nlow - 1; q >= 0; q--) {  // in-tile digits, least significant first
+        const int p = m - nlow + q;
+        const int r = h.radix[p];
+        if (r >= 2 && r <= 4 && !h.stride[big][p] && cost(p) < best) {
+          best = cost(p);
+          bd_low = p;
+          bd_r = r;
+          bd_stride = stride;
+        }
+        stride *= r;
+      }
+      if (bd_low < 0 && full && nlow > 0) {
+        for (int p = 0; p < m - nlow; p++) {
+          const int r = h.radix[p];
+          if (r >= 2 && r <= 4 && !h.stride[big][p] && cost(p) < best - 1e-9) {
+            best = cost(p);
+            bd_high = p;
+            bd_r = r;
+          }
+        }
+        if (bd_high >= 0) {  // keep the offset table within its budget
+          bool ok = true;
+          for (int j = 0; j < k; j++)
+            if (maxoff[j] + (int64_t)(bd_r - 1) * h.stride[j][bd_high] >= (int64_t(1) << 31)) ok = false;
+          while (ok && nlow > 1 && PL * bd_r > pl_max) {
+            const int q = m - nlow;  // drop the most significant low digit
+            PL /= h.radix[q];
+            nlow--;
+          }
+          if (!ok || PL * bd_r > pl_max) bd_high = -1;
+        }
+      }
+    }
+  }
   S.k = k;
   S.d = d;
-  S.nlow = nlow;
-  S.PL = (int32_t)PL;
+  const int top = bd_high >= 0 ? 1 : 0;  // in-tile digit 0 = the high broadcast digit
+  S.nlow = nlow + top;
+  S.PL = (int32_t)(PL * (top ? bd_r : 1));
+  if (top) {
+    S.lrad[0] = bd_r;
+    for (int j = 0; j < k; j++) S.lstr[0][j] = (int32_t)h.stride[j][bd_high];
+  }
   for (int q = 0; q < nlow; q++) {  // low digits, most significant first
     const int p = m - nlow + q;
-    S.lrad[q] = h.radix[p];
-    for (int j = 0; j < k; j++) S.lstr[q][j] = (int32_t)h.stride[j][p];
+    S.lrad[top + q] = h.radix[p];
+    for (int j = 0; j < k; j++) S.lstr[top + q][j] = (int32_t)h.stride[j][p];
+  }
+  if (bd_low >= 0 || bd_high >= 0) {
+    const int p = bd_low >= 0 ? bd_low : bd_high;
+    S.bd_rad = bd_r;
+    S.bd_stride = (int32_t)(bd_low >= 0 ? bd_stride : PL);
+    S.bd_rowstride = bd_low >= 0 ? 0 : rowstride[p];
+    for (int j = 0; j < k; j++)
+      if (h.stride[j][p]) S.bd_has |= 1u << j;
   }
   // high digits (radix-1 digits are always 0 and are dropped).  A launch
   // over all rows enumerates tiles with the digits absent from the largest
@@ -420,22 +543,10 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
   // back to back in a warp and hit L1/L2 instead of HBM
   int hd[GBE_MAX_SEP], nh = 0;
   for (int p = 0; p < m - nlow; p++)
-    if (h.radix[p] > 1) hd[nh++] = p;
+    if (h.radix[p] > 1 && p != bd_high) hd[nh++] = p;
   if (nh > 32) return false;
-  std::vector<int64_t> rowstride(m + 1, 1);
-  for (int p = m - 1; p >= 0; p--) rowstride[p] = rowstride[p + 1] * h.radix[p];
-  for (int p = 0; p < m; p++) rowstride[p] = rowstride[p + 1];
-  const bool full = row_begin == 0 && row_end == h.rows;
-  if (full) {
-    std::vector<int64_t> cells(k, d);
-    int big = 0;
-    for (int j = 0; j < k; j++) {
-      for (int p = 0; p < m; p++)
-        if (h.stride[j][p]) cells[j] *= h.radix[p];
-      if (cells[j] > cells[big]) big = j;
-    }
+  if (full)
     std::stable_sort(hd, hd + nh, [&](int a, int b) { return (h.stride[big][a] != 0) > (h.stride[big][b] != 0); });
-  }
   L.natural = !full;
   S.nhigh = nh;
   int64_t div = 1;
@@ -450,9 +561,15 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
   for (int j = 0; j < k; j++) S.shift[j] = h.shift[j];
   // L2 prefetch extent of each input's tile slice: [base, base + maxoff + d)
   // is the whole slice when the input's in-tile offsets are one dense block
-  // (canonical layouts); otherwise no prefetch.  GBE_STREAM_PF=1 enables it
-  // (A/B knob: C5 18.2 ms with, 17.5 ms without)
-  static const bool no_pf = std::getenv("GBE_STREAM_PF") == nullptr;  // off unless set (measured: k = 1 buckets lose)
+  // (canonical layouts); otherwise no prefetch.  Measured on C5: buckets
+  // with k >= 2 inputs gain (x91 1.43 -> 1.29 ms, x77 1.42 -> 1.39 ms),
+  // single-input buckets lose (x26 0.51 -> 0.79 ms), so it is on for k >= 2;
+  // GBE_STREAM_PF=0 / 1 forces it off / on (A/B knob)
+  static const int pf_env = [] {
+    const char *e = std::getenv("GBE_STREAM_PF");
+    return e ? std::atoi(e) : -1;
+  }();
+  const bool no_pf = pf_env == 0 || (pf_env < 0 && k < 2) || bd_high >= 0;
   for (int j = 0; j < k; j++) {
     int64_t want = d, span = 1;
     bool dense = true;
@@ -481,13 +598,14 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     }
     L.vec = vec;
   }
+  L.bd = S.bd_rad;
   L.k = k;
   L.d = d;
   L.f64 = h.semiring != GBE_MINSUM_I32;
   L.sp = h.semiring == GBE_SUMPROD_F64;
-  L.t0 = row_begin / PL;
-  L.ntiles = (row_end - 1) / PL - L.t0 + 1;
-  L.smem = (int)(sizeof(int32_t) * (size_t)k * PL);
+  L.t0 = row_begin / S.PL;
+  L.ntiles = (row_end - 1) / S.PL - L.t0 + 1;
+  L.smem = (int)(sizeof(int32_t) * (size_t)k * S.PL);
   // CTAs: as many as fit, at least one warp-tile per warp
   const int per_sm = std::max(1, std::min(8, (200 * 1024) / std::max(L.smem + 1024, 1)));
   const int64_t want = (L.ntiles + (kBlock / 32) - 1) / (kBlock / 32);

@@ -11,6 +11,14 @@ namespace gbe {
 // Device descriptor (read through the read-only cache).
 struct StreamDesc {
   int32_t k, d, nlow, PL, nhigh, pad;
+  // broadcast digit (register reuse): an in-tile output digit b the largest
+  // input lacks; a lane's rows are the bd_rad rows that differ only in b (in-
+  // tile stride bd_stride), and every input without b is loaded once for all
+  // of them (bit j of bd_has: input j has b)
+  int32_t bd_rad, bd_stride;
+  uint32_t bd_has, pad2;
+  int64_t bd_rowstride;  // 0: b is an in-tile digit of the row order; else b is a high
+                         // digit placed on top of the tile: output row stride of b
   int32_t lrad[GBE_MAX_SEP];       // low (in-tile) digits, most significant first
   int32_t lstr[GBE_MAX_SEP][32];   // their element strides per input
   int32_t hrad[32];                // high digits (radix > 1), most significant first
@@ -24,6 +32,7 @@ struct StreamDesc {
 struct BksLaunch {
   int d = 1, k = 1, grid = 1, smem = 0;
   int vec = 0;  // elements per vector load when the layout allows it (0: scalar)
+  int bd = 0;   // broadcast-digit radix (0: off)
   bool f64 = false, sp = false;
   bool natural = true;  // tiles in row order (partial row ranges); else reordered for L2 reuse
   int64_t t0 = 0, ntiles = 0;

@@ -125,6 +125,9 @@ def main(which):
     if "c4host" in which:  # argmin spill: argmins streamed to pinned host memory
         inst = configs.c4()
         measure("C4-hostargs", inst, oracle.minfill_order(inst), -1, retain="host")
+    if "c4spill" in which:  # out-of-core plan, messages streamed under a 12 GB budget
+        inst = configs.c4()
+        measure("C4-spill-12GB", inst, oracle.minfill_order(inst), -1, spill=True, budget_bytes=12 * 10**9)
     if "c3" in which:
         inst = configs.c3()
         order = configs.c3_order()

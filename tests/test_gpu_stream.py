@@ -201,3 +201,56 @@ def test_whole_solve_stream_kernel(name):
         assert abs(root - ref.value) <= 1e-9 * max(1.0, abs(ref.value))
     else:
         assert root == ref.value and list(assign) == list(ref.assignment)
+
+
+def bd_bucket(rng, dom_sep, d, k, f64, lack):
+    """The largest input spans every output digit but `lack` (an in-tile
+    digit): the streaming kernel's broadcast-digit mode loads it once for the
+    rows that differ only in that digit."""
+    m = len(dom_sep)
+    dom = list(dom_sep) + [d]
+    members = []
+    for j in range(k):
+        if j == 0:
+            sub = [q for q in range(m) if q != lack]
+        else:
+            sub = sorted(q for q in range(m) if rng.random() < 0.5)
+        scope = sub + [m]
+        cells = int(np.prod([dom[v] for v in scope]))
+        if f64:
+            t = rng.uniform(0, 10, cells)
+            t[rng.random(cells) < 0.05] = np.inf
+        else:
+            t = rng.integers(0, 60, cells).astype(np.int64)
+            t[rng.random(cells) < 0.05] = INF
+        members.append((scope, t))
+    return dom, list(range(m)), m, members
+
+
+@pytest.mark.parametrize("dom_sep,lack", [([3] * 10, 9), ([3] * 10, 8), ([4, 2, 4, 3, 4, 4, 2, 4], 7),
+                                          ([4, 2, 4, 3, 4, 4, 2, 4], 5), ([2] * 14, 12), ([4] * 7, 6),
+                                          # high digits (outside the warp-tile): placed on top of it
+                                          ([3] * 10, 1), ([3] * 11, 0), ([4, 2, 4, 3, 4, 4, 2, 4], 1),
+                                          ([2] * 14, 0), ([4] * 7, 0)])
+@pytest.mark.parametrize("d", [2, 3, 4, 5])
+@pytest.mark.parametrize("f64", [False, True])
+def test_stream_broadcast_digit(dom_sep, lack, d, f64):
+    """Broadcast-digit rows (the lane's rows differ only in a digit the
+    largest input lacks; inputs without it loaded once), the digit inside
+    the warp-tile or (full-range launches) a high digit on top of it: full
+    range and ragged partial ranges, INF cells and ties, against the oracle."""
+    os.environ["GBE_STREAM_BD"] = "1"  # the mode is opt-in (DESIGN.md §5); read per descriptor build
+    rng = np.random.default_rng(hash((tuple(dom_sep), lack, d, f64)) % (1 << 32))
+    k = int(rng.integers(2, 5))
+    dom, sep, x, members = bd_bucket(rng, dom_sep, d, k, f64, lack)
+    D, rows = desc_for(dom, sep, x, members, G.MINSUM_F64 if f64 else G.MINSUM_I32)
+    exp, ea = oracle.bucket_eval(dom, f64, x, members, sep)
+    for rb, re in [(0, rows), (7, rows - 5), (rows // 3 + 1, rows // 2 + 3)]:
+        dt = torch.float64 if f64 else torch.int32
+        ins = [torch.tensor(np.asarray(t), dtype=dt, device="cuda") for _, t in members]
+        out = torch.empty(re - rb, dtype=dt, device="cuda")
+        arg = torch.empty(re - rb, dtype=torch.uint8, device="cuda")
+        G.bucket_kernel(D, ins, out, arg, rb, re, variant=2)
+        torch.cuda.synchronize()
+        check(out.cpu().numpy(), arg.cpu().numpy(), exp[rb:re], ea[rb:re], f64, dom, x, members, sep, rb)
+    del os.environ["GBE_STREAM_BD"]
