@@ -146,8 +146,21 @@ gbe_status gbe_pseudotree(const gbe_problem *p, const int32_t *order,
  *    "shard_min_rows":N, "retain":"none"|"args"|"all"|"host", "timing":true,
  *    "kernel":-1|0|1|2, "autotune":true, "resident_inputs":false, "graph":true, "concurrent":true,
  *    "semiring":"minsum"|"sumprod", "count":"none"|"optimal"|"consistent",
- *    "host_arg_chunk":N}
+ *    "host_arg_chunk":N, "spill":false, "stage_bytes":N}
  * "retain":"all" keeps every table on the device for gbe_run_table().
+ * "spill":true (exact BE / DPOP, one rank, no "count"; needs "budget_bytes"
+ * > 0; else GBE_E_INVALID) makes an out-of-core plan (SURVEY §8(f) row 2,
+ * the chunked host<->device pipeline of Fig. 8): while the
+ * device peak plus the staging budget ("stage_bytes", default budget / 4
+ * clamped to [16 MB, 4 GB]; two slots of half of it) exceeds the budget, the
+ * largest remaining message moves to pinned host memory; every bucket then
+ * runs in row chunks (runs of whole blocks of its leading output digits)
+ * whose host-resident input slices are copied into a slot on an H2D stream
+ * while a D2H stream copies the previous chunk's rows and argmins out.
+ * Argmins go to host memory ("retain":"args"), or nowhere ("none").
+ * gbe_run_table() reads host messages from host memory.  A budget no
+ * chunking meets is GBE_E_BUDGET naming the largest bucket.  Eager (no
+ * CUDA-graph replay).
  * "retain":"host" (exact BE / DPOP, one rank, min-sum; else GBE_E_INVALID)
  * puts the argmin tables in pinned host memory: buckets run in row chunks of
  * "host_arg_chunk" rows (default 2^28) whose argmins stream out through a

@@ -1017,7 +1017,7 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     for (int p = 0; p < m - nl; p++) hd.push_back(p);
     const bool full = row_begin == 0 && row_end == h.rows;
     if (full)
-      std::stable_sort(hd.begin(), hd.end(), [&](int a, int b) { return has(big, a) > has(big, b); });
+      order_high_digits(h, hd.data(), (int)hd.size());
     f.nH = (int32_t)hd.size();
     if (f.nH > 31) continue;
     int64_t div = 1;

@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
   };
   constexpr int G = 32 / LPR;  // row groups per pass
   const int grp = lane / LPR, sub = lane % LPR;
-  static_assert(VEC == 1 || (VPL == VEC && DV == LPR * VEC), "vector path: one vector per lane, exact d");
+  static_assert(VEC == 1 || (VPL % VEC == 0 && DV == LPR * VPL), "vector path: whole vectors per lane, exact d");
   static_assert(!BD || (LPR == 1 && VEC == 1), "broadcast digit: one lane per row, scalar loads");
   // broadcast digit: pass rows are i = l0 + grp (i < PL / UN enumerates the
   // rows whose digit b is 0) and the lane's UN rows lb(i) + u * bs
@@ -170,13 +170,13 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
   const int64_t brs = BD ? (D->bd_rowstride ? D->bd_rowstride : (int64_t)bs) : 0;  // output-row stride of b
   const int PLi = BD ? PL / UN : PL;
   // value index of this lane's i-th value
-  auto vix = [&](int i) { return VEC > 1 ? sub * VEC + i : sub + i * LPR; };
+  auto vix = [&](int i) { return VEC > 1 ? sub * VPL + i : sub + i * LPR; };
   // inputs in chunks of KU: every load of a chunk is issued before the
   // first add (the adds keep the input order), so a lane has KU * UN * VPL
   // loads in flight instead of one input's worth per round trip
   constexpr int kLaneBytes = UN * VPL * (int)sizeof(T);
   constexpr int KU = kLaneBytes <= 32 ? 2 : 1;
-  const int lane_off = VEC > 1 ? sub * VEC : sub;
+  const int lane_off = VEC > 1 ? sub * VPL : sub;
   const T *pb[KU];  // this tile's first KU input pointers (hoisted per tile)
   int64_t trow = 0;
   // one pass = UN row groups of this warp (rows l0 + u * G + grp of the
@@ -239,7 +239,8 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
           }
           const T *q = pj + lo[lrow[u]];
           if constexpr (VEC > 1) {
-            VecLd<T, VEC>::ld(q, dst);
+#pragma unroll
+            for (int i = 0; i < VPL; i += VEC) VecLd<T, VEC>::ld(q + i, dst + i);
           } else {
 #pragma unroll
             for (int i = 0; i < VPL; i++)
@@ -368,7 +369,13 @@ cudaError_t dispatch(const StreamDesc *dd, const BksLaunch &L, const InPtrs &in,
     if constexpr (sizeof(T) == 8) {
       // (d = 4 with two lanes per row and one 16-byte load each measured
       // slower on C5 than one lane per row: x57 3.38 vs 2.30 ms)
+      // d = 4: one lane per row, two 16-byte loads (GBE_STREAM_V4=0: scalar, A/B knob)
+      static const bool v4 = [] {
+        const char *e = std::getenv("GBE_STREAM_V4");
+        return !(e && std::atoi(e) == 0);
+      }();
       if (L.d == 2) return launch<T, SP, 1, 2, 2, 4, 2>(dd, L, in, out, arg, rb, re, s);
+      if (L.d == 4 && v4) return launch<T, SP, 1, 4, 4, 4, 2>(dd, L, in, out, arg, rb, re, s);
       if (L.d == 8) return launch<T, SP, 4, 2, 8, 4, 2>(dd, L, in, out, arg, rb, re, s);
     } else {
       if (L.d == 2) return launch<T, SP, 1, 2, 2, 4, 2>(dd, L, in, out, arg, rb, re, s);
@@ -546,7 +553,7 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     if (h.radix[p] > 1 && p != bd_high) hd[nh++] = p;
   if (nh > 32) return false;
   if (full)
-    std::stable_sort(hd, hd + nh, [&](int a, int b) { return (h.stride[big][a] != 0) > (h.stride[big][b] != 0); });
+    order_high_digits(h, hd, nh);
   L.natural = !full;
   S.nhigh = nh;
   int64_t div = 1;

@@ -2,7 +2,10 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <utility>
+#include <vector>
 
 #include "gbe.h"
 
@@ -39,6 +42,34 @@ struct VTerm {
 
 // Kernel variants for the fused aggregate+project bucket kernel (BK)
 enum BkVariant { BK_AUTO = -1, BK_GENERIC = 0 };
+
+// Tile enumeration order of a full-range launch (host): the high output
+// digits p[0..n) are reordered so that the digits an input lacks vary
+// fastest, the largest input first: tiles that re-read one slice of an input
+// run back to back, so its re-reads hit L2 instead of HBM.  Lexicographic
+// over the inputs by decreasing size (a digit the largest input lacks goes
+// after one it has; ties by the next input; stable), so a bucket with
+// several large inputs that lack different digits gets L2 reuse for all of
+// them (with only the largest input's digits moved, C4-d4's x0 re-read its
+// two other 1e9-cell inputs from HBM 16-64 times).
+inline void order_high_digits(const gbe_bucket_desc &h, int *p, int n) {
+  const int k = h.ninputs, m = h.nsep;
+  std::vector<std::pair<double, int>> by;
+  for (int j = 0; j < k; j++) {
+    double c = h.d;
+    for (int q = 0; q < m; q++)
+      if (h.stride[j][q]) c *= h.radix[q];
+    by.push_back({-c, j});
+  }
+  std::stable_sort(by.begin(), by.end());
+  std::stable_sort(p, p + n, [&](int a, int b) {
+    for (auto &e : by) {
+      const bool la = h.stride[e.second][a] == 0, lb = h.stride[e.second][b] == 0;
+      if (la != lb) return lb;  // a before b when only b is lacked (b varies faster)
+    }
+    return false;
+  });
+}
 
 // Describes how the launcher tiles one bucket (computed on the host from the
 // descriptor; see kernels.cu).
