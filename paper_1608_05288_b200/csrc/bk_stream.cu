@@ -109,7 +109,7 @@ struct VecLd<int32_t, 2> {
   }
 };
 
-template <typename T, bool SP, int LPR, int VPL, int DV, int UN, int VEC = 1, bool BD = false>
+template <typename T, bool SP, int LPR, int VPL, int DV, int UN, int VEC = 1, bool BD = false, bool HX = false>
 __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restrict__ D, InPtrs in,
                                                     T *__restrict__ out, uint8_t *__restrict__ arg,
                                                     int64_t row_begin, int64_t row_end, int64_t t0,
@@ -129,6 +129,20 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
     }
     loff[idx] = o;
   }
+  // blocked high digits: output-row offset of every in-tile row
+  constexpr bool hxt = HX;
+  int64_t *rowoff = (int64_t *)(loff + ((k * PL + 1) & ~1));
+  if constexpr (HX)
+    for (int l0 = threadIdx.x; l0 < PL; l0 += blockDim.x) {
+      int l = l0;
+      int64_t o = 0;
+      for (int q = nlow - 1; q >= 0; q--) {
+        const int r = D->lrad[q];
+        o += (int64_t)(l % r) * D->lrowst[q];
+        l /= r;
+      }
+      rowoff[l0] = o;
+    }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -185,25 +199,27 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
     constexpr bool MASK = decltype(maskc)::value;
     Acc acc[UN][VPL];
     bool valid[UN];
-    int lrow[UN];      // in-tile row (offset-table index) of each of this lane's UN rows
-    int64_t grow[UN];  // its output row relative to the tile's first row
+    int lrow[UN];  // in-tile row (offset-table index) of each of this lane's UN rows
+    [[maybe_unused]] int lb = 0;
     if constexpr (BD) {
       const int i = l0 + grp;
-      const int lb = (i / bs) * bs * UN + i % bs;
+      lb = (i / bs) * bs * UN + i % bs;
 #pragma unroll
-      for (int u = 0; u < UN; u++) {
-        lrow[u] = lb + u * bs;
-        grow[u] = lb + u * brs;
-      }
+      for (int u = 0; u < UN; u++) lrow[u] = lb + u * bs;
     } else {
 #pragma unroll
-      for (int u = 0; u < UN; u++) grow[u] = lrow[u] = l0 + u * G + grp;
+      for (int u = 0; u < UN; u++) lrow[u] = l0 + u * G + grp;
     }
+    // output row of row u relative to the tile's first row (formed where used)
+    auto grow = [&](int u) -> int64_t {
+      if constexpr (BD) return lb + u * brs;
+      return (hxt && lrow[u] < PL) ? rowoff[lrow[u]] : (int64_t)lrow[u];
+    };
 #pragma unroll
     for (int u = 0; u < UN; u++) {
       if constexpr (MASK) {
         const int l = lrow[u];
-        const int64_t r = trow + grow[u];
+        const int64_t r = trow + grow(u);
         valid[u] = (BD ? l0 + grp < PLi : l < PL) && r >= row_begin && r < row_end;
       } else {
         valid[u] = true;
@@ -294,7 +310,7 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
         bv = 0;
       }
       if (sub == 0 && (!MASK || valid[u])) {
-        const int64_t r = trow + grow[u] - row_begin;
+        const int64_t r = trow + grow(u) - row_begin;
         out[r] = S::out(best);
         if (arg) arg[r] = (uint8_t)bv;
       }
@@ -324,7 +340,7 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
     constexpr int kStep = BD ? G : G * UN;  // pass rows (BD: rows with digit b = 0)
     // whole tile: unmasked passes (a tile with a high broadcast digit spans
     // rows up to trow + (UN - 1) * brs + PL / UN)
-    const int64_t tspan = (BD && brs != bs) ? (int64_t)(UN - 1) * brs + PLi : PL;
+    const int64_t tspan = (BD && brs != bs) ? (int64_t)(UN - 1) * brs + PLi : (hxt ? int64_t(0) : (int64_t)PL);
     if (trow >= row_begin && trow + tspan <= row_end)
       for (; l0 + kStep <= PLi; l0 += kStep) pass(std::false_type{}, l0);
     for (; l0 < PLi; l0 += kStep) pass(std::true_type{}, l0);
@@ -333,10 +349,10 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
   }
 }
 
-template <typename T, bool SP, int LPR, int VPL, int DV, int UN, int VEC = 1, bool BD = false>
+template <typename T, bool SP, int LPR, int VPL, int DV, int UN, int VEC = 1, bool BD = false, bool HX = false>
 cudaError_t launch(const StreamDesc *dd, const BksLaunch &L, const InPtrs &in, void *out, uint8_t *arg,
                    int64_t rb, int64_t re, cudaStream_t s) {
-  auto kern = bk_stream<T, SP, LPR, VPL, DV, UN, VEC, BD>;
+  auto kern = bk_stream<T, SP, LPR, VPL, DV, UN, VEC, BD, HX>;
   if (L.smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem);
     if (e != cudaSuccess) return e;
@@ -348,6 +364,25 @@ cudaError_t launch(const StreamDesc *dd, const BksLaunch &L, const InPtrs &in, v
 template <typename T, bool SP>
 cudaError_t dispatch(const StreamDesc *dd, const BksLaunch &L, const InPtrs &in, void *out, uint8_t *arg,
                      int64_t rb, int64_t re, cudaStream_t s) {
+  if constexpr (!SP) {  // blocked high digits (full-range launches, d <= 5, min-sum)
+    if (L.hx) {
+      bool al = true;
+      for (int j = 0; j < L.k; j++)
+        if ((uintptr_t)in.p[j] % 16) al = false;
+      if constexpr (sizeof(T) == 4) {
+        if (L.d == 4 && L.vec == 4 && al) return launch<T, SP, 1, 4, 4, 4, 4, false, true>(dd, L, in, out, arg, rb, re, s);
+      } else {
+        if (L.d == 4 && L.vec == 2 && al) return launch<T, SP, 1, 4, 4, 4, 2, false, true>(dd, L, in, out, arg, rb, re, s);
+      }
+      switch (L.d) {
+        case 2: return launch<T, SP, 1, 2, 2, sizeof(T) == 8 ? 4 : 8, 1, false, true>(dd, L, in, out, arg, rb, re, s);
+        case 3: return launch<T, SP, 1, 3, 3, sizeof(T) == 8 ? 4 : 8, 1, false, true>(dd, L, in, out, arg, rb, re, s);
+        case 4: return launch<T, SP, 1, 4, 4, 4, 1, false, true>(dd, L, in, out, arg, rb, re, s);
+        case 5: return launch<T, SP, 1, 5, 5, sizeof(T) == 8 ? 2 : 4, 1, false, true>(dd, L, in, out, arg, rb, re, s);
+        default: return cudaErrorInvalidValue;
+      }
+    }
+  }
   if constexpr (!SP) {  // broadcast digit of radix L.bd (one lane per row, d <= 5)
 #define GBE_BD(DVc)                                                                              \
   if (L.d == DVc) {                                                                              \
@@ -393,8 +428,8 @@ cudaError_t dispatch(const StreamDesc *dd, const BksLaunch &L, const InPtrs &in,
   {                                                                                              \
     const int u = un ? un : (UNdef);                                                             \
     if (u <= 2) return launch<T, SP, 1, DVc, DVc, 2>(dd, L, in, out, arg, rb, re, s);            \
-    if (u <= 4) return launch<T, SP, 1, DVc, DVc, 4>(dd, L, in, out, arg, rb, re, s);            \
-    return launch<T, SP, 1, DVc, DVc, 8>(dd, L, in, out, arg, rb, re, s);                        \
+    if (u <= 4 || F) return launch<T, SP, 1, DVc, DVc, 4>(dd, L, in, out, arg, rb, re, s);       \
+    if constexpr (!F) return launch<T, SP, 1, DVc, DVc, 8>(dd, L, in, out, arg, rb, re, s);      \
   }
   switch (L.d) {
     case 1: GBE_UN(1, 8)
@@ -405,12 +440,31 @@ cudaError_t dispatch(const StreamDesc *dd, const BksLaunch &L, const InPtrs &in,
     default: break;
   }
 #undef GBE_UN
+  // large domains: rows per lane per pass (GBE_STREAM_UNL: tuning knob; the
+  // lanes of a row reduce with shuffles, so several rows per pass overlap
+  // their loads and reduction chains)
+  static const int unl = [] {
+    const char *e = std::getenv("GBE_STREAM_UNL");
+    return e ? std::atoi(e) : 0;
+  }();
   if (L.d <= 8) return launch<T, SP, 2, 4, 0, 2>(dd, L, in, out, arg, rb, re, s);
   if (L.d <= 16) return launch<T, SP, 4, 4, 0, 2>(dd, L, in, out, arg, rb, re, s);
-  if (L.d <= 32) return launch<T, SP, 8, 4, 0, 2>(dd, L, in, out, arg, rb, re, s);
-  if (L.d <= 64) return launch<T, SP, 16, 4, 0, 1>(dd, L, in, out, arg, rb, re, s);
-  if (L.d <= 128) return launch<T, SP, 32, 4, 0, 1>(dd, L, in, out, arg, rb, re, s);
-  return launch<T, SP, 32, 8, 0, 1>(dd, L, in, out, arg, rb, re, s);
+  constexpr int UL = F ? 2 : 4;  // (f64 with 4 rows per lane spills at the 128-register cap)
+  if (L.d <= 32) return launch<T, SP, 8, 4, 0, 2>(dd, L, in, out, arg, rb, re, s);  // (4 rows: d = 25 slower)
+  if (L.d <= 64) {
+    if (unl == 1) return launch<T, SP, 16, 4, 0, 1>(dd, L, in, out, arg, rb, re, s);
+    return launch<T, SP, 16, 4, 0, UL>(dd, L, in, out, arg, rb, re, s);
+  }
+  if (L.d <= 128) {
+    if (unl == 1) return launch<T, SP, 32, 4, 0, 1>(dd, L, in, out, arg, rb, re, s);
+    return launch<T, SP, 32, 4, 0, UL>(dd, L, in, out, arg, rb, re, s);
+  }
+  if constexpr (F) {
+    return launch<T, SP, 32, 8, 0, 1>(dd, L, in, out, arg, rb, re, s);
+  } else {
+    if (unl == 1) return launch<T, SP, 32, 8, 0, 1>(dd, L, in, out, arg, rb, re, s);
+    return launch<T, SP, 32, 8, 0, 2>(dd, L, in, out, arg, rb, re, s);
+  }
 }
 
 }  // namespace
@@ -470,9 +524,59 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
   // in-tile digit when one qualifies, else (full-range launches) a high
   // digit placed on top of the warp-tile, whose rows then form radix(b) runs
   // of PL rows.  Chosen to minimise the loads per row sum_j (has b ? 1 : 1/r).
+  // blocked high digits (full-range launches): inputs of >= 16 MB that are
+  // not the two largest have their re-use served inside a tile -- the high
+  // digits they lack go on top of the warp-tile (the tile order serves the
+  // two largest inputs through L2).  A bucket with three large inputs that
+  // lack different digits (C4-d4's 4^16-row bucket) otherwise re-reads the
+  // third from HBM once per combination of its absent digits.
+  std::vector<int> hxd;
+  int64_t hxprod = 1;
+  {
+    const char *e = std::getenv("GBE_STREAM_HX");  // A/B knob (0: off)
+    const bool hx_off = (e && std::atoi(e) == 0) || d > 5 || d < 2 || h.semiring == GBE_SUMPROD_F64;
+    const double es = h.semiring == GBE_MINSUM_I32 ? 4.0 : 8.0;
+    std::vector<std::pair<double, int>> large;
+    for (int j = 0; j < k; j++)
+      if (cells[j] * es >= 16.0 * (1 << 20)) large.push_back({-(double)cells[j], j});
+    std::stable_sort(large.begin(), large.end());
+    for (size_t r = 2; full && !hx_off && r < large.size(); r++) {
+      const int j = large[r].second;
+      std::vector<int> cand;
+      int64_t prod = 1;
+      for (int p = 0; p < m - nlow; p++)
+        if (h.radix[p] > 1 && !h.stride[j][p] && std::find(hxd.begin(), hxd.end(), p) == hxd.end()) {
+          cand.push_back(p);
+          prod *= h.radix[p];
+        }
+      if (cand.empty()) continue;
+      // room: drop low digits (keeping >= 16 contiguous rows) until it fits
+      int nl = nlow;
+      int64_t pl = PL;
+      while (pl * hxprod * prod > pl_max && nl > 1 && pl / h.radix[m - nl] >= 16) {
+        pl /= h.radix[m - nl];
+        nl--;
+      }
+      if (pl * hxprod * prod > pl_max) continue;
+      bool fits = true;  // in-tile offsets stay int32
+      for (int jj = 0; jj < k; jj++) {
+        int64_t mo = 0;
+        for (int q = m - nl; q < m; q++) mo += (int64_t)(h.radix[q] - 1) * h.stride[jj][q];
+        for (int p : hxd) mo += (int64_t)(h.radix[p] - 1) * h.stride[jj][p];
+        for (int p : cand) mo += (int64_t)(h.radix[p] - 1) * h.stride[jj][p];
+        if (mo >= (int64_t(1) << 31)) fits = false;
+      }
+      if (!fits) continue;
+      nlow = nl;
+      PL = pl;
+      hxd.insert(hxd.end(), cand.begin(), cand.end());
+      hxprod *= prod;
+    }
+    std::sort(hxd.begin(), hxd.end());  // most significant first
+  }
   int bd_low = -1, bd_high = -1, bd_r = 0;
   int64_t bd_stride = 0;
-  {
+  if (hxd.empty()) {
     // measured slower on C5 (x57 2.55 -> 2.69 ms, x77 1.39 -> 1.56, x91
     // 1.30 -> 1.63 with the tiled kernel then winning): the rows per lane
     // drop to radix(b) and with them the loads in flight, while the re-reads
@@ -524,16 +628,23 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
   }
   S.k = k;
   S.d = d;
-  const int top = bd_high >= 0 ? 1 : 0;  // in-tile digit 0 = the high broadcast digit
+  const int top = bd_high >= 0 ? 1 : (int)hxd.size();  // in-tile digits above the low ones
   S.nlow = nlow + top;
-  S.PL = (int32_t)(PL * (top ? bd_r : 1));
-  if (top) {
+  S.PL = (int32_t)(PL * (bd_high >= 0 ? bd_r : hxprod));
+  S.hx = (int32_t)hxd.size();
+  if (bd_high >= 0) {
     S.lrad[0] = bd_r;
     for (int j = 0; j < k; j++) S.lstr[0][j] = (int32_t)h.stride[j][bd_high];
+  }
+  for (size_t q = 0; q < hxd.size(); q++) {
+    S.lrad[q] = h.radix[hxd[q]];
+    S.lrowst[q] = rowstride[hxd[q]];
+    for (int j = 0; j < k; j++) S.lstr[q][j] = (int32_t)h.stride[j][hxd[q]];
   }
   for (int q = 0; q < nlow; q++) {  // low digits, most significant first
     const int p = m - nlow + q;
     S.lrad[top + q] = h.radix[p];
+    S.lrowst[top + q] = rowstride[p];
     for (int j = 0; j < k; j++) S.lstr[top + q][j] = (int32_t)h.stride[j][p];
   }
   if (bd_low >= 0 || bd_high >= 0) {
@@ -550,7 +661,7 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
   // back to back in a warp and hit L1/L2 instead of HBM
   int hd[GBE_MAX_SEP], nh = 0;
   for (int p = 0; p < m - nlow; p++)
-    if (h.radix[p] > 1 && p != bd_high) hd[nh++] = p;
+    if (h.radix[p] > 1 && p != bd_high && std::find(hxd.begin(), hxd.end(), p) == hxd.end()) hd[nh++] = p;
   if (nh > 32) return false;
   if (full)
     order_high_digits(h, hd, nh);
@@ -576,7 +687,7 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     const char *e = std::getenv("GBE_STREAM_PF");
     return e ? std::atoi(e) : -1;
   }();
-  const bool no_pf = pf_env == 0 || (pf_env < 0 && k < 2) || bd_high >= 0;
+  const bool no_pf = pf_env == 0 || (pf_env < 0 && k < 2) || bd_high >= 0 || !hxd.empty();
   for (int j = 0; j < k; j++) {
     int64_t want = d, span = 1;
     bool dense = true;
@@ -606,15 +717,20 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     L.vec = vec;
   }
   L.bd = S.bd_rad;
+  L.hx = S.hx;
   L.k = k;
   L.d = d;
   L.f64 = h.semiring != GBE_MINSUM_I32;
   L.sp = h.semiring == GBE_SUMPROD_F64;
   L.t0 = row_begin / S.PL;
   L.ntiles = (row_end - 1) / S.PL - L.t0 + 1;
-  L.smem = (int)(sizeof(int32_t) * (size_t)k * S.PL);
+  L.smem = (int)(sizeof(int32_t) * (size_t)(((k * S.PL + 1) & ~1)) + (hxd.empty() ? 0 : 8 * (size_t)S.PL));
   // CTAs: as many as fit, at least one warp-tile per warp
-  const int per_sm = std::max(1, std::min(8, (200 * 1024) / std::max(L.smem + 1024, 1)));
+  static const int grid_cap = [] {  // GBE_STREAM_PER_SM: CTAs per SM cap (tuning knob: the window of
+    const char *e = std::getenv("GBE_STREAM_PER_SM");  // tiles in flight against L2 re-use)
+    return e ? std::max(1, std::atoi(e)) : 8;
+  }();
+  const int per_sm = std::max(1, std::min(grid_cap, (200 * 1024) / std::max(L.smem + 1024, 1)));
   const int64_t want = (L.ntiles + (kBlock / 32) - 1) / (kBlock / 32);
   L.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms * per_sm, want));
   return true;

@@ -19,6 +19,12 @@ struct StreamDesc {
   uint32_t bd_has, pad2;
   int64_t bd_rowstride;  // 0: b is an in-tile digit of the row order; else b is a high
                          // digit placed on top of the tile: output row stride of b
+  // blocked high digits: hx > 0 puts hx high output digits on top of the
+  // warp-tile (in-tile digits 0..hx-1) so an input lacking them re-reads its
+  // slice inside one tile (L1) instead of across tiles; the tile's rows are
+  // then not contiguous: output row of in-tile digit q has stride lrowst[q]
+  int32_t hx, pad3;
+  int64_t lrowst[GBE_MAX_SEP];
   int32_t lrad[GBE_MAX_SEP];       // low (in-tile) digits, most significant first
   int32_t lstr[GBE_MAX_SEP][32];   // their element strides per input
   int32_t hrad[32];                // high digits (radix > 1), most significant first
@@ -33,6 +39,7 @@ struct BksLaunch {
   int d = 1, k = 1, grid = 1, smem = 0;
   int vec = 0;  // elements per vector load when the layout allows it (0: scalar)
   int bd = 0;   // broadcast-digit radix (0: off)
+  int hx = 0;   // blocked high digits on top of the warp-tile (0: none)
   bool f64 = false, sp = false;
   bool natural = true;  // tiles in row order (partial row ranges); else reordered for L2 reuse
   int64_t t0 = 0, ntiles = 0;

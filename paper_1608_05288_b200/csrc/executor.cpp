@@ -1532,6 +1532,16 @@ static std::string stats_json(const RunImpl &R) {
       }
       o << "]";
     }
+    if (!R.D->use_fast[ti]) {  // post-merge inputs of the other variants
+      const gbe_bucket_desc &hd = R.D->h_desc[ti];
+      o << ",\"in_scope\":[";
+      for (int q = 0; q < hd.ninputs; q++) {
+        o << (q ? "," : "") << "\"";
+        for (int pp = 0; pp < hd.nsep; pp++) o << (hd.stride[q][pp] ? 'X' : '.');
+        o << "\"";
+      }
+      o << "]";
+    }
     o
       << ",\"ms\":" << (ti < R.ms.size() ? R.ms[ti] : -1.0f)
       << ",\"merge_ms\":" << (ti < R.merge_ms.size() ? R.merge_ms[ti] : -1.0f) << "}";

@@ -4,6 +4,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <tuple>
 #include <utility>
 #include <vector>
 
@@ -54,17 +56,34 @@ enum BkVariant { BK_AUTO = -1, BK_GENERIC = 0 };
 // two other 1e9-cell inputs from HBM 16-64 times).
 inline void order_high_digits(const gbe_bucket_desc &h, int *p, int n) {
   const int k = h.ninputs, m = h.nsep;
-  std::vector<std::pair<double, int>> by;
+  // rank: mode 0 (default) by size; mode 1: the inputs of >= 16 MB by the
+  // re-use factor of their slices over the high digits (product of the
+  // radices of the high digits they lack) -- their re-reads then happen
+  // within the fewest tiles -- then the rest by size (GBE_TILE_ORDER: knob)
+  static const int mode = [] {
+    const char *e = std::getenv("GBE_TILE_ORDER");
+    return e ? std::atoi(e) : 0;
+  }();
+  const double es = h.semiring == GBE_MINSUM_I32 ? 4.0 : 8.0;
+  std::vector<std::tuple<int, double, double, int>> by;  // (group, -reuse, -cells, j)
   for (int j = 0; j < k; j++) {
-    double c = h.d;
-    for (int q = 0; q < m; q++)
+    double c = h.d, reuse = 1;
+    for (int q = 0; q < m; q++) {
       if (h.stride[j][q]) c *= h.radix[q];
-    by.push_back({-c, j});
+    }
+    for (int i = 0; i < n; i++)
+      if (!h.stride[j][p[i]]) reuse *= h.radix[p[i]];
+    const bool large = c * es >= 16.0 * (1 << 20);
+    if (mode == 1)
+      by.emplace_back(large ? 0 : 1, large ? -reuse : 0.0, -c, j);
+    else
+      by.emplace_back(0, 0.0, -c, j);
   }
   std::stable_sort(by.begin(), by.end());
   std::stable_sort(p, p + n, [&](int a, int b) {
     for (auto &e : by) {
-      const bool la = h.stride[e.second][a] == 0, lb = h.stride[e.second][b] == 0;
+      const int j = std::get<3>(e);
+      const bool la = h.stride[j][a] == 0, lb = h.stride[j][b] == 0;
       if (la != lb) return lb;  // a before b when only b is lacked (b varies faster)
     }
     return false;

@@ -1,0 +1,7 @@
+set -u
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_stream.py -q -x > gpurun_out/pytest_r02n.log 2>&1; tail -2 gpurun_out/pytest_r02n.log; grep -E "^E " gpurun_out/pytest_r02n.log | head -5
+for E in "X=0" "GBE_STREAM_HX=0" "GBE_STREAM_PF=0"; do echo "== C4-d4 $E"; env $E timeout 300 python scripts/bench_detail.py c4d4 2>&1 | sed -n 2,6p; done
+echo "== C4"; timeout 300 python scripts/bench_detail.py c4 2>&1 | sed -n 2,4p
+echo "== C5"; timeout 300 python scripts/bench_detail.py c5 2>&1 | sed -n 2,4p
+timeout 600 python scripts/bench_domains.py 2>&1 | cut -c1-150

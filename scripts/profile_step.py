@@ -17,7 +17,7 @@ ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--which-fast", action="store_true")
 ap.add_argument("--var", type=int, default=-1)
 a = ap.parse_args()
-inst = {"c4": configs.c4, "c2": configs.c2, "c5": configs.c5, "c5sp": configs.c5}[a.workload]()
+inst = {"c4": configs.c4, "c2": configs.c2, "c5": configs.c5, "c5sp": configs.c5, "c4d4": configs.c4d4}[a.workload]()
 sp = a.workload == "c5sp"
 P = G.Problem.from_instance(inst)
 order, w = P.order()

@@ -254,3 +254,38 @@ def test_stream_broadcast_digit(dom_sep, lack, d, f64):
         torch.cuda.synchronize()
         check(out.cpu().numpy(), arg.cpu().numpy(), exp[rb:re], ea[rb:re], f64, dom, x, members, sep, rb)
     del os.environ["GBE_STREAM_BD"]
+
+
+@pytest.mark.parametrize("f64", [False, True])
+def test_stream_blocked_high_digits(f64):
+    """Three large inputs (>= 16 MB) that lack different high digits: the
+    third one's absent digits go on top of the warp-tile (its re-reads stay
+    inside a tile; the tile's rows are then strided), the two largest are
+    served by the tile order.  Full range through the streaming kernel,
+    against the oracle."""
+    rng = np.random.default_rng(77 + int(f64))
+    m, d = 12, 4
+    dom = [4] * m + [d]
+    lacks = [(2, 5), (3, 7), (0, 1)]
+    members = []
+    for la in lacks:
+        scope = [q for q in range(m) if q not in la] + [m]
+        cells = int(np.prod([dom[v] for v in scope]))
+        t = rng.uniform(0, 10, cells) if f64 else rng.integers(0, 60, cells).astype(np.int64)
+        members.append((scope, t))
+    small = [4, 9, m]
+    members.append((small, rng.uniform(0, 10, 64) if f64 else rng.integers(0, 60, 64).astype(np.int64)))
+    sep = list(range(m))
+    D, rows = desc_for(dom, sep, m, members, G.MINSUM_F64 if f64 else G.MINSUM_I32)
+    exp, ea = oracle.bucket_eval(dom, f64, m, members, sep)
+    for hx in ("1", "0"):
+        os.environ["GBE_STREAM_HX"] = hx
+        dt = torch.float64 if f64 else torch.int32
+        ins = [torch.tensor(np.asarray(t), dtype=dt, device="cuda") for _, t in members]
+        out = torch.empty(rows, dtype=dt, device="cuda")
+        arg = torch.empty(rows, dtype=torch.uint8, device="cuda")
+        G.bucket_kernel(D, ins, out, arg, 0, rows, variant=2)
+        torch.cuda.synchronize()
+        check(out.cpu().numpy(), arg.cpu().numpy(), exp, ea, f64, dom, m, members, sep, 0)
+        del ins, out, arg
+    del os.environ["GBE_STREAM_HX"]
