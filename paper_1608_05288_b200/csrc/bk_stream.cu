@@ -370,7 +370,14 @@ cudaError_t dispatch(const StreamDesc *dd, const BksLaunch &L, const InPtrs &in,
       for (int j = 0; j < L.k; j++)
         if ((uintptr_t)in.p[j] % 16) al = false;
       if constexpr (sizeof(T) == 4) {
-        if (L.d == 4 && L.vec == 4 && al) return launch<T, SP, 1, 4, 4, 4, 4, false, true>(dd, L, in, out, arg, rb, re, s);
+        static const int hxun = [] {  // GBE_STREAM_HXUN: rows per lane (tuning knob)
+          const char *e = std::getenv("GBE_STREAM_HXUN");
+          return e ? std::atoi(e) : 8;
+        }();
+        if (L.d == 4 && L.vec == 4 && al) {
+          if (hxun == 4) return launch<T, SP, 1, 4, 4, 4, 4, false, true>(dd, L, in, out, arg, rb, re, s);
+          return launch<T, SP, 1, 4, 4, 8, 4, false, true>(dd, L, in, out, arg, rb, re, s);
+        }
       } else {
         if (L.d == 4 && L.vec == 2 && al) return launch<T, SP, 1, 4, 4, 4, 2, false, true>(dd, L, in, out, arg, rb, re, s);
       }

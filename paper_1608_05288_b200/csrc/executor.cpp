@@ -468,9 +468,27 @@ static void plan_merges(const Plan &P, DevPlan *D, size_t ti, gbe_bucket_desc &h
       cand[0].clear();
     }
   }
+  // a class whose whole candidate set unions past the cap still merges its
+  // largest subset that fits: members taken smallest first while the union
+  // stays <= cap (C4-d4's x3: 6 class-0 inputs whose full union is 8x the
+  // cap; the 5 smallest fit)
   std::vector<std::vector<int>> sets;
-  for (int c = 0; c < 4; c++)
-    if (cand[c].size() >= 2 && union_cells(cand[c]) <= cap) sets.push_back(cand[c]);
+  for (int c = 0; c < 4; c++) {
+    if (cand[c].size() < 2) continue;
+    if (union_cells(cand[c]) <= cap) {
+      sets.push_back(cand[c]);
+      continue;
+    }
+    std::vector<int> byc = cand[c];
+    std::stable_sort(byc.begin(), byc.end(), [&](int a, int b) { return union_cells({a}) < union_cells({b}); });
+    std::vector<int> sub;
+    for (int j : byc) {
+      sub.push_back(j);
+      if (union_cells(sub) > cap) sub.pop_back();
+    }
+    std::sort(sub.begin(), sub.end());  // canonical member order inside the merged table
+    if (sub.size() >= 2) sets.push_back(sub);
+  }
   if (sets.empty()) return;
   size_t removed = 0;
   for (auto &st : sets) removed += st.size() - 1;
