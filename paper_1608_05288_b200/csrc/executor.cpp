@@ -399,7 +399,31 @@ static void plan_arena(const Plan &P, DevPlan *D, bool mbe_mode) {
 // fold adds no per-cell loads.  Sums are the same ones Alg. 1 line 3 forms
 // (P:204-205); for int32 with the clamp of A9 they are bit-identical, for
 // f64 the summation order changes (canonical order note).
-static void plan_merges(const Plan &P, DevPlan *D, size_t ti, gbe_bucket_desc &h, bool noinf) {
+// The high digit a tile of this bucket could carry on top (bk_fast "runs"):
+// the lowest-placed output digit the largest input lacks, of radix 2..5,
+// above the two lowest digits; -1 if none
+static int htile_candidate(const gbe_bucket_desc &h) {
+  const char *e = std::getenv("GBE_FAST_HTILE");  // opt-in (bk_fast.cu bkf_build)
+  if (!(e && std::atoi(e) == 1)) return -1;
+  const int m = h.nsep, k = h.ninputs;
+  if (m < 3 || k < 2 || h.d < 2 || h.d > 5) return -1;
+  int big = 0;
+  double bc = -1;
+  for (int j = 0; j < k; j++) {
+    double c = h.d;
+    for (int p = 0; p < m; p++)
+      if (h.stride[j][p]) c *= h.radix[p];
+    if (c > bc) {
+      bc = c;
+      big = j;
+    }
+  }
+  for (int p = m - 3; p >= 0; p--)
+    if (!h.stride[big][p] && h.radix[p] >= 2 && h.radix[p] <= 5) return p;
+  return -1;
+}
+
+static void plan_merges(const Plan &P, DevPlan *D, size_t ti, gbe_bucket_desc &h, bool noinf, int ht) {
   static const bool off = std::getenv("GBE_NO_MERGE") != nullptr;  // A/B knob
   const Task &t = P.tasks[ti];
   const int k = h.ninputs, m = h.nsep, d = h.d;
@@ -419,8 +443,18 @@ static void plan_merges(const Plan &P, DevPlan *D, size_t ti, gbe_bucket_desc &h
   FastDesc *F = new FastDesc();
   BkfLaunch L;
   const bool ok = bkf_build(h, t.shard.lo, t.shard.hi, D->num_sms, *F, L, noinf);
+  const int64_t pl_std = F->hot.PL;
   delete F;
   if (!ok) return;
+  // a candidate high digit ht for a run tile {ht} + the nl_h lowest digits
+  // (the same tile size as the low-digit tile): merged tables put ht right
+  // above those digits, so their slice over that tile is contiguous
+  int nl_h = 0;
+  if (ht >= 0) {
+    int64_t pl = h.radix[ht];
+    while (nl_h < m && m - 1 - nl_h > ht && pl * h.radix[m - 1 - nl_h] <= pl_std) pl *= h.radix[m - 1 - nl_h++];
+    if (nl_h < 1) ht = -1;
+  }
   auto has = [&](int j, int p) { return h.stride[j][p] != 0; };
   auto union_cells = [&](const std::vector<int> &js) {
     int64_t c = d;
@@ -517,6 +551,11 @@ static void plan_merges(const Plan &P, DevPlan *D, size_t ti, gbe_bucket_desc &h
           U.push_back(p);
           break;
         }
+    if (ht >= 0 && std::find(U.begin(), U.end(), ht) != U.end()) {  // ht just above the nl_h lowest digits
+      U.erase(std::find(U.begin(), U.end(), ht));
+      auto it = std::find_if(U.begin(), U.end(), [&](int p) { return p >= m - nl_h; });
+      U.insert(it, ht);
+    }
     DevPlan::Merge M;
     M.task = (int32_t)ti;
     M.src.assign(st.begin(), st.end());
@@ -708,14 +747,33 @@ static DevPlan *dev_plan(gbe_plan *gp) {
       D->in_map[ti].resize(h.ninputs);
       for (int j = 0; j < h.ninputs; j++) D->in_map[ti][j] = j;
     } else {
-      plan_merges(P, D, ti, h, noinf);
+      // merged tables laid out for a run tile (a high digit on top) are kept
+      // only when the tiled kernel then takes that tile; else re-merged in
+      // the canonical layout
+      const int ht = htile_candidate(h);
+      const gbe_bucket_desc h0 = h;
+      const size_t nm0 = D->merges.size();
+      plan_merges(P, D, ti, h, noinf, ht);
+      if (ht >= 0 && D->merges.size() > nm0) {
+        FastDesc *Ft = new FastDesc();
+        BkfLaunch Lt;
+        const bool okt = bkf_build(h, t.shard.lo, t.shard.hi, D->num_sms, *Ft, Lt, noinf, ht);
+        delete Ft;
+        if (!okt || Lt.htile < 0) {
+          D->merges.resize(nm0);
+          D->task_merges[ti].clear();
+          h = h0;
+          plan_merges(P, D, ti, h, noinf, -1);
+        }
+      }
     }
     D->h_desc[ti] = h;
     D->launch[ti] = bk_plan_launch(h, t.shard.lo, t.shard.hi, P.ex.kernel, D->num_sms);
     // kernel variant: tiled TMA (1), streaming (2), generic (0)
     const int want = P.ex.kernel;  // -1 auto
     const bool fast_ok = (want == -1 || want == 1) && !P.ex.count &&
-                         bkf_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_fast[ti], D->fl[ti], noinf);
+                         bkf_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_fast[ti], D->fl[ti], noinf,
+                                   htile_candidate(t.desc));
     const bool stream_ok = (want == -1 || want == 2) && !P.ex.count &&
                            bks_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_stream[ti], D->sl[ti]);
     D->cand[ti] = want == -1 && P.ex.autotune && kernel_policy() < 0 && !P.ex.host_args && !P.ex.spill && fast_ok &&
@@ -1539,7 +1597,8 @@ static std::string stats_json(const RunImpl &R) {
       o << ",\"tile_rows\":" << fh.PL << ",\"stages\":" << fh.nstages << ",\"staging_bufs\":" << fh.nout
         << ",\"groups\":" << R.D->fl[ti].NG << ",\"classes\":[" << fh.cls_off[1] - fh.cls_off[0] << ","
         << fh.cls_off[2] - fh.cls_off[1] << "," << fh.cls_off[3] - fh.cls_off[2] << "," << fh.cls_off[4] - fh.cls_off[3]
-        << "],\"g\":[" << R.D->fl[ti].g1 << "," << R.D->fl[ti].g2 << "],\"slen\":[";
+        << "],\"g\":[" << R.D->fl[ti].g1 << "," << R.D->fl[ti].g2 << "],\"htile\":" << R.D->fl[ti].htile
+        << ",\"slen\":[";
       for (int q = 0; q < fh.k; q++) o << (q ? "," : "") << fh.slen[q];
       o << "],\"in_scope\":[";  // per class-ordered input: the output digits it has
       const gbe_bucket_desc &hd = R.D->h_desc[ti];
