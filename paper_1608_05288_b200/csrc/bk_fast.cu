@@ -247,14 +247,9 @@ __device__ __forceinline__ void issue_tile(const ProdTiles &ps, const FastHot &f
 
 // in-tile row offset a * rs1 + b * rs2 of register-block row (a, b), formed
 // where it is used (two live registers instead of R * R2)
-// A tile with a high digit on top ("runs", FastHot::nrun > 1) stages run a
-// of its rows at a * rs1 + sk[a] (sk[a]: the 16-byte phase of run a's global
-// output, in elements) and its argmins dsk[a] bytes further (their own phase)
 struct RowOff {
   int rs1, rs2;
-  int sk[5], dsk[5];
-  __device__ __forceinline__ int operator()(int a, int b) const { return a * rs1 + b * rs2 + sk[a]; }
-  __device__ __forceinline__ int arg(int a, int l) const { return l + dsk[a]; }
+  __device__ __forceinline__ int operator()(int a, int b) const { return a * rs1 + b * rs2; }
 };
 
 // cell (a, b, v) = P0[v] (+ P1[a][v]) (+ P2[b][v]) (+ P3[a][b][v]) with the
@@ -302,7 +297,7 @@ __device__ __forceinline__ void combine(const typename SrF<T>::Acc (&P0)[DV],
           m -= log(z);
         }
         outs[l] = S::out(m);
-        args[loff.arg(a, l)] = 0;
+        args[l] = 0;
       } else {
         Acc best = c[0];
         int bv = 0;
@@ -314,7 +309,7 @@ __device__ __forceinline__ void combine(const typename SrF<T>::Acc (&P0)[DV],
           }
         if (S::kInt) gmax = gmax > best ? gmax : best;  // infinite rows fixed per group
         outs[l] = S::out(best);
-        args[loff.arg(a, l)] = (uint8_t)bv;
+        args[l] = (uint8_t)bv;
       }
     }
   }
@@ -332,12 +327,12 @@ __device__ __forceinline__ void combine_nf(const uint32_t (&P0)[DV], const uint3
                                            int32_t *outs, uint8_t *args, const RowOff &loff) {
   constexpr int SH = DV <= 4 ? 2 : 3;
   constexpr uint32_t MASK = (1u << SH) - 1u;
-  auto emit = [&](const uint32_t (&key)[DV], int a, int l) {
+  auto emit = [&](const uint32_t (&key)[DV], int l) {
     uint32_t m = key[0];
 #pragma unroll
     for (int v = 1; v < DV; v++) m = min(m, key[v]);
     outs[l] = (int32_t)(m >> SH);
-    args[loff.arg(a, l)] = (uint8_t)(m & MASK);
+    args[l] = (uint8_t)(m & MASK);
   };
   if constexpr (!H1) {
     uint32_t B[R2][DV];  // ((P0 + P2[b]) << SH) + v, shared by every a
@@ -352,7 +347,7 @@ __device__ __forceinline__ void combine_nf(const uint32_t (&P0)[DV], const uint3
         uint32_t key[DV];
 #pragma unroll
         for (int v = 0; v < DV; v++) key[v] = H3 ? B[b][v] + (P3[a][b][v] << SH) : B[b][v];
-        emit(key, a, loff(a, b));
+        emit(key, loff(a, b));
       }
   } else {
     uint32_t P2s[R2][DV];
@@ -375,7 +370,7 @@ __device__ __forceinline__ void combine_nf(const uint32_t (&P0)[DV], const uint3
           uint32_t x = H2 ? A[v] + P2s[b][v] : A[v];
           key[v] = H3 ? x + (P3[a][b][v] << SH) : x;
         }
-        emit(key, a, loff(a, b));
+        emit(key, loff(a, b));
       }
     }
   }
@@ -496,60 +491,40 @@ __global__ void __launch_bounds__((NG * GW + 1 + NG) * 32, 1)
     // the buffer of tile i - 1 is released once tile i is committed and at
     // most one store group is still reading shared memory
     const int lane = threadIdx.x & 31;
-    int i = 0;
-    // committed tiles whose staging buffers are not yet released, oldest
-    // first: a buffer is released once at most `depth` newer bulk-store
-    // groups may still be reading shared memory (depth 2 for run tiles,
-    // whose several smaller stores per tile take longer to drain)
-    const int depth = f.store_depth;
-    const int64_t rstride = Fg->run_stride;  // (hoisted: one global load per CTA)
-    int qg[4] = {0, 0, 0, 0}, qb[4] = {0, 0, 0, 0}, qn = 0;
+    int i = 0, pg = -1, pb = 0;
     for (int64_t t = t_begin + blockIdx.x; t < t_end; t += gridDim.x, i++) {
       const int g = i % NG, jg = i / NG, b = jg % nob;
       mbar_wait(&ofull[g][b], (uint32_t)((jg / nob) & 1));
-      const int64_t o0r = ostart[g][b];
-      const int PLr = f.run_rows;  // rows per run (PL when the tile is one run)
-      for (int a = 0; a < f.nrun; a++) {
-      const int64_t o0 = o0r + a * rstride;
-      T *outs = (T *)(sm + f.off_out + (g * nob + b) * f.out_bytes) + a * f.rso +
-                (int)((((uintptr_t)(out + o0)) & 15) / es);
-      uint8_t *args = sm + f.off_arg + (g * nob + b) * f.arg_bytes + a * f.rso + (int)(((uintptr_t)(arg + o0)) & 15);
+      const int64_t o0 = ostart[g][b];
+      T *outs = (T *)(sm + f.off_out + (g * nob + b) * f.out_bytes) + (int)((((uintptr_t)(out + o0)) & 15) / es);
+      uint8_t *args = sm + f.off_arg + (g * nob + b) * f.arg_bytes + (int)(((uintptr_t)(arg + o0)) & 15);
       T *gout = out + o0;
       const int h = (int)(((16 - (((uintptr_t)gout) & 15)) & 15) / es);
-      const int hh = min(h, PLr);
-      const int nmid = ((PLr - hh) * es / 16) * 16 / es;
-      const int tl = PLr - hh - nmid;
+      const int hh = min(h, PL);
+      const int nmid = ((PL - hh) * es / 16) * 16 / es;
+      const int tl = PL - hh - nmid;
       if (lane == 0 && nmid > 0) tma_store_1d(gout + hh, outs + hh, (uint32_t)(nmid * es));
       if (lane < hh) gout[lane] = outs[lane];
       if (lane < tl) gout[hh + nmid + lane] = outs[hh + nmid + lane];
       if (arg) {
         uint8_t *ga = arg + o0;
-        const int ha = min((int)((16 - (((uintptr_t)ga) & 15)) & 15), PLr);
-        const int nmida = ((PLr - ha) / 16) * 16;
-        const int tla = PLr - ha - nmida;
+        const int ha = min((int)((16 - (((uintptr_t)ga) & 15)) & 15), PL);
+        const int nmida = ((PL - ha) / 16) * 16;
+        const int tla = PL - ha - nmida;
         if (lane == 0 && nmida > 0) tma_store_1d(ga + ha, args + ha, (uint32_t)nmida);
         if (lane < ha) ga[lane] = args[lane];
         if (lane < tla) ga[ha + nmida + lane] = args[ha + nmida + lane];
       }
-      }
       __syncwarp();  // ragged ends read before the buffer is released
       if (lane == 0) {
         bulk_commit();
-        qg[qn] = g;
-        qb[qn] = b;
-        qn++;
-        if (qn > depth) {
-          if (depth == 1) bulk_wait_read<1>();
-          else if (depth == 2) bulk_wait_read<2>();
-          else bulk_wait_read<3>();
-          mbar_arrive(&oempty[qg[0]][qb[0]]);
-          for (int e = 1; e < qn; e++) {
-            qg[e - 1] = qg[e];
-            qb[e - 1] = qb[e];
-          }
-          qn--;
+        if (pg >= 0) {
+          bulk_wait_read<1>();
+          mbar_arrive(&oempty[pg][pb]);
         }
       }
+      pg = g;
+      pb = b;
     }
     if (lane == 0) bulk_wait_all();
     return;
@@ -561,9 +536,7 @@ __global__ void __launch_bounds__((NG * GW + 1 + NG) * 32, 1)
   const int c0 = f.cls_off[0], c1 = f.cls_off[1], c2 = f.cls_off[2], c3 = f.cls_off[3], c4 = f.cls_off[4];
   const int sel = CS >= 0 ? (CS & 7) : ((c2 > c1 ? 1 : 0) | (c3 > c2 ? 2 : 0) | (c4 > c3 ? 4 : 0));
   const bool has0 = CS >= 0 ? (CS & 8) != 0 : c1 > c0;
-  RowOff loff{f.rs1, f.rs2, {0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}};  // in-tile row offsets of the group digits
-  const int nrun = f.nrun;
-  const int64_t rstr = Fg->run_stride;
+  const RowOff loff{f.rs1, f.rs2};  // in-tile row offsets of the group digits
   unsigned char *const obase = sm + f.off_out + g * nob * f.out_bytes;
   unsigned char *const abase = sm + f.off_arg + g * nob * f.arg_bytes;
   uint32_t oph = 0;  // use round of the group's staging buffers (parity)
@@ -576,17 +549,8 @@ __global__ void __launch_bounds__((NG * GW + 1 + NG) * 32, 1)
     const int64_t o0 = rowstart[s] - row_begin;
     // staging: element l of this tile lives at index l + sh (16-byte phase of
     // its global address), so the aligned interior is one TMA bulk store
-    int sh = (int)((((uintptr_t)(out + o0)) & 15) / es);
-    int sha = (int)(((uintptr_t)(arg + o0)) & 15);
-    if (nrun > 1) {  // runs (g1 = the high digit): each run staged with its own phase
-#pragma unroll
-      for (int a = 0; a < R; a++) {
-        const int64_t oa = o0 + a * rstr;
-        loff.sk[a] = (int)((((uintptr_t)(out + oa)) & 15) / es);
-        loff.dsk[a] = (int)(((uintptr_t)(arg + oa)) & 15) - loff.sk[a];
-      }
-      sh = sha = 0;
-    }
+    const int sh = (int)((((uintptr_t)(out + o0)) & 15) / es);
+    const int sha = (int)(((uintptr_t)(arg + o0)) & 15);
     T *outs = (T *)(obase + b * f.out_bytes) + sh;
     uint8_t *args = abase + b * f.arg_bytes + sha;
     for (int q = ctid; q < Pmid; q += kGT) {
@@ -713,7 +677,7 @@ __global__ void __launch_bounds__((NG * GW + 1 + NG) * 32, 1)
               const int l = loff(a, bb);
               if ((uint32_t)outq[l] >= kInf) {
                 outq[l] = (T)kInf;
-                argq[loff.arg(a, l)] = 0;
+                argq[l] = 0;
               }
             }
         }
@@ -906,16 +870,21 @@ void build_qperm(FastDesc &F, int es, int R, int R2, int Pmid, int64_t rows) {
 }
 }  // namespace
 
-namespace {
-// One tile configuration: td = the tile digits, most significant first (the
-// low nl output digits, optionally with one high digit `htile` on top, which
-// is then forced to be g1 and makes the tile radix(htile) runs of output
-// rows); fills F / L and returns the per-cell shared-memory loads (the
-// cost), or a negative value when it does not fit.
-double try_tile(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int num_sms, FastDesc &F,
-                BkfLaunch &L, bool noinf, const std::vector<int> &td, int htile, int pass) {
+bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int num_sms,
+               FastDesc &F, BkfLaunch &L, bool noinf) {
   const int m = h.nsep, k = h.ninputs, DV = h.d;
   const int es = h.semiring == GBE_MINSUM_I32 ? 4 : 8;
+  if (m < 2 || k < 1 || k > 32 || DV < 2 || DV > 5) return false;
+  if (row_end <= row_begin) return false;
+  // tiny buckets: the tiled kernel's per-CTA setup (descriptor copy, offset
+  // tables, mbarrier ring) costs more than the bucket; bk_generic is faster
+  if ((row_end - row_begin) * DV < kMinCells) return false;
+  static const int64_t kPLMax = [] {  // rows per tile cap (GBE_FAST_PLMAX: tuning knob)
+    const char *e = std::getenv("GBE_FAST_PLMAX");
+    return e ? std::max<int64_t>(8, std::atoll(e)) : int64_t(16384);
+  }();
+  // one CTA per SM: dynamic shared-memory budget; GBE_FAST_SMEM_KB overrides
+  // it for tuning experiments
   static const char *smem_env = std::getenv("GBE_FAST_SMEM_KB");
   static const int kStagesMax = [] {
     const char *e = std::getenv("GBE_FAST_STAGES");
@@ -927,288 +896,210 @@ double try_tile(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, in
     const char *e = std::getenv("GBE_FAST_WANT_STAGES");
     return e ? std::max(2, std::min(kMaxStages, std::atoi(e))) : 4;
   }();
+  // inputs' sizes (cells) to find the largest
   auto has = [&](int j, int p) { return h.stride[j][p] != 0; };
-  const int nl = (int)td.size();
-  int64_t PL = 1;
-  std::vector<int64_t> tst(m, 0);  // in-tile (staging) row stride of each tile digit
-  for (int i = nl - 1; i >= 0; i--) {
-    tst[td[i]] = PL;
-    PL *= h.radix[td[i]];
-  }
-  // group digits: the pair (equal radix) or single digit with a supported
-  // register-blocking shape that minimises the per-cell shared-memory
-  // loads sum_j R^-|G \ S_j|; pairs win ties (more reuse per group)
-  double bestc = 1e30;
-  int g1 = -1, g2 = -1;
-  static const bool single_only = std::getenv("GBE_FAST_SINGLE") != nullptr;  // tuning knob
-  for (int ia = 0; ia < nl && !single_only; ia++)
-    for (int ib = ia + 1; ib < nl; ib++) {
-      const int a = td[ia], b = td[ib];
-      if (htile >= 0 && a != htile) continue;
-      int R = h.radix[a];
-      if (h.radix[b] != R || !supported(R, R, DV, es)) continue;
-      double c = 0;
-      for (int j = 0; j < k; j++) c += 1.0 / ((has(j, a) ? 1 : R) * (has(j, b) ? 1 : R));
-      if (c < bestc - 1e-12 || (c < bestc + 1e-12 && b > g2)) {
-        bestc = c;
-        g1 = a;
-        g2 = b;
+  std::vector<int64_t> cells(k, DV);
+  for (int j = 0; j < k; j++)
+    for (int p = 0; p < m; p++)
+      if (has(j, p)) cells[j] *= h.radix[p];
+  int big = 0;
+  for (int j = 1; j < k; j++)
+    if (cells[j] > cells[big]) big = j;
+
+  // pass 0: the largest tile whose ring holds kStagesWant stages; pass 1: the
+  // largest tile that fits at all
+  for (int pass = 0; pass < 2; pass++) {
+  for (int nl = m; nl >= 2; nl--) {
+    int64_t PL = 1;
+    for (int p = m - nl; p < m; p++) PL *= h.radix[p];
+    if (PL > kPLMax) continue;
+    // group digits: the pair (equal radix) or single digit with a supported
+    // register-blocking shape that minimises the per-cell shared-memory
+    // loads sum_j R^-|G \ S_j|; pairs win ties (more reuse per group)
+    double bestc = 1e30;
+    int g1 = -1, g2 = -1;
+    static const bool single_only = std::getenv("GBE_FAST_SINGLE") != nullptr;  // tuning knob
+    for (int a = m - nl; a < m && !single_only; a++)
+      for (int b = a + 1; b < m; b++) {
+        int R = h.radix[a];
+        if (h.radix[b] != R || !supported(R, R, DV, es)) continue;
+        double c = 0;
+        for (int j = 0; j < k; j++) c += 1.0 / ((has(j, a) ? 1 : R) * (has(j, b) ? 1 : R));
+        if (c < bestc - 1e-12 || (c < bestc + 1e-12 && b > g2)) {
+          bestc = c;
+          g1 = a;
+          g2 = b;
+        }
+      }
+    if (g1 < 0)
+      for (int a = m - nl; a < m; a++) {
+        int R = h.radix[a];
+        if (!supported(R, 1, DV, es)) continue;
+        double c = 0;
+        for (int j = 0; j < k; j++) c += 1.0 / (has(j, a) ? 1 : R);
+        if (c < bestc - 1e-12 || (c < bestc + 1e-12 && a > g1)) {
+          bestc = c;
+          g1 = a;
+        }
+      }
+    if (g1 < 0) continue;
+    const int R = h.radix[g1];
+    const int R2 = g2 >= 0 ? R : 1;
+    const int64_t Pmid = PL / (R * R2);
+    if (row_begin % PL || row_end % PL) continue;
+    const int NG = ng_of(es, R, R2, DV), GW = gw_of(es, R, R2, DV);
+    const size_t kSmemMax = (size_t)(smem_env ? std::atoi(smem_env) : 220) * 1024;
+    const int min_st = pass == 0 ? std::max(kStagesWant, 2 * NG) : NG;
+    // classes
+    std::memset(&F, 0, sizeof(F));
+    FastHot &f = F.hot;
+    f.k = k;
+    f.es = es;
+    f.PL = (int32_t)PL;
+    f.Pmid = (int32_t)Pmid;
+    f.R = R;
+    f.DV = DV;
+    int jj = 0;
+    for (int c = 0; c < 4; c++) {
+      f.cls_off[c] = jj;
+      for (int j = 0; j < k; j++) {
+        int cls = (has(j, g1) ? 1 : 0) + (g2 >= 0 && has(j, g2) ? 2 : 0);
+        if (cls != c) continue;
+        f.in_idx[jj] = j;
+        f.sg1[jj] = (int32_t)(h.stride[j][g1] * es);  // bytes
+        f.sg2[jj] = g2 >= 0 ? (int32_t)(h.stride[j][g2] * es) : 0;
+        int64_t sl = DV;
+        for (int p = m - nl; p < m; p++)
+          if (has(j, p)) sl *= h.radix[p];
+        f.slen[jj] = (int32_t)sl;
+        F.shift[jj] = h.shift[j];
+        jj++;
       }
     }
-  if (g1 < 0)
-    for (int ia = 0; ia < nl; ia++) {
-      const int a = td[ia];
-      if (htile >= 0 && a != htile) continue;
-      int R = h.radix[a];
-      if (!supported(R, 1, DV, es)) continue;
-      double c = 0;
-      for (int j = 0; j < k; j++) c += 1.0 / (has(j, a) ? 1 : R);
-      if (c < bestc - 1e-12 || (c < bestc + 1e-12 && a > g1)) {
-        bestc = c;
-        g1 = a;
+    f.cls_off[4] = jj;
+    // every input's tile slice must be ONE contiguous range of slen elements:
+    // the tile digits it has, walked from the least significant, carry the
+    // dense strides DV, DV*r, ... (canonical layouts always do; the bare
+    // primitive accepts arbitrary strides, which go to bk_generic)
+    bool dense = true;
+    for (int j = 0; j < k && dense; j++) {
+      int64_t want = DV;
+      for (int p = m - 1; p >= m - nl; p--) {
+        if (!has(j, p)) continue;
+        if (h.stride[j][p] != want) dense = false;
+        want *= h.radix[p];
       }
     }
-  if (g1 < 0) return -1;
-  const int R = h.radix[g1];
-  const int R2 = g2 >= 0 ? R : 1;
-  const int64_t Pmid = PL / (R * R2);
-  const bool runs = htile >= 0;
-  if (!runs && (row_begin % PL || row_end % PL)) return -1;
-  const int NG = ng_of(es, R, R2, DV), GW = gw_of(es, R, R2, DV);
-  const size_t kSmemMax = (size_t)(smem_env ? std::atoi(smem_env) : 220) * 1024;
-  const int min_st = pass == 0 ? std::max(kStagesWant, 2 * NG) : NG;
-  // classes
-  std::memset(&F, 0, sizeof(F));
-  FastHot &f = F.hot;
-  f.k = k;
-  f.es = es;
-  f.PL = (int32_t)PL;
-  f.Pmid = (int32_t)Pmid;
-  f.R = R;
-  f.DV = DV;
-  int jj = 0;
-  for (int c = 0; c < 4; c++) {
-    f.cls_off[c] = jj;
-    for (int j = 0; j < k; j++) {
-      int cls = (has(j, g1) ? 1 : 0) + (g2 >= 0 && has(j, g2) ? 2 : 0);
-      if (cls != c) continue;
-      f.in_idx[jj] = j;
-      f.sg1[jj] = (int32_t)(h.stride[j][g1] * es);  // bytes
-      f.sg2[jj] = g2 >= 0 ? (int32_t)(h.stride[j][g2] * es) : 0;
-      int64_t sl = DV;
-      for (int p : td)
-        if (has(j, p)) sl *= h.radix[p];
-      f.slen[jj] = (int32_t)sl;
-      F.shift[jj] = h.shift[j];
-      jj++;
-    }
-  }
-  f.cls_off[4] = jj;
-  // every input's tile slice must be ONE contiguous range of slen elements:
-  // the tile digits it has, walked from the least significant, carry the
-  // dense strides DV, DV*r, ... (canonical layouts always do for the low
-  // digits; a high digit on top needs the input's next digit above the tile
-  // digits to be it -- merged tables are laid out that way; the bare
-  // primitive accepts arbitrary strides, which go to bk_generic)
-  for (int j = 0; j < k; j++) {
-    int64_t want = DV;
-    for (int i = nl - 1; i >= 0; i--) {
-      const int p = td[i];
-      if (!has(j, p)) continue;
-      if (h.stride[j][p] != want) return -1;
-      want *= h.radix[p];
-    }
-  }
-  // mid digits (L minus g1, g2), tile order; FastHot holds at most 12
-  // (radix-1 digits would let the count exceed it)
-  if (nl - (g2 >= 0 ? 2 : 1) > 12) return -1;
-  f.nmid = 0;
-  std::vector<int64_t> rowstride(m);
-  {
+    if (!dense) continue;
+    // mid digits (L minus g1, g2), natural order; FastHot holds at most 12
+    // (radix-1 digits would let the count exceed it)
+    if (nl - (g2 >= 0 ? 2 : 1) > 12) continue;
+    f.nmid = 0;
     int64_t rowst = 1;
+    std::vector<int64_t> rowstride(m);
     for (int p = m - 1; p >= 0; p--) {
       rowstride[p] = rowst;
       rowst *= h.radix[p];
     }
-  }
-  for (int p : td) {
-    if (p == g1 || p == g2) continue;
-    int e = f.nmid++;
-    f.mrad[e] = h.radix[p];
-    f.mrow[e] = (int32_t)tst[p];
-    for (int q = 0; q < k; q++) f.mstr[e][q] = (int32_t)h.stride[f.in_idx[q]][p];
-  }
-  // runs: the staging row space is nrun runs of run_rows rows, rso apart
-  f.nrun = runs ? R : 1;
-  f.run_rows = (int32_t)(PL / f.nrun);
-  f.rso = runs ? (f.run_rows + 16 + 15) / 16 * 16 : 0;  // 16-byte aligned run bases (elements and argmin bytes)
-  static const int kDepth = [] {  // GBE_FAST_STORE_DEPTH: bulk-store groups in flight (tuning knob)
-    const char *e = std::getenv("GBE_FAST_STORE_DEPTH");
-    return e ? std::max(1, std::min(3, std::atoi(e))) : 0;
-  }();
-  f.store_depth = kDepth ? kDepth : (runs ? 2 : 1);
-  F.run_stride = runs ? rowstride[htile] : 0;
-  f.rs1 = runs ? f.rso : (int32_t)tst[g1];
-  f.rs2 = g2 >= 0 ? (int32_t)tst[g2] : 0;
-  build_qperm(F, es, R, R2, (int)Pmid, row_end - row_begin);
-  // H digits: every output digit not in the tile; for a full-range launch
-  // in the L2-friendly order (kernels.h order_high_digits), else natural
-  std::vector<int> hd;
-  for (int p = 0; p < m; p++)
-    if (std::find(td.begin(), td.end(), p) == td.end()) hd.push_back(p);
-  const bool full = row_begin == 0 && row_end == h.rows;
-  if (runs && !full) return -1;
-  if (full) order_high_digits(h, hd.data(), (int)hd.size());
-  f.nH = (int32_t)hd.size();
-  if (f.nH > 31) return -1;
-  int64_t div = 1;
-  for (int e = f.nH - 1; e >= 0; e--) {
-    int p = hd[e];
-    F.hrad[e] = h.radix[p];
-    F.hdiv[e] = div;
-    div *= h.radix[p];
-    F.hrow[e] = rowstride[p];
-    for (int q = 0; q < k; q++) F.hstr[e][q] = h.stride[f.in_idx[q]][p];
-  }
-  // shared-memory layout
-  size_t off = 0;
-  for (int q = 0; q < k; q++) {
-    f.soff[q] = (int32_t)off;
-    off += ((size_t)f.slen[q] * es + 32 + 15) & ~size_t(15);
-  }
-  f.stage_bytes = (int32_t)off;
-  const size_t orows = runs ? (size_t)f.nrun * f.rso : (size_t)PL;
-  f.out_bytes = (int32_t)((orows * es + 16 + 127) & ~size_t(127));
-  f.arg_bytes = (int32_t)((orows + 16 + 127) & ~size_t(127));
-  // 3 staging buffers when they fit beside the wanted ring (the store of
-  // a tile then has a whole tile of compute to drain), else 2
-  const size_t tabs = (size_t)(k + 1) * Pmid * 4 + 256 + 8 * ((size_t)f.nH * k + 64 * (size_t)(k + 1)) + 256;
-  const size_t obuf = (size_t)NG * ((size_t)f.out_bytes + f.arg_bytes);
-  static const int kNob = [] {  // GBE_FAST_NOUT: tuning knob (1 .. 3)
-    const char *e = std::getenv("GBE_FAST_NOUT");
-    return e ? std::max(1, std::min(kOutBufsMax, std::atoi(e))) : kOutBufsMax;
-  }();
-  int nob = kNob;
-  while (nob > std::min(2, kNob) && obuf * nob + tabs + (size_t)min_st * off > kSmemMax) nob--;
-  f.nout = nob;
-  size_t fixed = obuf * nob + tabs;
-  // the ring length is a multiple of NG: stage s then always serves group
-  // s mod NG, so a group waiting on a stage has consumed that stage's
-  // previous round itself and the mbarrier parity wait cannot alias a
-  // phase two rounds back (with an odd ring a group could wait on a stage
-  // whose previous round, the other group's, was not even issued yet)
-  int nst = kStagesMax - kStagesMax % NG;
-  while (nst > min_st && fixed + nst * off > kSmemMax) nst -= NG;
-  if (nst < NG || fixed + nst * off > kSmemMax) return -1;
-  const size_t stage1 = off;
-  f.nstages = nst;
-  off = nst * off;
-  f.off_out = (int32_t)off;
-  off += (size_t)NG * nob * f.out_bytes;
-  f.off_arg = (int32_t)off;
-  off += (size_t)NG * nob * f.arg_bytes;
-  f.off_tab = (int32_t)off;
-  off += (size_t)k * Pmid * 4;
-  f.off_mrow = (int32_t)off;
-  off += (size_t)Pmid * 4;
-  off = (off + 127) & ~size_t(127);
-  f.off_prod = (int32_t)off;  // producer decode tables: hstr[nH][k], 2 x (trow[32], tb[32][k])
-  off += 8 * ((size_t)f.nH * k + 2 * 32 * (size_t)(k + 1));
-  off = (off + 127) & ~size_t(127);
-  if (off > kSmemMax) return -1;
-  L.smem = (int)off;
-  L.cs = (f.cls_off[1] > f.cls_off[0] ? 8 : 0) | (f.cls_off[2] > f.cls_off[1] ? 1 : 0) |
-         (f.cls_off[3] > f.cls_off[2] ? 2 : 0) | (f.cls_off[4] > f.cls_off[3] ? 4 : 0);
-  L.NG = NG;
-  L.g1 = g1;
-  L.g2 = g2;
-  L.nf = noinf && es == 4 && h.semiring == GBE_MINSUM_I32;
-  L.block = (NG * GW + 1 + NG) * 32;
-  if (runs) {  // full range: tiles enumerate the high digits
-    L.t_begin = 0;
-    L.t_end = h.rows / PL;
-  } else {
+    for (int p = m - nl; p < m; p++) {
+      if (p == g1 || p == g2) continue;
+      int e = f.nmid++;
+      f.mrad[e] = h.radix[p];
+      f.mrow[e] = (int32_t)rowstride[p];
+      for (int q = 0; q < k; q++) f.mstr[e][q] = (int32_t)h.stride[f.in_idx[q]][p];
+    }
+    f.rs1 = (int32_t)rowstride[g1];
+    f.rs2 = g2 >= 0 ? (int32_t)rowstride[g2] : 0;
+    build_qperm(F, es, R, R2, (int)Pmid, row_end - row_begin);
+    // H digits: natural order; for a full-range launch, digits absent from
+    // the largest input go last (fastest) so their re-reads hit L2
+    std::vector<int> hd;
+    for (int p = 0; p < m - nl; p++) hd.push_back(p);
+    const bool full = row_begin == 0 && row_end == h.rows;
+    if (full)
+      order_high_digits(h, hd.data(), (int)hd.size());
+    f.nH = (int32_t)hd.size();
+    if (f.nH > 31) continue;
+    int64_t div = 1;
+    for (int e = f.nH - 1; e >= 0; e--) {
+      int p = hd[e];
+      F.hrad[e] = h.radix[p];
+      F.hdiv[e] = div;
+      div *= h.radix[p];
+      F.hrow[e] = rowstride[p];
+      for (int q = 0; q < k; q++) F.hstr[e][q] = h.stride[f.in_idx[q]][p];
+    }
+    if (!full) {  // natural order: tile index = row / PL
+      // (hd already natural)
+    }
+    // shared-memory layout
+    size_t off = 0;
+    for (int q = 0; q < k; q++) {
+      f.soff[q] = (int32_t)off;
+      off += ((size_t)f.slen[q] * es + 32 + 15) & ~size_t(15);
+    }
+    f.stage_bytes = (int32_t)off;
+    f.out_bytes = (int32_t)(((size_t)PL * es + 16 + 127) & ~size_t(127));
+    f.arg_bytes = (int32_t)(((size_t)PL + 16 + 127) & ~size_t(127));
+    // 3 staging buffers when they fit beside the wanted ring (the store of
+    // a tile then has a whole tile of compute to drain), else 2
+    const size_t tabs = (size_t)(k + 1) * Pmid * 4 + 256 + 8 * ((size_t)f.nH * k + 64 * (size_t)(k + 1)) + 256;
+    const size_t obuf = (size_t)NG * ((size_t)f.out_bytes + f.arg_bytes);
+    static const int kNob = [] {  // GBE_FAST_NOUT: tuning knob (2 or 3)
+      const char *e = std::getenv("GBE_FAST_NOUT");
+      return e ? std::max(1, std::min(kOutBufsMax, std::atoi(e))) : kOutBufsMax;
+    }();
+    int nob = kNob;
+    while (nob > std::min(2, kNob) && obuf * nob + tabs + (size_t)min_st * off > kSmemMax) nob--;
+    f.nout = nob;
+    size_t fixed = obuf * nob + tabs;
+    // the ring length is a multiple of NG: stage s then always serves group
+    // s mod NG, so a group waiting on a stage has consumed that stage's
+    // previous round itself and the mbarrier parity wait cannot alias a
+    // phase two rounds back (with an odd ring a group could wait on a stage
+    // whose previous round, the other group's, was not even issued yet)
+    int nst = kStagesMax - kStagesMax % NG;
+    while (nst > min_st && fixed + nst * off > kSmemMax) nst -= NG;
+    if (nst < NG || fixed + nst * off > kSmemMax) continue;
+    f.nstages = nst;
+    off = nst * off;
+    f.off_out = (int32_t)off;
+    off += (size_t)NG * nob * f.out_bytes;
+    f.off_arg = (int32_t)off;
+    off += (size_t)NG * nob * f.arg_bytes;
+    f.off_tab = (int32_t)off;
+    off += (size_t)k * Pmid * 4;
+    f.off_mrow = (int32_t)off;
+    off += (size_t)Pmid * 4;
+    off = (off + 127) & ~size_t(127);
+    f.off_prod = (int32_t)off;  // producer decode tables: hstr[nH][k], 2 x (trow[32], tb[32][k])
+    off += 8 * ((size_t)f.nH * k + 2 * 32 * (size_t)(k + 1));
+    off = (off + 127) & ~size_t(127);
+    if (off > kSmemMax) continue;
+    L.smem = (int)off;
+    L.cs = (f.cls_off[1] > f.cls_off[0] ? 8 : 0) | (f.cls_off[2] > f.cls_off[1] ? 1 : 0) |
+           (f.cls_off[3] > f.cls_off[2] ? 2 : 0) | (f.cls_off[4] > f.cls_off[3] ? 4 : 0);
+    L.NG = NG;
+    L.g1 = g1;
+    L.g2 = g2;
+    L.nf = noinf && es == 4 && h.semiring == GBE_MINSUM_I32;
+    L.block = (NG * GW + 1 + NG) * 32;
     L.t_begin = row_begin / PL;
     L.t_end = row_end / PL;
+    if (L.t_end >= (int64_t(1) << 32)) return false;  // the producer decodes 32-bit tile indices
+    int per_sm = (int)std::min<size_t>(std::max<size_t>(1, (220 * 1024) / (off + 4096)), 2048 / L.block);
+    per_sm = std::max(1, std::min(per_sm, NG == 2 ? 1 : 8));
+    int64_t tiles = L.t_end - L.t_begin;
+    L.grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms * per_sm));
+    L.R = R;
+    L.R2 = R2;
+    L.DV = DV;
+    L.es = es;
+    L.sp = h.semiring == GBE_SUMPROD_F64;
+    return true;
   }
-  if (L.t_end >= (int64_t(1) << 32)) return -1;  // the producer decodes 32-bit tile indices
-  int per_sm = (int)std::min<size_t>(std::max<size_t>(1, (220 * 1024) / (off + 4096)), 2048 / L.block);
-  per_sm = std::max(1, std::min(per_sm, NG == 2 ? 1 : 8));
-  int64_t tiles = L.t_end - L.t_begin;
-  L.grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms * per_sm));
-  L.R = R;
-  L.R2 = R2;
-  L.DV = DV;
-  L.es = es;
-  L.sp = h.semiring == GBE_SUMPROD_F64;
-  L.htile = htile;
-  L.stage_per_row = (double)stage1 / (double)PL;
-  return bestc;
-}
-}  // namespace
-
-// host: choose the tile digits, the group digits, the tile order, the smem
-// layout; false when the bucket does not fit this kernel (-> bk_generic).
-// htile >= 0 (full-range launches): also try tiles with that high digit on
-// top (as g1: the register blocks then span its values, so an input that
-// lacks it is loaded once for all of them); kept when its loads per cell
-// beat the low-digit tile's, or tie with less staged input per row.
-bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int num_sms,
-               FastDesc &F, BkfLaunch &L, bool noinf, int htile) {
-  const int m = h.nsep, k = h.ninputs, DV = h.d;
-  if (m < 2 || k < 1 || k > 32 || DV < 2 || DV > 5) return false;
-  if (row_end <= row_begin) return false;
-  // tiny buckets: the tiled kernel's per-CTA setup (descriptor copy, offset
-  // tables, mbarrier ring) costs more than the bucket; bk_generic is faster
-  if ((row_end - row_begin) * DV < kMinCells) return false;
-  static const int64_t kPLMax = [] {  // rows per tile cap (GBE_FAST_PLMAX: tuning knob)
-    const char *e = std::getenv("GBE_FAST_PLMAX");
-    return e ? std::max<int64_t>(8, std::atoll(e)) : int64_t(16384);
-  }();
-  // run tiles are opt-in (GBE_FAST_HTILE=1, read per call): on C4's x57
-  // they give the x6-like structure (both inputs reused in registers, half
-  // the staged bytes per row, 8 stages) yet measured slower, 7.9 -> 11.6 ms:
-  // the consumers then wait on the storer (52 % of the stall samples at the
-  // staging-buffer wait), which issues three smaller bulk stores per tile
-  const char *ht_env = std::getenv("GBE_FAST_HTILE");
-  const bool ht_off = !(ht_env && std::atoi(ht_env) == 1);
-  // pass 0: the largest tile whose ring holds the wanted stages; pass 1: the
-  // largest tile that fits at all
-  auto search = [&](int ht, FastDesc &Fo, BkfLaunch &Lo) -> double {
-    for (int pass = 0; pass < 2; pass++)
-      for (int nl = m; nl >= 1; nl--) {
-        std::vector<int> td;
-        int64_t PL = 1;
-        if (ht >= 0) {
-          if (ht >= m - nl) continue;  // the high digit must be above the low ones
-          td.push_back(ht);
-          PL *= h.radix[ht];
-        } else if (nl < 2) {
-          continue;
-        }
-        for (int p = m - nl; p < m; p++) {
-          td.push_back(p);
-          PL *= h.radix[p];
-        }
-        if (PL > kPLMax) continue;
-        const double c = try_tile(h, row_begin, row_end, num_sms, Fo, Lo, noinf, td, ht, pass);
-        if (c >= 0) return c;
-      }
-    return -1;
-  };
-  const double c0 = search(-1, F, L);
-  if (htile < 0 || ht_off || htile >= m || !(row_begin == 0 && row_end == h.rows)) return c0 >= 0;
-  FastDesc *F1 = new FastDesc();
-  BkfLaunch L1;
-  const double c1 = search(htile, *F1, L1);
-  const bool take = c1 >= 0 && (c0 < 0 || c1 < c0 - 1e-9 ||
-                                (c1 < c0 + 1e-9 && L1.stage_per_row < L.stage_per_row - 1e-9));
-  if (take) {
-    std::memcpy(&F, F1, sizeof(FastDesc));
-    L = L1;
   }
-  delete F1;
-  return c0 >= 0 || take;
+  return false;
 }
 
 cudaError_t bkf_launch(const FastDesc *dev_f, const BkfLaunch &L, const InPtrs &in, void *out,

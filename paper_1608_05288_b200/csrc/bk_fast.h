@@ -24,10 +24,6 @@ struct FastHot {
   int32_t mstr[12][32];  // their element strides per input
   int32_t off_out, off_arg, off_tab, off_mrow, off_prod;
   int32_t nstages, out_bytes, arg_bytes, nout;
-  // runs: a tile with a high digit h on top (g1 = h) covers nrun = radix(h)
-  // runs of run_rows consecutive output rows, run_stride apart; run a is
-  // staged at a * rso (+ its 16-byte phase).  nrun = 1: one run of PL rows
-  int32_t nrun, run_rows, rso, store_depth;
 };
 
 struct FastDesc {
@@ -43,7 +39,6 @@ struct FastDesc {
   // combinations a warp handles together hit distinct shared-memory banks
   // (qperm_on = 0: identity)
   int32_t qperm_on, pad3;
-  int64_t run_stride;  // output rows between the runs of a tile (nrun > 1)
   uint16_t qperm[kMaxPmid];
 };
 
@@ -54,16 +49,12 @@ struct BkfLaunch {
   int NG = 1;       // consumer groups per CTA
   int g1 = -1, g2 = -1;  // group (register-blocking) digits
   int cs = -1;           // class structure (bit 3: class 0 present, bits 0-2: classes 1-3)
-  int htile = -1;        // high digit on top of the tile (runs), -1: none
-  double stage_per_row = 0;  // staged input bytes per output row
   int grid = 1, block = 256, smem = 0;
   int64_t t_begin = 0, t_end = 0;
 };
 
-// htile >= 0: also consider tiles with that high output digit on top (see
-// bk_fast.cu); the merged tables of the bucket must be laid out for it
 bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int num_sms,
-               FastDesc &F, BkfLaunch &L, bool noinf = false, int htile = -1);
+               FastDesc &F, BkfLaunch &L, bool noinf = false);
 cudaError_t bkf_launch(const FastDesc *dev_f, const BkfLaunch &L, const InPtrs &in, void *out,
                        uint8_t *arg, int64_t row_begin, cudaStream_t s);
 

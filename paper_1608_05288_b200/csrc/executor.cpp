@@ -112,6 +112,9 @@ struct DevPlan {
     int32_t task = -1;
     gbe_bucket_desc h{};
     BkLaunchInfo li{};
+    bool stream = false;  // run by the streaming kernel (else bk_generic)
+    StreamDesc sd{};
+    BksLaunch sl{};
     std::vector<int32_t> src;  // task input indices (canonical member positions)
     size_t bytes = 0;
   };
@@ -119,6 +122,7 @@ struct DevPlan {
   std::vector<std::vector<int32_t>> task_merges;  // per task: its merges
   std::vector<std::vector<int32_t>> in_map;       // per task input: member index, or -(1 + merge)
   gbe_bucket_desc *d_mdesc = nullptr;
+  StreamDesc *d_mstream = nullptr;  // streaming-kernel descriptors of the merges
   // "retain":"host" (§8(f) row 2, argmin spill): each bucket runs in row
   // chunks whose argmins land in a 2-slot device ring and stream to mapped
   // pinned host memory on a copy stream while the next chunk computes (the
@@ -217,6 +221,7 @@ struct DevPlan {
       }
     cudaFree(d_desc);
     cudaFree(d_mdesc);
+    cudaFree(d_mstream);
     cudaFree(d_cfast);
     cudaFree(d_cstream);
     cudaFree(d_ring);
@@ -399,31 +404,7 @@ static void plan_arena(const Plan &P, DevPlan *D, bool mbe_mode) {
 // fold adds no per-cell loads.  Sums are the same ones Alg. 1 line 3 forms
 // (P:204-205); for int32 with the clamp of A9 they are bit-identical, for
 // f64 the summation order changes (canonical order note).
-// The high digit a tile of this bucket could carry on top (bk_fast "runs"):
-// the lowest-placed output digit the largest input lacks, of radix 2..5,
-// above the two lowest digits; -1 if none
-static int htile_candidate(const gbe_bucket_desc &h) {
-  const char *e = std::getenv("GBE_FAST_HTILE");  // opt-in (bk_fast.cu bkf_build)
-  if (!(e && std::atoi(e) == 1)) return -1;
-  const int m = h.nsep, k = h.ninputs;
-  if (m < 3 || k < 2 || h.d < 2 || h.d > 5) return -1;
-  int big = 0;
-  double bc = -1;
-  for (int j = 0; j < k; j++) {
-    double c = h.d;
-    for (int p = 0; p < m; p++)
-      if (h.stride[j][p]) c *= h.radix[p];
-    if (c > bc) {
-      bc = c;
-      big = j;
-    }
-  }
-  for (int p = m - 3; p >= 0; p--)
-    if (!h.stride[big][p] && h.radix[p] >= 2 && h.radix[p] <= 5) return p;
-  return -1;
-}
-
-static void plan_merges(const Plan &P, DevPlan *D, size_t ti, gbe_bucket_desc &h, bool noinf, int ht) {
+static void plan_merges(const Plan &P, DevPlan *D, size_t ti, gbe_bucket_desc &h, bool noinf) {
   static const bool off = std::getenv("GBE_NO_MERGE") != nullptr;  // A/B knob
   const Task &t = P.tasks[ti];
   const int k = h.ninputs, m = h.nsep, d = h.d;
@@ -443,18 +424,8 @@ static void plan_merges(const Plan &P, DevPlan *D, size_t ti, gbe_bucket_desc &h
   FastDesc *F = new FastDesc();
   BkfLaunch L;
   const bool ok = bkf_build(h, t.shard.lo, t.shard.hi, D->num_sms, *F, L, noinf);
-  const int64_t pl_std = F->hot.PL;
   delete F;
   if (!ok) return;
-  // a candidate high digit ht for a run tile {ht} + the nl_h lowest digits
-  // (the same tile size as the low-digit tile): merged tables put ht right
-  // above those digits, so their slice over that tile is contiguous
-  int nl_h = 0;
-  if (ht >= 0) {
-    int64_t pl = h.radix[ht];
-    while (nl_h < m && m - 1 - nl_h > ht && pl * h.radix[m - 1 - nl_h] <= pl_std) pl *= h.radix[m - 1 - nl_h++];
-    if (nl_h < 1) ht = -1;
-  }
   auto has = [&](int j, int p) { return h.stride[j][p] != 0; };
   auto union_cells = [&](const std::vector<int> &js) {
     int64_t c = d;
@@ -551,11 +522,7 @@ static void plan_merges(const Plan &P, DevPlan *D, size_t ti, gbe_bucket_desc &h
           U.push_back(p);
           break;
         }
-    if (ht >= 0 && std::find(U.begin(), U.end(), ht) != U.end()) {  // ht just above the nl_h lowest digits
-      U.erase(std::find(U.begin(), U.end(), ht));
-      auto it = std::find_if(U.begin(), U.end(), [&](int p) { return p >= m - nl_h; });
-      U.insert(it, ht);
-    }
+
     DevPlan::Merge M;
     M.task = (int32_t)ti;
     M.src.assign(st.begin(), st.end());
@@ -577,6 +544,11 @@ static void plan_merges(const Plan &P, DevPlan *D, size_t ti, gbe_bucket_desc &h
       hm.stride[i][U.size()] = 1;
     }
     M.li = bk_plan_launch(hm, 0, hm.rows, BK_GENERIC, D->num_sms);
+    // the sum (a d = 1 bucket) streams: tiles of the trailing digits, vector
+    // loads, several rows per lane (bk_generic measured 0.8 TB/s on C4's
+    // largest merges); GBE_MERGE_GENERIC: A/B knob
+    static const bool mg = std::getenv("GBE_MERGE_GENERIC") != nullptr;
+    M.stream = !mg && bks_build(hm, 0, hm.rows, D->num_sms, M.sd, M.sl);
     M.bytes = el * (size_t)hm.rows;
     // the bucket reads the merged table with its own mixed-radix strides
     int64_t st_ = d;
@@ -747,33 +719,14 @@ static DevPlan *dev_plan(gbe_plan *gp) {
       D->in_map[ti].resize(h.ninputs);
       for (int j = 0; j < h.ninputs; j++) D->in_map[ti][j] = j;
     } else {
-      // merged tables laid out for a run tile (a high digit on top) are kept
-      // only when the tiled kernel then takes that tile; else re-merged in
-      // the canonical layout
-      const int ht = htile_candidate(h);
-      const gbe_bucket_desc h0 = h;
-      const size_t nm0 = D->merges.size();
-      plan_merges(P, D, ti, h, noinf, ht);
-      if (ht >= 0 && D->merges.size() > nm0) {
-        FastDesc *Ft = new FastDesc();
-        BkfLaunch Lt;
-        const bool okt = bkf_build(h, t.shard.lo, t.shard.hi, D->num_sms, *Ft, Lt, noinf, ht);
-        delete Ft;
-        if (!okt || Lt.htile < 0) {
-          D->merges.resize(nm0);
-          D->task_merges[ti].clear();
-          h = h0;
-          plan_merges(P, D, ti, h, noinf, -1);
-        }
-      }
+      plan_merges(P, D, ti, h, noinf);
     }
     D->h_desc[ti] = h;
     D->launch[ti] = bk_plan_launch(h, t.shard.lo, t.shard.hi, P.ex.kernel, D->num_sms);
     // kernel variant: tiled TMA (1), streaming (2), generic (0)
     const int want = P.ex.kernel;  // -1 auto
     const bool fast_ok = (want == -1 || want == 1) && !P.ex.count &&
-                         bkf_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_fast[ti], D->fl[ti], noinf,
-                                   htile_candidate(t.desc));
+                         bkf_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_fast[ti], D->fl[ti], noinf);
     const bool stream_ok = (want == -1 || want == 2) && !P.ex.count &&
                            bks_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_stream[ti], D->sl[ti]);
     D->cand[ti] = want == -1 && P.ex.autotune && kernel_policy() < 0 && !P.ex.host_args && !P.ex.spill && fast_ok &&
@@ -850,6 +803,9 @@ static DevPlan *dev_plan(gbe_plan *gp) {
   CK(cudaMalloc(&D->d_mdesc, sizeof(gbe_bucket_desc) * std::max<size_t>(D->merges.size(), 1)));
   for (size_t mi = 0; mi < D->merges.size(); mi++)
     CK(cudaMemcpy(D->d_mdesc + mi, &D->merges[mi].h, sizeof(gbe_bucket_desc), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&D->d_mstream, sizeof(StreamDesc) * std::max<size_t>(D->merges.size(), 1)));
+  for (size_t mi = 0; mi < D->merges.size(); mi++)
+    CK(cudaMemcpy(D->d_mstream + mi, &D->merges[mi].sd, sizeof(StreamDesc), cudaMemcpyHostToDevice));
   CK(cudaMalloc(&D->d_desc, sizeof(gbe_bucket_desc) * nt));
   if (!P.tasks.empty())
     CK(cudaMemcpy(D->d_desc, D->h_desc.data(), sizeof(gbe_bucket_desc) * P.tasks.size(), cudaMemcpyHostToDevice));
@@ -1207,7 +1163,10 @@ static void run_util(RunImpl &R) {
       if (P.ex.timing) rec(ev[3 * ti]);
       for (int32_t mi : D->task_merges[ti]) {
         const DevPlan::Merge &M = D->merges[mi];
-        CK(bk_launch(M.h, D->d_mdesc + mi, mins[mi], R.base + R.A->off_merge[mi], nullptr, 0, M.h.rows, M.li, st));
+        if (M.stream)
+          CK(bks_launch(D->d_mstream + mi, M.sl, mins[mi], R.base + R.A->off_merge[mi], nullptr, 0, M.h.rows, st));
+        else
+          CK(bk_launch(M.h, D->d_mdesc + mi, mins[mi], R.base + R.A->off_merge[mi], nullptr, 0, M.h.rows, M.li, st));
         static const bool sync_m = std::getenv("GBE_SYNC_EACH") != nullptr;  // debugging knob
         if (sync_m && !capturing) {
           cudaError_t e = cudaStreamSynchronize(st);
@@ -1597,8 +1556,7 @@ static std::string stats_json(const RunImpl &R) {
       o << ",\"tile_rows\":" << fh.PL << ",\"stages\":" << fh.nstages << ",\"staging_bufs\":" << fh.nout
         << ",\"groups\":" << R.D->fl[ti].NG << ",\"classes\":[" << fh.cls_off[1] - fh.cls_off[0] << ","
         << fh.cls_off[2] - fh.cls_off[1] << "," << fh.cls_off[3] - fh.cls_off[2] << "," << fh.cls_off[4] - fh.cls_off[3]
-        << "],\"g\":[" << R.D->fl[ti].g1 << "," << R.D->fl[ti].g2 << "],\"htile\":" << R.D->fl[ti].htile
-        << ",\"slen\":[";
+        << "],\"g\":[" << R.D->fl[ti].g1 << "," << R.D->fl[ti].g2 << "],\"slen\":[";
       for (int q = 0; q < fh.k; q++) o << (q ? "," : "") << fh.slen[q];
       o << "],\"in_scope\":[";  // per class-ordered input: the output digits it has
       const gbe_bucket_desc &hd = R.D->h_desc[ti];
