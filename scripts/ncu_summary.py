@@ -22,7 +22,12 @@ hdr, vals = raw[0], raw[2]
 for h, v in zip(hdr, vals):
     if h in ("dram__bytes_read.sum", "dram__bytes_write.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
              "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum", "smsp__sass_inst_executed_op_shared_ld.sum",
-             "smsp__sass_inst_executed_op_global_st.sum") or (h.startswith("smsp__pcsamp_warps_issue_stalled") and not h.endswith("not_issued")):
+             "smsp__sass_inst_executed_op_global_st.sum") or h.endswith("pct_of_peak_sustained_elapsed") and (
+                 h.startswith("l1tex__") or h.startswith("lts__") or h.startswith("dram__") or h.startswith("gpu__compute_memory")) or h in (
+             "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
+             "l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_st.sum",
+             "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_pipe_lsu_wavefronts.sum",
+             "l1tex__data_pipe_lsu_wavefronts_mem_lg.sum", "lts__t_sectors_op_read.sum", "lts__t_sectors_op_write.sum") or (h.startswith("smsp__pcsamp_warps_issue_stalled") and not h.endswith("not_issued")):
         if v not in ("0", ""):
             print(f"{h:70s} {v} {raw[1][hdr.index(h)]}")
 src = list(csv.reader(io.StringIO(run("--page", "source", "--csv", "--print-source", "sass"))))
