@@ -109,11 +109,12 @@ struct VecLd<int32_t, 2> {
   }
 };
 
-template <typename T, bool SP, int LPR, int VPL, int DV, int UN, int VEC = 1, bool BD = false, bool HX = false>
+template <typename T, bool SP, int LPR, int VPL, int DV, int UN, int VEC = 1, bool BD = false, bool HX = false,
+          int B2 = 1>
 __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restrict__ D, InPtrs in,
                                                     T *__restrict__ out, uint8_t *__restrict__ arg,
                                                     int64_t row_begin, int64_t row_end, int64_t t0,
-                                                    int64_t ntiles) {
+                                                    int64_t ntiles, bool pf) {
   using S = SrS<T>;
   using Acc = typename S::Acc;
   extern __shared__ int32_t loff[];  // [k][PL] in-tile element offsets
@@ -176,12 +177,16 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
   constexpr int G = 32 / LPR;  // row groups per pass
   const int grp = lane / LPR, sub = lane % LPR;
   static_assert(VEC == 1 || (VPL % VEC == 0 && DV == LPR * VPL), "vector path: whole vectors per lane, exact d");
-  static_assert(!BD || (LPR == 1 && VEC == 1), "broadcast digit: one lane per row, scalar loads");
-  // broadcast digit: pass rows are i = l0 + grp (i < PL / UN enumerates the
-  // rows whose digit b is 0) and the lane's UN rows lb(i) + u * bs
+  static_assert(!BD || LPR == 1, "broadcast digits: one lane per row");
+  static_assert(B2 == 1 || (BD && UN % B2 == 0), "second broadcast digit: UN = B1 * B2 rows per lane");
+  // broadcast digits: pass rows are i = l0 + grp (i < PL / UN enumerates the
+  // rows whose broadcast digits are 0) and the lane's UN rows lb(i) + u * bs,
+  // u = u1 * B2 + u2 (u1: digit b1, u2: digit b2 when B2 > 1)
   const int bs = BD ? D->bd_stride : 0;
   const uint32_t bhas = BD ? D->bd_has : 0u;
-  const int64_t brs = BD ? (D->bd_rowstride ? D->bd_rowstride : (int64_t)bs) : 0;  // output-row stride of b
+  const uint32_t bhas2 = B2 > 1 ? D->bd_has2 : ~0u;
+  const int64_t brs = BD ? (D->bd_rowstride ? D->bd_rowstride : (int64_t)bs) : 0;  // output-row stride of b1
+  const int64_t brs2 = B2 > 1 ? D->bd_rowstride2 : 0;                               // ... of b2
   const int PLi = BD ? PL / UN : PL;
   // value index of this lane's i-th value
   auto vix = [&](int i) { return VEC > 1 ? sub * VPL + i : sub + i * LPR; };
@@ -212,7 +217,7 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
     }
     // output row of row u relative to the tile's first row (formed where used)
     auto grow = [&](int u) -> int64_t {
-      if constexpr (BD) return lb + u * brs;
+      if constexpr (BD) return lb + (u / B2) * brs + (u % B2) * brs2;
       return (hxt && lrow[u] < PL) ? rowoff[lrow[u]] : (int64_t)lrow[u];
     };
 #pragma unroll
@@ -239,18 +244,37 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
         if (j >= k) break;
         const T *pj = FIRST ? pb[jj] : (const T *)in.p[j] + shfl64(base, j) + lane_off;
         const int32_t *lo = loff + j * PL;
-        // an input without the broadcast digit: one load serves all UN rows
-        const bool once = BD && !((bhas >> j) & 1u);
+        // an input without a broadcast digit: the rows that differ only in
+        // the digits it lacks share one load (row u copies row src(u))
+        const bool h1 = !BD || ((bhas >> j) & 1u), h2 = (bhas2 >> j) & 1u;
 #pragma unroll
         for (int u = 0; u < UN; u++) {
           if (MASK && !valid[u]) continue;
           Acc *dst = (FIRST && jj == 0) ? acc[u] : x[jj][u];
-          if (BD && u > 0 && once) {
-            const Acc *src = (FIRST && jj == 0) ? acc[0] : x[jj][0];
-            if (!MASK || valid[0]) {
+          if constexpr (BD) {
+            // src(u) = u with the digits the input lacks set to 0; every
+            // branch indexes the register arrays with compile-time constants
+            const int u1 = u / B2, u2 = u % B2;
+            auto from = [&](int sidx) {  // (sidx constant after unrolling)
+              const Acc *sp = (FIRST && jj == 0) ? acc[sidx] : x[jj][sidx];
 #pragma unroll
-              for (int i = 0; i < VPL; i++) dst[i] = src[i];
-              continue;
+              for (int i = 0; i < VPL; i++) dst[i] = sp[i];
+            };
+            if (!h1 && !h2) {
+              if (u != 0 && (!MASK || valid[0])) {
+                from(0);
+                continue;
+              }
+            } else if (!h1) {
+              if (u1 != 0 && (!MASK || valid[u2])) {
+                from(u2);
+                continue;
+              }
+            } else if (!h2) {
+              if (u2 != 0 && (!MASK || valid[u1 * B2])) {
+                from(u1 * B2);
+                continue;
+              }
             }
           }
           const T *q = pj + lo[lrow[u]];
@@ -325,7 +349,7 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
     int64_t nbase = 0, nrow0 = 0;
     if (tt + nwarps < ntiles) {
       decode(t0 + tt + nwarps, nbase, nrow0);
-      if (lane < k && D->pf_bytes[lane] > 0) {
+      if (pf && lane < k && D->pf_bytes[lane] > 0) {
         const uintptr_t a = (uintptr_t)((const T *)in.p[lane] + nbase);
         const uintptr_t a16 = a & ~(uintptr_t)15;
         const uint32_t bytes = (uint32_t)((a + D->pf_bytes[lane] - a16 + 15) & ~(uintptr_t)15);
@@ -340,7 +364,8 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
     constexpr int kStep = BD ? G : G * UN;  // pass rows (BD: rows with digit b = 0)
     // whole tile: unmasked passes (a tile with a high broadcast digit spans
     // rows up to trow + (UN - 1) * brs + PL / UN)
-    const int64_t tspan = (BD && brs != bs) ? (int64_t)(UN - 1) * brs + PLi : (hxt ? int64_t(0) : (int64_t)PL);
+    const int64_t tspan = (BD && brs != bs) ? (int64_t)(UN / B2 - 1) * brs + (int64_t)(B2 - 1) * brs2 + PLi
+                                            : (hxt ? int64_t(0) : (int64_t)PL);
     if (trow >= row_begin && trow + tspan <= row_end)
       for (; l0 + kStep <= PLi; l0 += kStep) pass(std::false_type{}, l0);
     for (; l0 < PLi; l0 += kStep) pass(std::true_type{}, l0);
@@ -349,15 +374,30 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
   }
 }
 
-template <typename T, bool SP, int LPR, int VPL, int DV, int UN, int VEC = 1, bool BD = false, bool HX = false>
+template <typename T, bool SP, int LPR, int VPL, int DV, int UN, int VEC = 1, bool BD = false, bool HX = false,
+          int B2 = 1>
 cudaError_t launch(const StreamDesc *dd, const BksLaunch &L, const InPtrs &in, void *out, uint8_t *arg,
                    int64_t rb, int64_t re, cudaStream_t s) {
-  auto kern = bk_stream<T, SP, LPR, VPL, DV, UN, VEC, BD, HX>;
+  auto kern = bk_stream<T, SP, LPR, VPL, DV, UN, VEC, BD, HX, B2>;
   if (L.smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem);
     if (e != cudaSuccess) return e;
   }
-  kern<<<L.grid, kBlock, L.smem, s>>>(dd, in, (T *)out, arg, rb, re, L.t0, L.ntiles);
+  // one wave: the CTAs that are resident at once (registers / shared memory
+  // of this instantiation) and no more, so every warp walks its tiles round
+  // robin in one window of the L2-friendly tile order (C5: 15.3 -> 14.8 ms
+  // against 8 CTAs per SM in waves; GBE_STREAM_WAVES=1 restores waves)
+  static const bool waves = [] {
+    const char *e = std::getenv("GBE_STREAM_WAVES");
+    return e && std::atoi(e) == 1;
+  }();
+  int grid = L.grid;
+  if (!waves) {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kBlock, L.smem) == cudaSuccess && nb > 0)
+      grid = (int)std::min<int64_t>(grid, (int64_t)nb * L.sms);
+  }
+  kern<<<grid, kBlock, L.smem, s>>>(dd, in, (T *)out, arg, rb, re, L.t0, L.ntiles, L.pf);
   return cudaGetLastError();
 }
 
@@ -390,17 +430,32 @@ cudaError_t dispatch(const StreamDesc *dd, const BksLaunch &L, const InPtrs &in,
       }
     }
   }
-  if constexpr (!SP) {  // broadcast digit of radix L.bd (one lane per row, d <= 5)
-#define GBE_BD(DVc)                                                                              \
-  if (L.d == DVc) {                                                                              \
-    if (L.bd == 2) return launch<T, SP, 1, DVc, DVc, 2, 1, true>(dd, L, in, out, arg, rb, re, s); \
-    if (L.bd == 3) return launch<T, SP, 1, DVc, DVc, 3, 1, true>(dd, L, in, out, arg, rb, re, s); \
-    if (L.bd == 4) return launch<T, SP, 1, DVc, DVc, 4, 1, true>(dd, L, in, out, arg, rb, re, s); \
-  }
+  if constexpr (!SP) {  // broadcast digits: L.bd rows per lane (one digit, or two of radix 2)
     if (L.bd) {
-      GBE_BD(2) GBE_BD(3) GBE_BD(4) GBE_BD(5)
-    }
+      bool al = L.vec > 1;
+      for (int j = 0; j < L.k && al; j++)
+        if ((uintptr_t)in.p[j] % 16) al = false;
+      constexpr int V2 = 2, V4 = sizeof(T) == 8 ? 2 : 4;  // vector widths for d = 2, 4
+#define GBE_BD(DVc, UNc, B2c)                                                                           \
+  if (L.d == DVc) {                                                                                     \
+    if constexpr (DVc == 2) {                                                                           \
+      if (al) return launch<T, SP, 1, 2, 2, UNc, V2, true, false, B2c>(dd, L, in, out, arg, rb, re, s); \
+    }                                                                                                   \
+    if constexpr (DVc == 4) {                                                                           \
+      if (al) return launch<T, SP, 1, 4, 4, UNc, V4, true, false, B2c>(dd, L, in, out, arg, rb, re, s); \
+    }                                                                                                   \
+    return launch<T, SP, 1, DVc, DVc, UNc, 1, true, false, B2c>(dd, L, in, out, arg, rb, re, s);        \
+  }
+      if (L.bd2 == 2 && L.bd == 4) {
+        GBE_BD(2, 4, 2) GBE_BD(3, 4, 2) GBE_BD(4, 4, 2) GBE_BD(5, 4, 2)
+      } else if (L.bd2 <= 1) {
+        if (L.bd == 2) { GBE_BD(2, 2, 1) GBE_BD(3, 2, 1) GBE_BD(4, 2, 1) GBE_BD(5, 2, 1) }
+        if (L.bd == 3) { GBE_BD(2, 3, 1) GBE_BD(3, 3, 1) GBE_BD(4, 3, 1) GBE_BD(5, 3, 1) }
+        if (L.bd == 4) { GBE_BD(2, 4, 1) GBE_BD(3, 4, 1) GBE_BD(4, 4, 1) GBE_BD(5, 4, 1) }
+      }
 #undef GBE_BD
+      return cudaErrorInvalidValue;
+    }
   }
   // vector path: every input 16-byte aligned (offsets are multiples of VEC,
   // checked by bks_build)
@@ -514,6 +569,8 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     PL /= h.radix[q];
   }
   std::memset(&S, 0, sizeof(S));
+  L.pf_ok = false;
+  L.pf = false;
   const bool full = row_begin == 0 && row_end == h.rows;
   std::vector<int64_t> cells(k, d);
   int big = 0;
@@ -633,15 +690,88 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
       }
     }
   }
+  // high broadcast digits (opt-in: GBE_STREAM_BD2=1, read per build): when
+  // the largest input lacks high output digits, a lane's rows are the
+  // combinations of two radix-2 such digits (or all values of one of radix
+  // 3-4) placed on top of the warp-tile, and every input lacking one of them
+  // is loaded once per combination of the others -- its re-reads come from
+  // registers instead of L1/L2/HBM.  Measured SLOWER although it halves the
+  // loads (C5 x57 1.89 -> 2.37 ms, x77 1.37 -> 1.50, x91 1.22 -> 1.48;
+  // C4-d4 x80 2.62 -> 4.42): the kernel is bound by the latency of its
+  // loads, not their number, and the lane's rows are no longer contiguous
+  // (GBE_STREAM_BD2=2: on for inputs >= 16 MB, the rule it was measured with)
+  int bd_high2 = -1;
+  if (hxd.empty() && bd_low < 0 && bd_high < 0 && full && nlow > 0 && d >= 2 && d <= 5 &&
+      h.semiring != GBE_SUMPROD_F64) {
+    const char *e2 = std::getenv("GBE_STREAM_BD2");
+    const double es = h.semiring == GBE_MINSUM_I32 ? 4.0 : 8.0;
+    const int bd2_env = e2 ? std::atoi(e2) : 0;
+    if (bd2_env == 1 || (bd2_env == 2 && cells[big] * es >= 16.0 * (1 << 20))) {
+      std::vector<int> lack;  // high digits of radix 2..4 the largest input lacks
+      for (int p = 0; p < m - nlow; p++)
+        if (h.radix[p] >= 2 && h.radix[p] <= 4 && !h.stride[big][p]) lack.push_back(p);
+      auto cost = [&](int p1, int p2) {  // loads per row
+        double c = 0;
+        for (int j = 0; j < k; j++)
+          c += 1.0 / ((h.stride[j][p1] ? 1 : h.radix[p1]) * (p2 >= 0 && !h.stride[j][p2] ? h.radix[p2] : 1));
+        return c;
+      };
+      double best = (double)k - 0.25;
+      int b1 = -1, b2 = -1;
+      for (size_t a = 0; a < lack.size(); a++) {
+        const int p1 = lack[a];
+        if (h.radix[p1] >= 3 && cost(p1, -1) < best) {
+          best = cost(p1, -1);
+          b1 = p1;
+          b2 = -1;
+        }
+        for (size_t b = a + 1; b < lack.size(); b++) {
+          const int p2 = lack[b];
+          if (h.radix[p1] == 2 && h.radix[p2] == 2 && cost(p1, p2) < best - 1e-9) {
+            best = cost(p1, p2);
+            b1 = p1;
+            b2 = p2;
+          }
+        }
+      }
+      if (b1 >= 0) {
+        const int un = h.radix[b1] * (b2 >= 0 ? 2 : 1);
+        bool ok = true;  // in-tile offsets stay int32
+        for (int j = 0; j < k; j++) {
+          int64_t mo = maxoff[j] + (int64_t)(h.radix[b1] - 1) * h.stride[j][b1];
+          if (b2 >= 0) mo += h.stride[j][b2];
+          if (mo >= (int64_t(1) << 31)) ok = false;
+        }
+        while (ok && nlow > 1 && PL * un > pl_max) {
+          const int q = m - nlow;  // drop the most significant low digit
+          PL /= h.radix[q];
+          nlow--;
+        }
+        if (ok && PL * un <= pl_max) {
+          bd_high = b1;
+          bd_high2 = b2;
+          bd_r = h.radix[b1];
+        }
+      }
+    }
+  }
   S.k = k;
   S.d = d;
-  const int top = bd_high >= 0 ? 1 : (int)hxd.size();  // in-tile digits above the low ones
+  const int nbd = bd_high < 0 ? 0 : (bd_high2 >= 0 ? 2 : 1);
+  const int top = nbd ? nbd : (int)hxd.size();  // in-tile digits above the low ones
   S.nlow = nlow + top;
-  S.PL = (int32_t)(PL * (bd_high >= 0 ? bd_r : hxprod));
+  S.PL = (int32_t)(PL * (bd_high >= 0 ? bd_r * (bd_high2 >= 0 ? 2 : 1) : hxprod));
   S.hx = (int32_t)hxd.size();
   if (bd_high >= 0) {
     S.lrad[0] = bd_r;
     for (int j = 0; j < k; j++) S.lstr[0][j] = (int32_t)h.stride[j][bd_high];
+  }
+  if (bd_high2 >= 0) {
+    S.lrad[1] = 2;
+    for (int j = 0; j < k; j++) S.lstr[1][j] = (int32_t)h.stride[j][bd_high2];
+    S.bd_rowstride2 = rowstride[bd_high2];
+    for (int j = 0; j < k; j++)
+      if (h.stride[j][bd_high2]) S.bd_has2 |= 1u << j;
   }
   for (size_t q = 0; q < hxd.size(); q++) {
     S.lrad[q] = h.radix[hxd[q]];
@@ -668,7 +798,8 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
   // back to back in a warp and hit L1/L2 instead of HBM
   int hd[GBE_MAX_SEP], nh = 0;
   for (int p = 0; p < m - nlow; p++)
-    if (h.radix[p] > 1 && p != bd_high && std::find(hxd.begin(), hxd.end(), p) == hxd.end()) hd[nh++] = p;
+    if (h.radix[p] > 1 && p != bd_high && p != bd_high2 && std::find(hxd.begin(), hxd.end(), p) == hxd.end())
+      hd[nh++] = p;
   if (nh > 32) return false;
   if (full)
     order_high_digits(h, hd, nh);
@@ -694,7 +825,10 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     const char *e = std::getenv("GBE_STREAM_PF");
     return e ? std::atoi(e) : -1;
   }();
-  const bool no_pf = pf_env == 0 || (pf_env < 0 && k < 2) || bd_high >= 0 || !hxd.empty();
+  // pf_ok: some input can be prefetched; L.pf: on by default (the executor's
+  // autotuning also times the other setting)
+  const bool no_pf = pf_env == 0 || bd_high >= 0 || !hxd.empty();
+  L.pf = !no_pf && (pf_env == 1 || k >= 2);
   for (int j = 0; j < k; j++) {
     int64_t want = d, span = 1;
     bool dense = true;
@@ -707,7 +841,9 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     }
     const int64_t bytes = span * d * (h.semiring == GBE_MINSUM_I32 ? 4 : 8);
     S.pf_bytes[j] = (dense && !no_pf && bytes >= 256 && bytes < (int64_t(1) << 30)) ? bytes : 0;
+    if (S.pf_bytes[j]) L.pf_ok = true;
   }
+  if (!L.pf_ok) L.pf = false;
   // vector loads: one 16-byte (f64 d = 2, 4, 8; int32 d = 4, 8, 16) or
   // 8-byte (int32 d = 2) load per lane when every offset is a multiple of VEC
   {
@@ -723,7 +859,8 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     }
     L.vec = vec;
   }
-  L.bd = S.bd_rad;
+  L.bd = S.bd_rad * (bd_high2 >= 0 ? 2 : 1);
+  L.bd2 = bd_high2 >= 0 ? 2 : 1;
   L.hx = S.hx;
   L.k = k;
   L.d = d;
@@ -740,6 +877,7 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
   const int per_sm = std::max(1, std::min(grid_cap, (200 * 1024) / std::max(L.smem + 1024, 1)));
   const int64_t want = (L.ntiles + (kBlock / 32) - 1) / (kBlock / 32);
   L.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms * per_sm, want));
+  L.sms = num_sms;
   return true;
 }
 

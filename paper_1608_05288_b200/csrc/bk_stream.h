@@ -19,6 +19,10 @@ struct StreamDesc {
   uint32_t bd_has, pad2;
   int64_t bd_rowstride;  // 0: b is an in-tile digit of the row order; else b is a high
                          // digit placed on top of the tile: output row stride of b
+  // a second broadcast digit b2 (high, radix 2, on top of the tile below b):
+  // the lane's rows are then (b, b2) pairs; bit j of bd_has2: input j has b2
+  uint32_t bd_has2, pad4;
+  int64_t bd_rowstride2;  // output row stride of b2
   // blocked high digits: hx > 0 puts hx high output digits on top of the
   // warp-tile (in-tile digits 0..hx-1) so an input lacking them re-reads its
   // slice inside one tile (L1) instead of across tiles; the tile's rows are
@@ -38,10 +42,14 @@ struct StreamDesc {
 struct BksLaunch {
   int d = 1, k = 1, grid = 1, smem = 0;
   int vec = 0;  // elements per vector load when the layout allows it (0: scalar)
-  int bd = 0;   // broadcast-digit radix (0: off)
+  int bd = 0;   // broadcast digits: rows per lane (0: off)
+  int bd2 = 1;  // radix of the second broadcast digit (1: one digit)
   int hx = 0;   // blocked high digits on top of the warp-tile (0: none)
   bool f64 = false, sp = false;
   bool natural = true;  // tiles in row order (partial row ranges); else reordered for L2 reuse
+  bool pf_ok = false;   // some input's tile slice can be prefetched into L2 (dense, canonical layout)
+  bool pf = false;      // prefetch on (default: k >= 2 inputs; the executor's autotuning may flip it)
+  int sms = 1;          // SMs of the device (the grid is one wave of resident CTAs)
   int64_t t0 = 0, ntiles = 0;
 };
 

@@ -98,13 +98,21 @@ struct DevPlan {
   std::vector<BksLaunch> sl;
   std::vector<char> use_stream;
   StreamDesc *d_stream = nullptr;
-  // autotuning (exec option "autotune", kernel auto): tasks both variants can
-  // run are timed with the tiled kernel on one solve and the streaming
-  // kernel on the next (eager, CUDA events around each launch); then each
-  // keeps the faster one and the graph is captured with the final choice
-  std::vector<char> cand;
-  std::vector<float> t_fast, t_stream;
-  int tune_phase = -1;  // -1: no tuning; 0..3: the next solve times tiled / streaming / tiled / streaming; 4: done
+  // autotuning (exec option "autotune", kernel auto): a task with more than
+  // one candidate launch -- the tiled kernel, the streaming kernel with and
+  // without its L2 prefetch -- runs candidate p mod nc on tuning solve p
+  // (eager, CUDA events around each launch; solves 0..nc-1 pay lazy module
+  // loading and are not scored, solves nc..2nc-1 are); then each task keeps
+  // its fastest candidate (3 % margin over its default) and the graph is
+  // captured with the final choice
+  struct Cand {
+    int variant;  // 1 tiled, 2 streaming
+    bool pf;      // streaming: L2 prefetch of the next tile's slices
+  };
+  std::vector<std::vector<Cand>> cands;  // [task]: candidate 0 = the default choice
+  std::vector<std::vector<float>> t_cand;
+  int tune_nc = 0;      // max candidates over the tuned tasks
+  int tune_phase = -1;  // -1: no tuning; 0..2*tune_nc-1: the next tuning solve; 2*tune_nc: done
   std::vector<cudaEvent_t> tune_ev;
   // pre-aggregation of small inputs (DESIGN.md §5 "input merging"): merge mi
   // sums some inputs of task merges[mi].task into one table, a d = 1 bucket
@@ -699,9 +707,9 @@ static DevPlan *dev_plan(gbe_plan *gp) {
   D->h_stream.resize(P.tasks.size());
   D->sl.resize(P.tasks.size());
   D->use_stream.assign(P.tasks.size(), 0);
-  D->cand.assign(P.tasks.size(), 0);
-  D->t_fast.assign(P.tasks.size(), 0.f);
-  D->t_stream.assign(P.tasks.size(), 0.f);
+  D->cands.assign(P.tasks.size(), {});
+  D->t_cand.assign(P.tasks.size(), {});
+  D->tune_nc = 0;
   D->task_merges.assign(P.tasks.size(), {});
   D->in_map.assign(P.tasks.size(), {});
   for (size_t ti = 0; ti < P.tasks.size(); ti++) {
@@ -729,15 +737,30 @@ static DevPlan *dev_plan(gbe_plan *gp) {
                          bkf_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_fast[ti], D->fl[ti], noinf);
     const bool stream_ok = (want == -1 || want == 2) && !P.ex.count &&
                            bks_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_stream[ti], D->sl[ti]);
-    D->cand[ti] = want == -1 && P.ex.autotune && kernel_policy() < 0 && !P.ex.host_args && !P.ex.spill && fast_ok &&
-                  stream_ok;
-    if (D->cand[ti]) D->tune_phase = 0;
     if (fast_ok && (!stream_ok || !prefer_stream(h, D->fl[ti]))) {
       D->use_fast[ti] = 1;
       D->launch[ti].variant = 1;
     } else if (stream_ok) {
       D->use_stream[ti] = 1;
       D->launch[ti].variant = 2;
+    }
+    // autotuning candidates: the default first, then the other variant and
+    // the streaming kernel with its L2 prefetch flipped (unless forced)
+    const bool tune = want == -1 && P.ex.autotune && kernel_policy() < 0 && !P.ex.host_args && !P.ex.spill;
+    if (tune && (fast_ok || stream_ok)) {
+      static const bool pf_forced = std::getenv("GBE_STREAM_PF") != nullptr;
+      auto &cs = D->cands[ti];
+      const bool pf = D->sl[ti].pf, pf_alt = stream_ok && D->sl[ti].pf_ok && !pf_forced;
+      if (D->use_fast[ti]) cs.push_back({1, false});
+      if (stream_ok) cs.push_back({2, pf});
+      if (fast_ok && !D->use_fast[ti]) cs.push_back({1, false});
+      if (pf_alt) cs.push_back({2, !pf});
+      if (cs.size() < 2) cs.clear();
+      if (!cs.empty()) {
+        D->tune_phase = 0;
+        D->tune_nc = std::max(D->tune_nc, (int)cs.size());
+        D->t_cand[ti].assign(cs.size(), 0.f);
+      }
     }
   }
   if (P.ex.spill) {
@@ -1033,7 +1056,7 @@ static void run_util(RunImpl &R) {
   // built-in NCCL one (it only enqueues work on the stream; a Python hook
   // that stages through the host cannot be captured)
   // autotuning solve: eager, candidates forced to one variant, timed
-  const bool tuning = D->tune_phase >= 0 && D->tune_phase < 4;
+  const bool tuning = D->tune_phase >= 0 && D->tune_phase < 2 * D->tune_nc;
   if (tuning) {
     while (D->tune_ev.size() < 2 * nt) {
       cudaEvent_t e;
@@ -1041,9 +1064,12 @@ static void run_util(RunImpl &R) {
       D->tune_ev.push_back(e);
     }
     for (size_t ti = 0; ti < nt; ti++)
-      if (D->cand[ti]) {
-        D->use_fast[ti] = (D->tune_phase & 1) == 0;
-        D->use_stream[ti] = (D->tune_phase & 1) == 1;
+      if (!D->cands[ti].empty()) {
+        const int ci = D->tune_phase % D->tune_nc;
+        const DevPlan::Cand c = D->cands[ti][ci < (int)D->cands[ti].size() ? ci : 0];
+        D->use_fast[ti] = c.variant == 1;
+        D->use_stream[ti] = c.variant == 2;
+        D->sl[ti].pf = c.pf;
       }
   }
   const bool graph = P.ex.graph && (W == 1 || g_ag_graph) && !g_alloc && !R.arena_own && !P.ex.host_args &&
@@ -1243,7 +1269,7 @@ static void run_util(RunImpl &R) {
           CK(cudaEventRecord(D->c_ev[slot], D->cp_stream));
           ring_n++;
         }
-      } else if (tuning && D->cand[ti]) {
+      } else if (tuning && !D->cands[ti].empty()) {
         CK(cudaEventRecord(D->tune_ev[2 * ti], st));
         if (D->use_fast[ti])
           CK(bkf_launch(D->d_fast + ti, D->fl[ti], ins[ti], out, argp, sh.lo, st));
@@ -1353,24 +1379,28 @@ static void run_util(RunImpl &R) {
   if (graph) A.runs++;
   CK(cudaStreamSynchronize(s));
   R.optimum = read_value(p, hopt);
-  if (tuning) {  // this solve's candidate times; after both phases keep the faster variant
+  if (tuning) {  // this solve's candidate times; after both rounds keep each task's fastest
+    const int ci = D->tune_phase % D->tune_nc;
     for (size_t ti = 0; ti < nt; ti++)
-      if (D->cand[ti]) {
+      if (!D->cands[ti].empty() && ci < (int)D->cands[ti].size()) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, D->tune_ev[2 * ti], D->tune_ev[2 * ti + 1]));
-        // the first solve of each variant pays lazy module loading: keep the
-        // second (phases 2, 3)
-        if (D->tune_phase >= 2) ((D->tune_phase & 1) == 0 ? D->t_fast : D->t_stream)[ti] = ms;
+        // the first round pays lazy module loading: keep the second
+        if (D->tune_phase >= D->tune_nc) D->t_cand[ti][ci] = ms;
       }
-    if (++D->tune_phase == 4) {
+    if (++D->tune_phase == 2 * D->tune_nc) {
       for (auto &a : D->arena) a.runs = std::max(a.runs, 1);  // every kernel has run: capture next
-      for (size_t ti = 0; ti < nt; ti++)
-        if (D->cand[ti]) {
-          const bool st = D->t_stream[ti] < 0.97f * D->t_fast[ti];
-          D->use_stream[ti] = st;
-          D->use_fast[ti] = !st;
-          D->launch[ti].variant = st ? 2 : 1;
-        }
+      for (size_t ti = 0; ti < nt; ti++) {
+        const auto &cs = D->cands[ti];
+        if (cs.empty()) continue;
+        size_t best = 0;  // the default unless another candidate is >= 3 % faster
+        for (size_t c = 1; c < cs.size(); c++)
+          if (D->t_cand[ti][c] < 0.97f * D->t_cand[ti][0] && D->t_cand[ti][c] < D->t_cand[ti][best]) best = c;
+        D->use_fast[ti] = cs[best].variant == 1;
+        D->use_stream[ti] = cs[best].variant == 2;
+        D->sl[ti].pf = cs[best].pf;
+        D->launch[ti].variant = cs[best].variant;
+      }
     }
   }
   if (P.ex.count) std::memcpy(&R.count, hopt + 8, sizeof(double));

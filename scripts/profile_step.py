@@ -31,8 +31,17 @@ for _ in range(a.steps):
 want = int(os.environ.get("PROF_VARIANT", "1"))  # 1 tiled (bk_fast), 2 streaming (bk_stream)
 fast = [t for t in st["tasks"] if t["variant"] == want]
 big = max(range(len(fast)), key=lambda i: fast[i]["cells"]) if a.var < 0 else [i for i, t in enumerate(fast) if t["var"] == a.var][0]
+sel = fast[big]
+if want == 2:  # input merges also launch bk_stream, just before their bucket (serial chain in timing mode)
+    idx = 0
+    for t in st["tasks"]:
+        idx += t.get("merges", 0)
+        if t is sel:
+            break
+        idx += 1 if t["variant"] == 2 else 0
+    big = idx
 if a.which_fast:
     print(big)
 else:
     print(json.dumps({"root": root, "fast_launches": len(fast), "largest_fast_index": big,
-                      "largest": fast[big]}))
+                      "largest": sel}))

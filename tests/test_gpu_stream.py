@@ -289,3 +289,51 @@ def test_stream_blocked_high_digits(f64):
         check(out.cpu().numpy(), arg.cpu().numpy(), exp, ea, f64, dom, m, members, sep, 0)
         del ins, out, arg
     del os.environ["GBE_STREAM_HX"]
+
+
+@pytest.mark.parametrize("dom_sep,lacks", [([2, 3, 2, 2, 3, 3, 3, 3, 3], (0, 2)),  # two radix-2 digits
+                                           ([2, 2, 4, 3, 2, 4, 2, 4, 4], (1, 4)),
+                                           ([3, 4, 3, 3, 3, 3, 3, 3, 3], (1,)),    # one radix-4 digit
+                                           ([3, 2, 3, 3, 3, 3, 3, 3, 3], (0,)),    # one radix-3 digit
+                                           ([2, 2, 2, 3, 3, 3, 3, 3, 3], (0, 1, 2))])
+@pytest.mark.parametrize("d", [2, 3, 4, 5])
+@pytest.mark.parametrize("f64", [False, True])
+def test_stream_high_broadcast_digits(dom_sep, lacks, d, f64):
+    """High broadcast digits (opt-in, measured slower; forced here): the largest input lacks high output digits, a lane's rows are the
+    combinations of two radix-2 such digits (or the values of one of radix
+    3-4) on top of the warp-tile, inputs lacking one load once per
+    combination of the others.  Full range (the mode's only use) plus a
+    partial range (plain streaming), INF cells and ties, against the oracle."""
+    os.environ["GBE_STREAM_BD2"] = "1"
+    try:
+        rng = np.random.default_rng(hash((tuple(dom_sep), lacks, d, f64, "bd2")) % (1 << 32))
+        m = len(dom_sep)
+        dom = list(dom_sep) + [d]
+        members = []
+        for j in range(int(rng.integers(2, 5))):
+            if j == 0:
+                sub = [q for q in range(m) if q not in lacks]
+            else:  # other inputs: random subsets (some lack a broadcast digit, some not)
+                sub = sorted(q for q in range(m) if rng.random() < 0.5)
+            scope = sub + [m]
+            cells = int(np.prod([dom[v] for v in scope]))
+            if f64:
+                t = rng.uniform(0, 10, cells).round(1)  # ties
+                t[rng.random(cells) < 0.05] = np.inf
+            else:
+                t = rng.integers(0, 30, cells).astype(np.int64)
+                t[rng.random(cells) < 0.05] = INF
+            members.append((scope, t))
+        sep = list(range(m))
+        D, rows = desc_for(dom, sep, m, members, G.MINSUM_F64 if f64 else G.MINSUM_I32)
+        exp, ea = oracle.bucket_eval(dom, f64, m, members, sep)
+        dt = torch.float64 if f64 else torch.int32
+        for rb, re in [(0, rows), (5, rows - 3)]:
+            ins = [torch.tensor(np.asarray(t), dtype=dt, device="cuda") for _, t in members]
+            out = torch.empty(re - rb, dtype=dt, device="cuda")
+            arg = torch.empty(re - rb, dtype=torch.uint8, device="cuda")
+            G.bucket_kernel(D, ins, out, arg, rb, re, variant=2)
+            torch.cuda.synchronize()
+            check(out.cpu().numpy(), arg.cpu().numpy(), exp[rb:re], ea[rb:re], f64, dom, m, members, sep, rb)
+    finally:
+        del os.environ["GBE_STREAM_BD2"]
