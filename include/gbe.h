@@ -288,8 +288,11 @@ gbe_status gbe_bucket_kernel(const void *desc, const void *const *dev_inputs, vo
                              void *stream);
 
 /* The same with the kernel variant chosen by the caller: -1 auto (as
- * gbe_bucket_kernel), 0 generic, 1 tiled TMA, 2 streaming; GBE_E_INVALID if
- * the descriptor does not fit the requested variant. */
+ * gbe_bucket_kernel), 0 generic, 1 tiled TMA, 2 streaming, 3 streaming in
+ * its staged mode (per-warp TMA double buffers; d = 2..5, min-sum, every
+ * input's warp-tile slice one dense range; it reads inputs in 16-byte
+ * granules like the tiled variant); GBE_E_INVALID if the descriptor does not
+ * fit the requested variant. */
 gbe_status gbe_bucket_kernel_ex(const void *desc, const void *const *dev_inputs, void *dev_out,
                                 uint8_t *dev_arg, int64_t row_begin, int64_t row_end, void *stream,
                                 int32_t variant);

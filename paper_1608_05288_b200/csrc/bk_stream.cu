@@ -69,6 +69,36 @@ struct SrS<double> {
   __device__ __forceinline__ static double out(Acc a) { return a; }
 };
 
+// staged mode: mbarrier / TMA bulk-copy wrappers (PTX)
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void *smem_dst, const void *gsrc, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ int64_t shfl64(int64_t x, int src) {
   return (int64_t)__shfl_sync(0xffffffffu, (long long)x, src);
 }
@@ -80,20 +110,24 @@ __device__ __forceinline__ int64_t shfl64(int64_t x, int src) {
 // spans the trailing digits are contiguous (needs every offset a multiple of
 // VEC and aligned tables: checked on the host and at launch).  DV > 0: the
 // domain size is that compile-time constant; DV = 0: runtime d, masked.
+// (SM: the pointer is into shared memory -- the staged mode -- and takes a
+// plain load instead of the read-only global path)
 template <typename T, int VEC>
 struct VecLd;
 template <>
 struct VecLd<double, 2> {
+  template <bool SM>
   __device__ __forceinline__ static void ld(const double *p, double *v) {
-    const double2 x = __ldg((const double2 *)p);
+    const double2 x = SM ? *(const double2 *)p : __ldg((const double2 *)p);
     v[0] = x.x;
     v[1] = x.y;
   }
 };
 template <>
 struct VecLd<int32_t, 4> {
+  template <bool SM>
   __device__ __forceinline__ static void ld(const int32_t *p, uint32_t *v) {
-    const int4 x = __ldg((const int4 *)p);
+    const int4 x = SM ? *(const int4 *)p : __ldg((const int4 *)p);
     v[0] = (uint32_t)x.x;
     v[1] = (uint32_t)x.y;
     v[2] = (uint32_t)x.z;
@@ -102,15 +136,16 @@ struct VecLd<int32_t, 4> {
 };
 template <>
 struct VecLd<int32_t, 2> {
+  template <bool SM>
   __device__ __forceinline__ static void ld(const int32_t *p, uint32_t *v) {
-    const int2 x = __ldg((const int2 *)p);
+    const int2 x = SM ? *(const int2 *)p : __ldg((const int2 *)p);
     v[0] = (uint32_t)x.x;
     v[1] = (uint32_t)x.y;
   }
 };
 
 template <typename T, bool SP, int LPR, int VPL, int DV, int UN, int VEC = 1, bool BD = false, bool HX = false,
-          int B2 = 1>
+          int B2 = 1, bool STG = false>
 __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restrict__ D, InPtrs in,
                                                     T *__restrict__ out, uint8_t *__restrict__ arg,
                                                     int64_t row_begin, int64_t row_end, int64_t t0,
@@ -149,6 +184,25 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (gw >= ntiles) return;
+  // staged mode (STG): each warp owns two shared-memory buffers; buffer b
+  // holds the input slices of one of its tiles, filled by TMA bulk copies
+  // (one per input, issued by lane j) one tile ahead of the compute, with
+  // completion on the buffer's mbarrier -- the bytes in flight no longer
+  // cost registers and the copies of tile i+1 overlap the compute of tile i
+  [[maybe_unused]] unsigned char *wbuf = nullptr;
+  [[maybe_unused]] uint64_t *wbar = nullptr;
+  if constexpr (STG) {
+    unsigned char *sm = (unsigned char *)loff;
+    const int w = threadIdx.x >> 5;
+    wbar = (uint64_t *)(sm + D->stg_off) + 2 * w;
+    wbuf = sm + D->stg_off + 16 * (kBlock / 32) + (size_t)w * 2 * D->stg_buf;
+    if (lane == 0) {
+      mbar_init(&wbar[0], 1);
+      mbar_init(&wbar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+  }
   // tile decode: lane q < nhigh computes high digit q of the tile index
   // (32-bit division when the index fits), lane j < k sums its input's base
   // offset and every lane the tile's first output row.  Warps take tiles
@@ -198,6 +252,12 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
   const int lane_off = VEC > 1 ? sub * VPL : sub;
   const T *pb[KU];  // this tile's first KU input pointers (hoisted per tile)
   int64_t trow = 0;
+  [[maybe_unused]] const unsigned char *wb = nullptr;  // STG: this tile's buffer
+  [[maybe_unused]] int32_t skew = 0;                  // STG: lane j: 16-byte phase of input j's slice
+  // STG: element pointer of input j in this tile's buffer
+  auto sptr = [&](int j) -> const T * {
+    return (const T *)(wb + D->stg_soff[j] + __shfl_sync(0xffffffffu, skew, j)) + lane_off;
+  };
   // one pass = UN row groups of this warp (rows l0 + u * G + grp of the
   // tile); MASK: rows past the tile or outside [row_begin, row_end) skipped
   auto pass = [&](auto maskc, int l0) {
@@ -242,7 +302,7 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
       for (int jj = 0; jj < KU; jj++) {
         const int j = j0 + jj;
         if (j >= k) break;
-        const T *pj = FIRST ? pb[jj] : (const T *)in.p[j] + shfl64(base, j) + lane_off;
+        const T *pj = FIRST ? pb[jj] : (STG ? sptr(j) : (const T *)in.p[j] + shfl64(base, j) + lane_off);
         const int32_t *lo = loff + j * PL;
         // an input without a broadcast digit: the rows that differ only in
         // the digits it lacks share one load (row u copies row src(u))
@@ -280,11 +340,11 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
           const T *q = pj + lo[lrow[u]];
           if constexpr (VEC > 1) {
 #pragma unroll
-            for (int i = 0; i < VPL; i += VEC) VecLd<T, VEC>::ld(q + i, dst + i);
+            for (int i = 0; i < VPL; i += VEC) VecLd<T, VEC>::template ld<STG>(q + i, dst + i);
           } else {
 #pragma unroll
             for (int i = 0; i < VPL; i++)
-              if (DV > 0 || sub + i * LPR < d) dst[i] = S::ld(q + i * LPR);
+              if (DV > 0 || sub + i * LPR < d) dst[i] = STG ? (Acc)q[i * LPR] : S::ld(q + i * LPR);
           }
         }
       }
@@ -344,12 +404,39 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
   // slices prefetched into L2 with one bulk (TMA) prefetch per input: the
   // loads of a tile then find their data in L2, so a warp keeps a whole
   // tile of bytes in flight without holding registers for them
+  // STG: the bulk copies of the tile whose input bases are tb (lane j) into
+  // buffer bb (one per input, its 16-byte-aligned covering range); returns
+  // lane j's skew (the slice's 16-byte phase)
+  [[maybe_unused]] auto issue = [&](int bb, int64_t tb) -> int32_t {
+    uintptr_t a16 = 0;
+    uint32_t bytes = 0, sk = 0;
+    if (lane < k) {
+      const uintptr_t a = (uintptr_t)((const T *)in.p[lane] + tb);
+      a16 = a & ~(uintptr_t)15;
+      bytes = (uint32_t)((a + (uintptr_t)D->stg_slice[lane] - a16 + 15) & ~(uintptr_t)15);
+      sk = (uint32_t)(a - a16);
+    }
+    const uint32_t total = __reduce_add_sync(0xffffffffu, bytes);
+    // the buffer's previous reads (generic proxy) before the async-proxy writes
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive_expect_tx(&wbar[bb], total);
+    __syncwarp();
+    if (bytes) tma_load_1d(wbuf + (size_t)bb * D->stg_buf + D->stg_soff[lane], (const void *)a16, bytes, &wbar[bb]);
+    return (int32_t)sk;
+  };
   decode(t0 + gw, base, row0);
+  [[maybe_unused]] int bcur = 0;
+  [[maybe_unused]] uint32_t bph = 0;
+  [[maybe_unused]] int32_t nskew = 0;
+  if constexpr (STG) skew = issue(0, base);
   for (int64_t tt = gw; tt < ntiles; tt += nwarps) {
     int64_t nbase = 0, nrow0 = 0;
     if (tt + nwarps < ntiles) {
       decode(t0 + tt + nwarps, nbase, nrow0);
-      if (pf && lane < k && D->pf_bytes[lane] > 0) {
+      if constexpr (STG) {
+        nskew = issue(bcur ^ 1, nbase);
+      } else if (pf && lane < k && D->pf_bytes[lane] > 0) {
         const uintptr_t a = (uintptr_t)((const T *)in.p[lane] + nbase);
         const uintptr_t a16 = a & ~(uintptr_t)15;
         const uint32_t bytes = (uint32_t)((a + D->pf_bytes[lane] - a16 + 15) & ~(uintptr_t)15);
@@ -357,9 +444,17 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
       }
     }
     trow = row0;
+    if constexpr (STG) {
+      mbar_wait(&wbar[bcur], bph);
+      wb = wbuf + (size_t)bcur * D->stg_buf;
 #pragma unroll
-    for (int jj = 0; jj < KU; jj++)
-      if (jj < k) pb[jj] = (const T *)in.p[jj] + shfl64(base, jj) + lane_off;
+      for (int jj = 0; jj < KU; jj++)
+        if (jj < k) pb[jj] = sptr(jj);
+    } else {
+#pragma unroll
+      for (int jj = 0; jj < KU; jj++)
+        if (jj < k) pb[jj] = (const T *)in.p[jj] + shfl64(base, jj) + lane_off;
+    }
     int l0 = 0;
     constexpr int kStep = BD ? G : G * UN;  // pass rows (BD: rows with digit b = 0)
     // whole tile: unmasked passes (a tile with a high broadcast digit spans
@@ -369,16 +464,22 @@ __global__ void __launch_bounds__(kBlock, 2) bk_stream(const StreamDesc *__restr
     if (trow >= row_begin && trow + tspan <= row_end)
       for (; l0 + kStep <= PLi; l0 += kStep) pass(std::false_type{}, l0);
     for (; l0 < PLi; l0 += kStep) pass(std::true_type{}, l0);
+    if constexpr (STG) {
+      __syncwarp();  // every lane done with buffer bcur before it is refilled
+      skew = nskew;
+      bcur ^= 1;
+      if (bcur == 0) bph ^= 1;
+    }
     base = nbase;
     row0 = nrow0;
   }
 }
 
 template <typename T, bool SP, int LPR, int VPL, int DV, int UN, int VEC = 1, bool BD = false, bool HX = false,
-          int B2 = 1>
+          int B2 = 1, bool STG = false>
 cudaError_t launch(const StreamDesc *dd, const BksLaunch &L, const InPtrs &in, void *out, uint8_t *arg,
                    int64_t rb, int64_t re, cudaStream_t s) {
-  auto kern = bk_stream<T, SP, LPR, VPL, DV, UN, VEC, BD, HX, B2>;
+  auto kern = bk_stream<T, SP, LPR, VPL, DV, UN, VEC, BD, HX, B2, STG>;
   if (L.smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem);
     if (e != cudaSuccess) return e;
@@ -404,6 +505,28 @@ cudaError_t launch(const StreamDesc *dd, const BksLaunch &L, const InPtrs &in, v
 template <typename T, bool SP>
 cudaError_t dispatch(const StreamDesc *dd, const BksLaunch &L, const InPtrs &in, void *out, uint8_t *arg,
                      int64_t rb, int64_t re, cudaStream_t s) {
+  if constexpr (!SP) {  // staged mode (d = 2..5, one lane per row, the unstaged shapes' rows per lane)
+    if (L.stg) {
+      bool al = L.vec > 1;
+      for (int j = 0; j < L.k && al; j++)
+        if ((uintptr_t)in.p[j] % 16) al = false;
+      constexpr bool F = sizeof(T) == 8;
+      constexpr int V4 = F ? 2 : 4;
+      switch (L.d) {
+        case 2:
+          if (al) return launch<T, SP, 1, 2, 2, 4, 2, false, false, 1, true>(dd, L, in, out, arg, rb, re, s);
+          return launch<T, SP, 1, 2, 2, F ? 4 : 8, 1, false, false, 1, true>(dd, L, in, out, arg, rb, re, s);
+        case 3: return launch<T, SP, 1, 3, 3, F ? 4 : 8, 1, false, false, 1, true>(dd, L, in, out, arg, rb, re, s);
+        case 4:
+          // (f64: 2 rows per lane -- 4 spill at the 128-register cap; shared-
+          // memory loads need fewer rows in flight than global ones)
+          if (al) return launch<T, SP, 1, 4, 4, F ? 2 : 4, V4, false, false, 1, true>(dd, L, in, out, arg, rb, re, s);
+          return launch<T, SP, 1, 4, 4, F ? 2 : 4, 1, false, false, 1, true>(dd, L, in, out, arg, rb, re, s);
+        case 5: return launch<T, SP, 1, 5, 5, F ? 2 : 4, 1, false, false, 1, true>(dd, L, in, out, arg, rb, re, s);
+        default: return cudaErrorInvalidValue;
+      }
+    }
+  }
   if constexpr (!SP) {  // blocked high digits (full-range launches, d <= 5, min-sum)
     if (L.hx) {
       bool al = true;
@@ -541,7 +664,7 @@ int bks_lanes_per_row(int d) {
 }
 
 bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int num_sms, StreamDesc &S,
-               BksLaunch &L) {
+               BksLaunch &L, bool stage) {
   const int m = h.nsep, k = h.ninputs, d = h.d;
   if (k < 1 || k > 32 || d < 1 || d > GBE_MAX_DOMAIN || row_end <= row_begin) return false;
   // warp-tile: trailing output digits while the CTA's offset table stays
@@ -568,9 +691,47 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     const int q = m - 1 - nlow;
     PL /= h.radix[q];
   }
+  // staged mode: every input's slice over the in-tile digits must be one
+  // dense range (bulk-copyable), and two per-warp buffers of them plus the
+  // offset table must fit the CTA's shared-memory budget
+  // (GBE_STREAM_STAGE_KB, default 100 KB: two CTAs per SM): drop low digits
+  // until they do
+  const int esz = h.semiring == GBE_MINSUM_I32 ? 4 : 8;
+  std::vector<int64_t> sbytes(k, 0);
+  int64_t sbuf = 0;
+  if (stage) {
+    if (d < 2 || d > 5 || h.semiring == GBE_SUMPROD_F64) return false;
+    static const int stg_kb = [] {
+      const char *e = std::getenv("GBE_STREAM_STAGE_KB");
+      return e ? std::max(16, std::min(220, std::atoi(e))) : 100;
+    }();
+    for (;;) {
+      bool dense = true;
+      sbuf = 0;
+      for (int j = 0; j < k; j++) {
+        int64_t want = d, span = 1;
+        for (int q = nlow - 1; q >= 0; q--) {
+          const int p = m - nlow + q;
+          if (!h.stride[j][p]) continue;
+          if (h.stride[j][p] != want) dense = false;
+          want *= h.radix[p];
+          span *= h.radix[p];
+        }
+        sbytes[j] = span * d * esz;
+        sbuf += ((sbytes[j] + 15) & ~int64_t(15)) + 32;
+      }
+      if (!dense) return false;
+      const int64_t need = ((4 * (int64_t)k * PL + 15) & ~int64_t(15)) + 16 * (kBlock / 32) + 2 * (kBlock / 32) * sbuf;
+      if (need <= (int64_t)stg_kb * 1024) break;
+      if (nlow <= 1 || PL / h.radix[m - nlow] < 32) return false;
+      PL /= h.radix[m - nlow];  // drop the most significant low digit
+      nlow--;
+    }
+  }
   std::memset(&S, 0, sizeof(S));
   L.pf_ok = false;
   L.pf = false;
+  L.stg = stage;
   const bool full = row_begin == 0 && row_end == h.rows;
   std::vector<int64_t> cells(k, d);
   int big = 0;
@@ -598,7 +759,7 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
   int64_t hxprod = 1;
   {
     const char *e = std::getenv("GBE_STREAM_HX");  // A/B knob (0: off)
-    const bool hx_off = (e && std::atoi(e) == 0) || d > 5 || d < 2 || h.semiring == GBE_SUMPROD_F64;
+    const bool hx_off = (e && std::atoi(e) == 0) || d > 5 || d < 2 || h.semiring == GBE_SUMPROD_F64 || stage;
     const double es = h.semiring == GBE_MINSUM_I32 ? 4.0 : 8.0;
     std::vector<std::pair<double, int>> large;
     for (int j = 0; j < k; j++)
@@ -648,7 +809,7 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     // tests can enable it)
     const char *bd_env = std::getenv("GBE_STREAM_BD");
     const bool bd_off = !(bd_env && std::atoi(bd_env) == 1);
-    if (!bd_off && d <= 5 && d >= 2 && h.semiring != GBE_SUMPROD_F64 && k >= 1) {
+    if (!bd_off && !stage && d <= 5 && d >= 2 && h.semiring != GBE_SUMPROD_F64 && k >= 1) {
       auto cost = [&](int p) {
         double c = 0;
         for (int j = 0; j < k; j++) c += h.stride[j][p] ? 1.0 : 1.0 / h.radix[p];
@@ -701,7 +862,7 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
   // loads, not their number, and the lane's rows are no longer contiguous
   // (GBE_STREAM_BD2=2: on for inputs >= 16 MB, the rule it was measured with)
   int bd_high2 = -1;
-  if (hxd.empty() && bd_low < 0 && bd_high < 0 && full && nlow > 0 && d >= 2 && d <= 5 &&
+  if (!stage && hxd.empty() && bd_low < 0 && bd_high < 0 && full && nlow > 0 && d >= 2 && d <= 5 &&
       h.semiring != GBE_SUMPROD_F64) {
     const char *e2 = std::getenv("GBE_STREAM_BD2");
     const double es = h.semiring == GBE_MINSUM_I32 ? 4.0 : 8.0;
@@ -827,7 +988,7 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
   }();
   // pf_ok: some input can be prefetched; L.pf: on by default (the executor's
   // autotuning also times the other setting)
-  const bool no_pf = pf_env == 0 || bd_high >= 0 || !hxd.empty();
+  const bool no_pf = pf_env == 0 || bd_high >= 0 || !hxd.empty() || stage;
   L.pf = !no_pf && (pf_env == 1 || k >= 2);
   for (int j = 0; j < k; j++) {
     int64_t want = d, span = 1;
@@ -869,6 +1030,18 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
   L.t0 = row_begin / S.PL;
   L.ntiles = (row_end - 1) / S.PL - L.t0 + 1;
   L.smem = (int)(sizeof(int32_t) * (size_t)(((k * S.PL + 1) & ~1)) + (hxd.empty() ? 0 : 8 * (size_t)S.PL));
+  if (stage) {  // [offset table][per-warp mbarriers][per-warp buffers x 2]
+    if (L.pf) L.pf = false;
+    S.stg_off = (int32_t)((4 * (int64_t)k * S.PL + 15) & ~int64_t(15));
+    S.stg_buf = (int32_t)sbuf;
+    int64_t o = 0;
+    for (int j = 0; j < k; j++) {
+      S.stg_soff[j] = (int32_t)o;
+      S.stg_slice[j] = (int32_t)sbytes[j];
+      o += ((sbytes[j] + 15) & ~int64_t(15)) + 32;
+    }
+    L.smem = (int)(S.stg_off + 16 * (kBlock / 32) + 2 * (kBlock / 32) * sbuf);
+  }
   // CTAs: as many as fit, at least one warp-tile per warp
   static const int grid_cap = [] {  // GBE_STREAM_PER_SM: CTAs per SM cap (tuning knob: the window of
     const char *e = std::getenv("GBE_STREAM_PER_SM");  // tiles in flight against L2 re-use)

@@ -37,6 +37,11 @@ struct StreamDesc {
   int64_t hrow[32];                // output-row stride of each high digit
   int64_t pf_bytes[32];            // bytes of input j's tile slice to prefetch into L2 (0: none)
   int64_t shift[32];
+  // staged mode: dynamic shared memory = [k*PL offset table][per-warp
+  // mbarrier pairs at stg_off][per-warp buffer pairs of stg_buf bytes];
+  // input j's slice (stg_slice bytes) at stg_soff within a buffer
+  int32_t stg_off, stg_buf;
+  int32_t stg_soff[32], stg_slice[32];
 };
 
 struct BksLaunch {
@@ -50,12 +55,15 @@ struct BksLaunch {
   bool pf_ok = false;   // some input's tile slice can be prefetched into L2 (dense, canonical layout)
   bool pf = false;      // prefetch on (default: k >= 2 inputs; the executor's autotuning may flip it)
   int sms = 1;          // SMs of the device (the grid is one wave of resident CTAs)
+  bool stg = false;     // staged mode: per-warp TMA double buffers of the input slices
   int64_t t0 = 0, ntiles = 0;
 };
 
 // false when the descriptor does not fit (more than 32 high digits of radix > 1)
+// stage: build the staged-mode descriptor (false when the slices are not
+// dense ranges or d is outside 2..5 or sum-product)
 bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int num_sms, StreamDesc &S,
-               BksLaunch &L);
+               BksLaunch &L, bool stage = false);
 cudaError_t bks_launch(const StreamDesc *dev_s, const BksLaunch &L, const InPtrs &in, void *out, uint8_t *arg,
                        int64_t row_begin, int64_t row_end, cudaStream_t s);
 // lanes that split one row's domain (1 for d <= 5, up to 32)

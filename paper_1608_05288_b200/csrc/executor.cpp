@@ -98,6 +98,12 @@ struct DevPlan {
   std::vector<BksLaunch> sl;
   std::vector<char> use_stream;
   StreamDesc *d_stream = nullptr;
+  // the streaming kernel's staged mode (per-warp TMA double buffers): its
+  // own descriptors (smaller warp-tiles); use_stage picks it for a task
+  std::vector<StreamDesc> h_stage;
+  std::vector<BksLaunch> sl3;
+  std::vector<char> use_stage;
+  StreamDesc *d_stage = nullptr;
   // autotuning (exec option "autotune", kernel auto): a task with more than
   // one candidate launch -- the tiled kernel, the streaming kernel with and
   // without its L2 prefetch -- runs candidate p mod nc on tuning solve p
@@ -108,6 +114,7 @@ struct DevPlan {
   struct Cand {
     int variant;  // 1 tiled, 2 streaming
     bool pf;      // streaming: L2 prefetch of the next tile's slices
+    bool stage;   // streaming: staged mode
   };
   std::vector<std::vector<Cand>> cands;  // [task]: candidate 0 = the default choice
   std::vector<std::vector<float>> t_cand;
@@ -245,6 +252,7 @@ struct DevPlan {
     for (auto e : c_ev) if (e) cudaEventDestroy(e);
     cudaFree(d_fast);
     cudaFree(d_stream);
+    cudaFree(d_stage);
     cudaFree(d_off);
     cudaFree(d_poff);
     cudaFree(d_prad);
@@ -707,6 +715,9 @@ static DevPlan *dev_plan(gbe_plan *gp) {
   D->h_stream.resize(P.tasks.size());
   D->sl.resize(P.tasks.size());
   D->use_stream.assign(P.tasks.size(), 0);
+  D->h_stage.resize(P.tasks.size());
+  D->sl3.resize(P.tasks.size());
+  D->use_stage.assign(P.tasks.size(), 0);
   D->cands.assign(P.tasks.size(), {});
   D->t_cand.assign(P.tasks.size(), {});
   D->tune_nc = 0;
@@ -737,11 +748,21 @@ static DevPlan *dev_plan(gbe_plan *gp) {
                          bkf_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_fast[ti], D->fl[ti], noinf);
     const bool stream_ok = (want == -1 || want == 2) && !P.ex.count &&
                            bks_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_stream[ti], D->sl[ti]);
-    if (fast_ok && (!stream_ok || !prefer_stream(h, D->fl[ti]))) {
+    // staged mode (GBE_STREAM_STAGE: unset/0 never -- measured 2-4x slower
+    // on C5 and C4-d4; 1 the default wherever it fits; 2 an
+    // autotuning candidate)
+    static const int stage_env = [] {
+      const char *e = std::getenv("GBE_STREAM_STAGE");
+      return e ? std::atoi(e) : 0;
+    }();
+    const bool stage_ok = stream_ok && stage_env != 0 && !P.ex.host_args && !P.ex.spill &&
+                          bks_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_stage[ti], D->sl3[ti], true);
+    if (fast_ok && (!stream_ok || !prefer_stream(h, D->fl[ti])) && !(stage_ok && stage_env == 1)) {
       D->use_fast[ti] = 1;
       D->launch[ti].variant = 1;
     } else if (stream_ok) {
       D->use_stream[ti] = 1;
+      D->use_stage[ti] = stage_ok && stage_env == 1;
       D->launch[ti].variant = 2;
     }
     // autotuning candidates: the default first, then the other variant and
@@ -751,10 +772,12 @@ static DevPlan *dev_plan(gbe_plan *gp) {
       static const bool pf_forced = std::getenv("GBE_STREAM_PF") != nullptr;
       auto &cs = D->cands[ti];
       const bool pf = D->sl[ti].pf, pf_alt = stream_ok && D->sl[ti].pf_ok && !pf_forced;
-      if (D->use_fast[ti]) cs.push_back({1, false});
-      if (stream_ok) cs.push_back({2, pf});
-      if (fast_ok && !D->use_fast[ti]) cs.push_back({1, false});
-      if (pf_alt) cs.push_back({2, !pf});
+      if (D->use_fast[ti]) cs.push_back({1, false, false});
+      if (D->use_stage[ti]) cs.push_back({2, false, true});
+      if (stream_ok) cs.push_back({2, pf, false});
+      if (fast_ok && !D->use_fast[ti]) cs.push_back({1, false, false});
+      if (pf_alt) cs.push_back({2, !pf, false});
+      if (stage_ok && !D->use_stage[ti]) cs.push_back({2, false, true});
       if (cs.size() < 2) cs.clear();
       if (!cs.empty()) {
         D->tune_phase = 0;
@@ -819,6 +842,9 @@ static DevPlan *dev_plan(gbe_plan *gp) {
   CK(cudaMalloc(&D->d_stream, sizeof(StreamDesc) * std::max<size_t>(P.tasks.size(), 1)));
   if (!P.tasks.empty())
     CK(cudaMemcpy(D->d_stream, D->h_stream.data(), sizeof(StreamDesc) * P.tasks.size(), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&D->d_stage, sizeof(StreamDesc) * std::max<size_t>(P.tasks.size(), 1)));
+  if (!P.tasks.empty())
+    CK(cudaMemcpy(D->d_stage, D->h_stage.data(), sizeof(StreamDesc) * P.tasks.size(), cudaMemcpyHostToDevice));
   CK(cudaMalloc(&D->d_fast, sizeof(FastDesc) * std::max<size_t>(P.tasks.size(), 1)));
   if (!P.tasks.empty())
     CK(cudaMemcpy(D->d_fast, D->h_fast.data(), sizeof(FastDesc) * P.tasks.size(), cudaMemcpyHostToDevice));
@@ -1069,6 +1095,7 @@ static void run_util(RunImpl &R) {
         const DevPlan::Cand c = D->cands[ti][ci < (int)D->cands[ti].size() ? ci : 0];
         D->use_fast[ti] = c.variant == 1;
         D->use_stream[ti] = c.variant == 2;
+        D->use_stage[ti] = c.stage;
         D->sl[ti].pf = c.pf;
       }
   }
@@ -1274,7 +1301,8 @@ static void run_util(RunImpl &R) {
         if (D->use_fast[ti])
           CK(bkf_launch(D->d_fast + ti, D->fl[ti], ins[ti], out, argp, sh.lo, st));
         else
-          CK(bks_launch(D->d_stream + ti, D->sl[ti], ins[ti], out, argp, sh.lo, sh.hi, st));
+          CK(D->use_stage[ti] ? bks_launch(D->d_stage + ti, D->sl3[ti], ins[ti], out, argp, sh.lo, sh.hi, st)
+                              : bks_launch(D->d_stream + ti, D->sl[ti], ins[ti], out, argp, sh.lo, sh.hi, st));
         CK(cudaEventRecord(D->tune_ev[2 * ti + 1], st));
       } else if (P.ex.count)
         CK(bk_count_launch(D->h_desc[ti], D->d_desc + ti, ins[ti], cins[ti], out,
@@ -1282,7 +1310,8 @@ static void run_util(RunImpl &R) {
       else if (D->use_fast[ti])
         CK(bkf_launch(D->d_fast + ti, D->fl[ti], ins[ti], out, argp, sh.lo, st));
       else if (D->use_stream[ti])
-        CK(bks_launch(D->d_stream + ti, D->sl[ti], ins[ti], out, argp, sh.lo, sh.hi, st));
+        CK(D->use_stage[ti] ? bks_launch(D->d_stage + ti, D->sl3[ti], ins[ti], out, argp, sh.lo, sh.hi, st)
+                            : bks_launch(D->d_stream + ti, D->sl[ti], ins[ti], out, argp, sh.lo, sh.hi, st));
       else
         CK(bk_launch(D->h_desc[ti], D->d_desc + ti, ins[ti], out, argp, sh.lo, sh.hi, D->launch[ti], st));
       if (P.ex.timing) rec(ev[3 * ti + 2]);
@@ -1398,6 +1427,7 @@ static void run_util(RunImpl &R) {
           if (D->t_cand[ti][c] < 0.97f * D->t_cand[ti][0] && D->t_cand[ti][c] < D->t_cand[ti][best]) best = c;
         D->use_fast[ti] = cs[best].variant == 1;
         D->use_stream[ti] = cs[best].variant == 2;
+        D->use_stage[ti] = cs[best].stage;
         D->sl[ti].pf = cs[best].pf;
         D->launch[ti].variant = cs[best].variant;
       }
@@ -1580,7 +1610,8 @@ static std::string stats_json(const RunImpl &R) {
     o << (ti ? "," : "") << "{\"var\":" << t.var << ",\"mb\":" << t.mb << ",\"rows\":" << local
       << ",\"d\":" << t.d << ",\"k\":" << t.desc.ninputs << ",\"cells\":" << local * t.d
       << ",\"bytes\":" << bytes << ",\"variant\":" << R.D->launch[ti].variant
-      << ",\"k_eff\":" << R.D->h_desc[ti].ninputs << ",\"merges\":" << R.D->task_merges[ti].size();
+      << ",\"k_eff\":" << R.D->h_desc[ti].ninputs << ",\"merges\":" << R.D->task_merges[ti].size()
+      << ",\"staged\":" << (R.D->use_stream[ti] && R.D->use_stage[ti] ? "true" : "false");
     if (R.D->use_fast[ti]) {
       const FastHot &fh = R.D->h_fast[ti].hot;
       o << ",\"tile_rows\":" << fh.PL << ",\"stages\":" << fh.nstages << ",\"staging_bufs\":" << fh.nout
@@ -1742,7 +1773,7 @@ int bucket_kernel_variant(const gbe_bucket_desc *h, int64_t row_begin, int64_t r
 // the bare hot primitive
 void bucket_kernel(const gbe_bucket_desc *h, const void *const *dev_inputs, void *dev_out,
                    uint8_t *dev_arg, int64_t row_begin, int64_t row_end, void *stream, int variant) {
-  if (variant < -1 || variant > 2) GBE_FAIL(GBE_E_INVALID, "variant must be -1, 0, 1 or 2");
+  if (variant < -1 || variant > 3) GBE_FAIL(GBE_E_INVALID, "variant must be -1, 0, 1, 2 or 3");
   if (!h) GBE_FAIL(GBE_E_INVALID, "null descriptor");
   if (h->semiring != GBE_MINSUM_I32 && h->semiring != GBE_MINSUM_F64 && h->semiring != GBE_SUMPROD_F64)
     GBE_FAIL(GBE_E_INVALID, "bad semiring");
@@ -1765,6 +1796,22 @@ void bucket_kernel(const gbe_bucket_desc *h, const void *const *dev_inputs, void
   InPtrs in{};
   for (int j = 0; j < h->ninputs; j++) in.p[j] = dev_inputs[j];
   const int var = variant >= 0 ? variant : bucket_kernel_variant(h, row_begin, row_end);
+  if (var == 3) {  // streaming, staged mode
+    StreamDesc *Sd = new StreamDesc();
+    BksLaunch sl;
+    const bool ok = bks_build(*h, row_begin, row_end, nsm, *Sd, sl, true);
+    if (ok) {
+      StreamDesc *d_s = (StreamDesc *)dalloc(sizeof(StreamDesc), s);
+      cudaError_t e = cudaMemcpyAsync(d_s, Sd, sizeof(StreamDesc), cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess) e = bks_launch(d_s, sl, in, dev_out, dev_arg, row_begin, row_end, s);
+      dfree(d_s, s);
+      delete Sd;
+      CK(e);
+      return;
+    }
+    delete Sd;
+    GBE_FAIL(GBE_E_INVALID, "the staged streaming kernel does not fit this descriptor");
+  }
   if (var == 2) {  // streaming
     StreamDesc *Sd = new StreamDesc();
     BksLaunch sl;

@@ -340,7 +340,8 @@ class Run:
 
 def bucket_kernel(desc: BucketDesc, inputs, out, arg, row_begin, row_end, stream=None, variant=-1):
     """The hot primitive on device pointers (ints) or torch tensors; variant
-    -1 auto, 0 generic, 1 tiled TMA, 2 streaming (gbe_bucket_kernel_ex)."""
+    -1 auto, 0 generic, 1 tiled TMA, 2 streaming, 3 streaming staged
+    (gbe_bucket_kernel_ex)."""
     def p(x):
         if x is None:
             return None

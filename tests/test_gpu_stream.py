@@ -337,3 +337,116 @@ def test_stream_high_broadcast_digits(dom_sep, lacks, d, f64):
             check(out.cpu().numpy(), arg.cpu().numpy(), exp[rb:re], ea[rb:re], f64, dom, m, members, sep, rb)
     finally:
         del os.environ["GBE_STREAM_BD2"]
+
+
+def run_variant(D, members, f64, rb, re, variant):
+    dt = torch.float64 if f64 else torch.int32
+    ins = [torch.tensor(np.asarray(t), dtype=dt, device="cuda") for _, t in members]
+    out = torch.empty(max(re - rb, 1), dtype=dt, device="cuda")
+    arg = torch.empty(max(re - rb, 1), dtype=torch.uint8, device="cuda")
+    G.bucket_kernel(D, ins, out, arg, rb, re, variant=variant)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()[:re - rb], arg.cpu().numpy()[:re - rb]
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_staged_random_descriptors(seed):
+    """The streaming kernel's staged mode (variant 3: per-warp TMA double
+    buffers of the tile's input slices, shared-memory loads): random
+    canonical descriptors, d = 2..5, int32 with INF cells and f64, full and
+    ragged partial row ranges, against the oracle."""
+    rng = np.random.default_rng(4100 + seed)
+    f64 = seed % 2 == 1
+    m = int(rng.integers(1, 10))
+    dom_sep = [int(v) for v in rng.integers(1, 5, m)]
+    d = int(rng.integers(2, 6))
+    dom, sep, x, members = bucket(rng, dom_sep, d, int(rng.integers(1, 7)), f64)
+    D, rows = desc_for(dom, sep, x, members, G.MINSUM_F64 if f64 else G.MINSUM_I32)
+    for rb, re in [(0, rows), (int(rng.integers(0, rows)), rows)]:
+        re = max(re, rb + 1)
+        got, ga = run_variant(D, members, f64, rb, re, 3)
+        exp, ea = oracle.bucket_eval(dom, f64, x, members, sep, rb, re)
+        check(got, ga, exp, ea, f64, dom, x, members, sep, rb)
+
+
+@pytest.mark.parametrize("f64", [False, True])
+def test_staged_many_tiles_per_warp(f64):
+    """Staged mode over 10-25 warp-tiles per warp (both buffers of every
+    warp reused many times: the mbarrier phases flip), one large input
+    lacking a high digit plus small ones, full range and a ragged range, vs
+    the oracle."""
+    rng = np.random.default_rng(4200 + int(f64))
+    if f64:
+        dom_sep, d = [2, 4, 3, 4, 4, 3, 4, 4, 3, 4, 4, 2, 2], 4
+    else:
+        dom_sep, d = [3] * 15, 3
+    m = len(dom_sep)
+    dom = list(dom_sep) + [d]
+    members = []
+    for j, sub in enumerate([list(range(1, m)), [0, 3, m - 1], [2, m - 2], [m - 1]]):
+        scope = sub + [m]
+        cells = int(np.prod([dom[v] for v in scope]))
+        t = rng.uniform(0, 10, cells).round(1) if f64 else rng.integers(0, 40, cells).astype(np.int64)
+        if j == 1:
+            t[rng.random(cells) < 0.05] = np.inf if f64 else INF
+        members.append((scope, t))
+    D, rows = desc_for(dom, list(range(m)), m, members, G.MINSUM_F64 if f64 else G.MINSUM_I32)
+    for rb, re in [(0, rows), (12345, rows - 777)]:
+        got, ga = run_variant(D, members, f64, rb, re, 3)
+        exp, ea = oracle.bucket_eval(dom, f64, m, members, list(range(m)), rb, re)
+        check(got, ga, exp, ea, f64, dom, m, members, list(range(m)), rb)
+
+
+STAGED_SOLVE = r"""
+import json, sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from tests import test_gpu_stream as T
+import gen, oracle, paper_1608_05288_b200 as G
+from gen import configs
+res = []
+for name in ["c2", "bn", "sf_inf"]:
+    inst = configs.c2() if name == "c2" else (gen.belief_net(40, 2, 4, 3, 10, 3) if name == "bn" else gen.scalefree(60, 3, 0.1, 4))
+    P = G.Problem.from_instance(inst)
+    order, _ = P.order()
+    plan = G.Plan(P, order, retain="all", kernel=2)
+    info = plan.info()
+    ok = True
+    for rep in range(2):
+        run_, root = plan.dpop_util()
+        st = run_.stats()
+        staged = sum(1 for t in st["tasks"] if t.get("staged"))
+        ref = oracle.solve_be(inst, order)
+        dom = [int(v) for v in inst.dom]
+        try:
+            for t, (ti, ot) in enumerate(zip(info["tables"], ref.tables)):
+                o, a = run_.table(t, ti["rows"])
+                if inst.is_f64:
+                    mem = [([int(v) for v in inst.scope(i)], inst.table(i)) if kd == 0 else (list(ref.tables[i].sep), ref.tables[i].out)
+                           for kd, i in ot.members]
+                    T.check(o, a, ot.out, ot.arg, True, dom, ot.var, mem, ot.sep)
+                else:
+                    T.check(o, a, ot.out, ot.arg, False)
+            assign = run_.value()
+            if inst.is_f64:
+                ok = ok and abs(root - ref.value) <= 1e-9 * max(1.0, abs(ref.value))
+            else:
+                ok = ok and root == ref.value and list(assign) == list(ref.assignment)
+        except AssertionError:
+            ok = False
+        run_.close()
+    res.append({"name": name, "staged": staged, "ok": ok})
+print(json.dumps(res))
+"""
+
+
+def test_whole_solve_staged():
+    """Whole solves with every bucket the staged mode fits staged
+    (GBE_STREAM_STAGE=1, read once per process: a subprocess): tables,
+    argmins, optimum and assignment against the oracle, two solves per plan
+    (the second a CUDA-graph replay)."""
+    env = dict(os.environ, GBE_STREAM_STAGE="1")
+    r = subprocess.run([sys.executable, "-c", STAGED_SOLVE, ROOT], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert all(x["staged"] > 0 for x in res), res
+    assert all(x["ok"] for x in res), res
