@@ -669,7 +669,11 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
   if (k < 1 || k > 32 || d < 1 || d > GBE_MAX_DOMAIN || row_end <= row_begin) return false;
   // warp-tile: trailing output digits while the CTA's offset table stays
   // <= 32 KB (k * PL int32) and every in-tile offset fits int32
-  const int pl_max = std::max(1, std::min(4096, 8192 / k));
+  static const int pl_cap = [] {  // GBE_STREAM_PLMAX: warp-tile rows cap (tuning knob)
+    const char *e = std::getenv("GBE_STREAM_PLMAX");
+    return e ? std::max(32, std::atoi(e)) : 4096;
+  }();
+  const int pl_max = std::max(1, std::min(pl_cap, 8192 / k));
   int nlow = 0;
   int64_t PL = 1;
   int64_t maxoff[32] = {0};
