@@ -664,7 +664,7 @@ int bks_lanes_per_row(int d) {
 }
 
 bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int num_sms, StreamDesc &S,
-               BksLaunch &L, bool stage) {
+               BksLaunch &L, bool stage, int pl_cap_rows) {
   const int m = h.nsep, k = h.ninputs, d = h.d;
   if (k < 1 || k > 32 || d < 1 || d > GBE_MAX_DOMAIN || row_end <= row_begin) return false;
   // warp-tile: trailing output digits while the CTA's offset table stays
@@ -673,7 +673,7 @@ bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     const char *e = std::getenv("GBE_STREAM_PLMAX");
     return e ? std::max(32, std::atoi(e)) : 4096;
   }();
-  const int pl_max = std::max(1, std::min(pl_cap, 8192 / k));
+  const int pl_max = std::max(1, std::min(pl_cap_rows > 0 ? std::min(pl_cap, pl_cap_rows) : pl_cap, 8192 / k));
   int nlow = 0;
   int64_t PL = 1;
   int64_t maxoff[32] = {0};

@@ -62,8 +62,9 @@ struct BksLaunch {
 // false when the descriptor does not fit (more than 32 high digits of radix > 1)
 // stage: build the staged-mode descriptor (false when the slices are not
 // dense ranges or d is outside 2..5 or sum-product)
+// pl_cap_rows > 0: warp-tiles of at most that many rows
 bool bks_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int num_sms, StreamDesc &S,
-               BksLaunch &L, bool stage = false);
+               BksLaunch &L, bool stage = false, int pl_cap_rows = 0);
 cudaError_t bks_launch(const StreamDesc *dev_s, const BksLaunch &L, const InPtrs &in, void *out, uint8_t *arg,
                        int64_t row_begin, int64_t row_end, cudaStream_t s);
 // lanes that split one row's domain (1 for d <= 5, up to 32)

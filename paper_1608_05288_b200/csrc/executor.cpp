@@ -104,6 +104,20 @@ struct DevPlan {
   std::vector<BksLaunch> sl3;
   std::vector<char> use_stage;
   StreamDesc *d_stage = nullptr;
+  // a second streaming descriptor with warp-tiles of at most half the rows
+  // (an autotuning candidate: C5 x77 1.36 -> 1.10 ms, C4-d4 x27 0.91 -> 0.71
+  // ms, while x91 / x80 lose with it); use_half picks it for a task
+  std::vector<StreamDesc> h_half;
+  std::vector<BksLaunch> slh;
+  std::vector<char> use_half;
+  StreamDesc *d_half = nullptr;
+  // the streaming launch of task ti with the descriptor its choice names
+  cudaError_t stream_launch(size_t ti, const InPtrs &in, void *out, uint8_t *arg, int64_t lo, int64_t hi,
+                            cudaStream_t st) const {
+    if (use_stage[ti]) return bks_launch(d_stage + ti, sl3[ti], in, out, arg, lo, hi, st);
+    if (use_half[ti]) return bks_launch(d_half + ti, slh[ti], in, out, arg, lo, hi, st);
+    return bks_launch(d_stream + ti, sl[ti], in, out, arg, lo, hi, st);
+  }
   // autotuning (exec option "autotune", kernel auto): a task with more than
   // one candidate launch -- the tiled kernel, the streaming kernel with and
   // without its L2 prefetch -- runs candidate p mod nc on tuning solve p
@@ -115,6 +129,7 @@ struct DevPlan {
     int variant;  // 1 tiled, 2 streaming
     bool pf;      // streaming: L2 prefetch of the next tile's slices
     bool stage;   // streaming: staged mode
+    bool half;    // streaming: the half-tile descriptor
   };
   std::vector<std::vector<Cand>> cands;  // [task]: candidate 0 = the default choice
   std::vector<std::vector<float>> t_cand;
@@ -253,6 +268,7 @@ struct DevPlan {
     cudaFree(d_fast);
     cudaFree(d_stream);
     cudaFree(d_stage);
+    cudaFree(d_half);
     cudaFree(d_off);
     cudaFree(d_poff);
     cudaFree(d_prad);
@@ -718,6 +734,9 @@ static DevPlan *dev_plan(gbe_plan *gp) {
   D->h_stage.resize(P.tasks.size());
   D->sl3.resize(P.tasks.size());
   D->use_stage.assign(P.tasks.size(), 0);
+  D->h_half.resize(P.tasks.size());
+  D->slh.resize(P.tasks.size());
+  D->use_half.assign(P.tasks.size(), 0);
   D->cands.assign(P.tasks.size(), {});
   D->t_cand.assign(P.tasks.size(), {});
   D->tune_nc = 0;
@@ -772,12 +791,25 @@ static DevPlan *dev_plan(gbe_plan *gp) {
       static const bool pf_forced = std::getenv("GBE_STREAM_PF") != nullptr;
       auto &cs = D->cands[ti];
       const bool pf = D->sl[ti].pf, pf_alt = stream_ok && D->sl[ti].pf_ok && !pf_forced;
-      if (D->use_fast[ti]) cs.push_back({1, false, false});
-      if (D->use_stage[ti]) cs.push_back({2, false, true});
-      if (stream_ok) cs.push_back({2, pf, false});
-      if (fast_ok && !D->use_fast[ti]) cs.push_back({1, false, false});
-      if (pf_alt) cs.push_back({2, !pf, false});
-      if (stage_ok && !D->use_stage[ti]) cs.push_back({2, false, true});
+      if (D->use_fast[ti]) cs.push_back({1, false, false, false});
+      if (D->use_stage[ti]) cs.push_back({2, false, true, false});
+      if (stream_ok) cs.push_back({2, pf, false, false});
+      if (fast_ok && !D->use_fast[ti]) cs.push_back({1, false, false, false});
+      if (pf_alt) cs.push_back({2, !pf, false, false});
+      if (stage_ok && !D->use_stage[ti]) cs.push_back({2, false, true, false});
+      // half-tile streaming descriptor (when it really has shorter tiles)
+      static const bool half_off = [] {
+        const char *e = std::getenv("GBE_STREAM_HALF");
+        return e && std::atoi(e) == 0;
+      }();
+      if (stream_ok && !half_off && D->h_stream[ti].PL >= 64 &&
+          bks_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_half[ti], D->slh[ti], false,
+                    D->h_stream[ti].PL / 2) &&
+          D->h_half[ti].PL < D->h_stream[ti].PL) {
+        const bool hp = D->slh[ti].pf;
+        cs.push_back({2, hp, false, true});
+        if (D->slh[ti].pf_ok && !pf_forced) cs.push_back({2, !hp, false, true});
+      }
       if (cs.size() < 2) cs.clear();
       if (!cs.empty()) {
         D->tune_phase = 0;
@@ -842,6 +874,9 @@ static DevPlan *dev_plan(gbe_plan *gp) {
   CK(cudaMalloc(&D->d_stream, sizeof(StreamDesc) * std::max<size_t>(P.tasks.size(), 1)));
   if (!P.tasks.empty())
     CK(cudaMemcpy(D->d_stream, D->h_stream.data(), sizeof(StreamDesc) * P.tasks.size(), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&D->d_half, sizeof(StreamDesc) * std::max<size_t>(P.tasks.size(), 1)));
+  if (!P.tasks.empty())
+    CK(cudaMemcpy(D->d_half, D->h_half.data(), sizeof(StreamDesc) * P.tasks.size(), cudaMemcpyHostToDevice));
   CK(cudaMalloc(&D->d_stage, sizeof(StreamDesc) * std::max<size_t>(P.tasks.size(), 1)));
   if (!P.tasks.empty())
     CK(cudaMemcpy(D->d_stage, D->h_stage.data(), sizeof(StreamDesc) * P.tasks.size(), cudaMemcpyHostToDevice));
@@ -1096,7 +1131,8 @@ static void run_util(RunImpl &R) {
         D->use_fast[ti] = c.variant == 1;
         D->use_stream[ti] = c.variant == 2;
         D->use_stage[ti] = c.stage;
-        D->sl[ti].pf = c.pf;
+        D->use_half[ti] = c.half;
+        (c.half ? D->slh[ti] : D->sl[ti]).pf = c.pf;
       }
   }
   const bool graph = P.ex.graph && (W == 1 || g_ag_graph) && !g_alloc && !R.arena_own && !P.ex.host_args &&
@@ -1301,8 +1337,7 @@ static void run_util(RunImpl &R) {
         if (D->use_fast[ti])
           CK(bkf_launch(D->d_fast + ti, D->fl[ti], ins[ti], out, argp, sh.lo, st));
         else
-          CK(D->use_stage[ti] ? bks_launch(D->d_stage + ti, D->sl3[ti], ins[ti], out, argp, sh.lo, sh.hi, st)
-                              : bks_launch(D->d_stream + ti, D->sl[ti], ins[ti], out, argp, sh.lo, sh.hi, st));
+          CK(D->stream_launch(ti, ins[ti], out, argp, sh.lo, sh.hi, st));
         CK(cudaEventRecord(D->tune_ev[2 * ti + 1], st));
       } else if (P.ex.count)
         CK(bk_count_launch(D->h_desc[ti], D->d_desc + ti, ins[ti], cins[ti], out,
@@ -1310,8 +1345,7 @@ static void run_util(RunImpl &R) {
       else if (D->use_fast[ti])
         CK(bkf_launch(D->d_fast + ti, D->fl[ti], ins[ti], out, argp, sh.lo, st));
       else if (D->use_stream[ti])
-        CK(D->use_stage[ti] ? bks_launch(D->d_stage + ti, D->sl3[ti], ins[ti], out, argp, sh.lo, sh.hi, st)
-                            : bks_launch(D->d_stream + ti, D->sl[ti], ins[ti], out, argp, sh.lo, sh.hi, st));
+        CK(D->stream_launch(ti, ins[ti], out, argp, sh.lo, sh.hi, st));
       else
         CK(bk_launch(D->h_desc[ti], D->d_desc + ti, ins[ti], out, argp, sh.lo, sh.hi, D->launch[ti], st));
       if (P.ex.timing) rec(ev[3 * ti + 2]);
@@ -1428,7 +1462,8 @@ static void run_util(RunImpl &R) {
         D->use_fast[ti] = cs[best].variant == 1;
         D->use_stream[ti] = cs[best].variant == 2;
         D->use_stage[ti] = cs[best].stage;
-        D->sl[ti].pf = cs[best].pf;
+        D->use_half[ti] = cs[best].half;
+        (cs[best].half ? D->slh[ti] : D->sl[ti]).pf = cs[best].pf;
         D->launch[ti].variant = cs[best].variant;
       }
     }
@@ -1611,7 +1646,8 @@ static std::string stats_json(const RunImpl &R) {
       << ",\"d\":" << t.d << ",\"k\":" << t.desc.ninputs << ",\"cells\":" << local * t.d
       << ",\"bytes\":" << bytes << ",\"variant\":" << R.D->launch[ti].variant
       << ",\"k_eff\":" << R.D->h_desc[ti].ninputs << ",\"merges\":" << R.D->task_merges[ti].size()
-      << ",\"staged\":" << (R.D->use_stream[ti] && R.D->use_stage[ti] ? "true" : "false");
+      << ",\"staged\":" << (R.D->use_stream[ti] && R.D->use_stage[ti] ? "true" : "false")
+      << ",\"half_tiles\":" << (R.D->use_stream[ti] && R.D->use_half[ti] ? "true" : "false");
     if (R.D->use_fast[ti]) {
       const FastHot &fh = R.D->h_fast[ti].hot;
       o << ",\"tile_rows\":" << fh.PL << ",\"stages\":" << fh.nstages << ",\"staging_bufs\":" << fh.nout

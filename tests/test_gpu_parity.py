@@ -375,7 +375,9 @@ def test_graph_replay_matches_oracle(torch_cuda, name, concurrent):
     "concurrent" that graph is the task DAG (sibling subtrees overlap, arena
     ranges reused under DAG edges).  Every replay must equal the oracle: all
     tables and argmins (retain all), optimum + assignment (retain args) and the
-    value-only optimum (retain none, maximum arena reuse)."""
+    value-only optimum (retain none, maximum arena reuse).  Autotuning is off
+    so the graph is captured on the first solve and replayed from the second
+    (with it, the first 2n solves are eager candidate timings)."""
     inst = configs.c2() if name == "c2" else INSTANCES[name]()
     P = G.Problem.from_instance(inst)
     order, _ = P.order()
@@ -384,7 +386,7 @@ def test_graph_replay_matches_oracle(torch_cuda, name, concurrent):
     def same(v):
         return math.isclose(v, orun.value, rel_tol=1e-9) if inst.is_f64 else v == orun.value
 
-    plan = G.Plan(P, order, retain="all", concurrent=concurrent)
+    plan = G.Plan(P, order, retain="all", concurrent=concurrent, autotune=False)
     info = plan.info()
     for rep in range(3):
         run, root = plan.dpop_util()
@@ -392,13 +394,13 @@ def test_graph_replay_matches_oracle(torch_cuda, name, concurrent):
         if rep == 2:
             _check_tables(run, info, orun, inst.is_f64)
         run.close()
-    plan = G.Plan(P, order, concurrent=concurrent)
+    plan = G.Plan(P, order, concurrent=concurrent, autotune=False)
     for rep in range(4):
         opt, a = plan.solve_be()
         assert same(opt), rep
         if not inst.is_f64:
             assert list(a) == list(orun.assignment), rep
-    plan = G.Plan(P, order, retain="none", concurrent=concurrent)
+    plan = G.Plan(P, order, retain="none", concurrent=concurrent, autotune=False)
     for rep in range(4):
         opt, _ = plan.solve_be(assignment=False)
         assert same(opt), rep
@@ -412,12 +414,42 @@ def test_graph_replay_mbe(torch_cuda, ib):
     P = G.Problem.from_instance(inst)
     order, _ = P.order()
     orun = oracle.solve_mbe(inst, order, ib)
-    plan = G.Plan(P, order, ib)
+    plan = G.Plan(P, order, ib, autotune=False)
     for rep in range(4):
         lo, up, a = plan.solve_mbe()
         assert (lo, up) == (orun.value, orun.upper), rep
         assert list(a) == list(orun.assignment), rep
-    plan = G.Plan(P, order, ib, retain="none")
+    plan = G.Plan(P, order, ib, retain="none", autotune=False)
     for rep in range(4):
         lo, _, _ = plan.solve_mbe(assignment=False)
         assert lo == orun.value, rep
+
+
+@pytest.mark.parametrize("name", ["scalefree", "bn", "c2"])
+def test_autotuned_plan_every_solve(torch_cuda, name):
+    """With autotuning on, a plan's first 2n solves run the buckets' candidate
+    launches (tiled, streaming, prefetch flipped, half-length warp-tiles) in
+    turn, eagerly; then the chosen ones are captured and replayed.  Every
+    solve -- each candidate round, the capture and the replays -- must equal
+    the oracle (optimum, assignment), and the tables of the last replay too."""
+    inst = configs.c2() if name == "c2" else INSTANCES[name]()
+    P = G.Problem.from_instance(inst)
+    order, _ = P.order()
+    orun = oracle.solve_be(inst, order)
+    plan = G.Plan(P, order, retain="all")
+    info = plan.info()
+    tuned, replays = 0, 0
+    for rep in range(16):
+        run, root = plan.dpop_util()
+        st = run.stats()
+        tuned += bool(st.get("autotune_solve"))
+        replays += bool(st.get("graph_replay"))
+        if inst.is_f64:
+            assert math.isclose(root, orun.value, rel_tol=1e-9), rep
+        else:
+            assert root == orun.value, rep
+            assert list(run.value()) == list(orun.assignment), rep
+        if rep == 15:
+            _check_tables(run, info, orun, inst.is_f64)
+        run.close()
+    assert tuned >= 2 and replays >= 2, (tuned, replays)
