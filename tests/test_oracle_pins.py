@@ -669,3 +669,16 @@ def test_symbolic_bucket_structure_matches_oracle_tables(seed):
     for t, rt in zip(tabs, ref.tables):
         assert t["var"] == rt.var and t["sep"] == list(rt.sep) and t["rows"] == rt.rows
         assert t["members"] == rt.members
+
+
+def test_fnv1a_published_vectors():
+    """The golden-file table digest (not method arithmetic) is 64-bit FNV-1a:
+    pinned to the algorithm's published test vectors (offset basis for the
+    empty input; "a" and "foobar"), and chaining over several arrays equals
+    hashing their concatenation."""
+    def b(s):
+        return np.frombuffer(s, dtype=np.uint8)
+    assert oracle.fnv1a(b(b"")) == 0xCBF29CE484222325
+    assert oracle.fnv1a(b(b"a")) == 0xAF63DC4C8601EC8C
+    assert oracle.fnv1a(b(b"foobar")) == 0x85944171F73967E8
+    assert oracle.fnv1a(b(b"foo"), b(b"bar")) == oracle.fnv1a(b(b"foobar"))
