@@ -917,18 +917,54 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     // register-blocking shape that minimises the per-cell shared-memory
     // loads sum_j R^-|G \ S_j|; pairs win ties (more reuse per group)
     double bestc = 1e30;
-    int g1 = -1, g2 = -1;
+    int g1 = -1, g2 = -1, bestw = 1 << 30;
     static const bool single_only = std::getenv("GBE_FAST_SINGLE") != nullptr;  // tuning knob
+    // ties on the load cost: the pair whose first warp's 32 output rows
+    // (register-block row 0 of slots q = 0..31) fall in the fewest shared-
+    // memory banks per bank -- the staging stores' conflict degree -- then
+    // the later pair (GBE_FAST_BANKTIE=0: the later pair only)
+    static const bool banktie = [] {
+      const char *e = std::getenv("GBE_FAST_BANKTIE");
+      return !(e && std::atoi(e) == 0);
+    }();
+    std::vector<int64_t> rowst_all(m);
+    {
+      int64_t r = 1;
+      for (int p = m - 1; p >= 0; p--) {
+        rowst_all[p] = r;
+        r *= h.radix[p];
+      }
+    }
+    auto store_ways = [&](int a, int b) {  // max rows of warp 0 per bank
+      if (!banktie) return 0;
+      std::vector<int> mids;
+      for (int p = m - nl; p < m; p++)
+        if (p != a && p != b) mids.push_back(p);
+      int cnt[32] = {0}, w = 0;
+      for (int q = 0; q < 32; q++) {
+        int x = q;
+        int64_t row = 0;
+        for (int e = (int)mids.size() - 1; e >= 0; e--) {
+          row += (int64_t)(x % h.radix[mids[e]]) * rowst_all[mids[e]];
+          x /= h.radix[mids[e]];
+        }
+        if (x) break;  // fewer than 32 slots
+        w = std::max(w, ++cnt[row & 31]);
+      }
+      return w;
+    };
     for (int a = m - nl; a < m && !single_only; a++)
       for (int b = a + 1; b < m; b++) {
         int R = h.radix[a];
         if (h.radix[b] != R || !supported(R, R, DV, es)) continue;
         double c = 0;
         for (int j = 0; j < k; j++) c += 1.0 / ((has(j, a) ? 1 : R) * (has(j, b) ? 1 : R));
-        if (c < bestc - 1e-12 || (c < bestc + 1e-12 && b > g2)) {
+        const int w = (c < bestc + 1e-12) ? store_ways(a, b) : 0;
+        if (c < bestc - 1e-12 || (c < bestc + 1e-12 && (w < bestw || (w == bestw && b > g2)))) {
           bestc = c;
           g1 = a;
           g2 = b;
+          bestw = w;
         }
       }
     if (g1 < 0)
