@@ -297,7 +297,7 @@ __device__ __forceinline__ void combine(const typename SrF<T>::Acc (&P0)[DV],
           m -= log(z);
         }
         outs[l] = S::out(m);
-        args[l] = 0;
+        if (args) args[l] = 0;
       } else {
         Acc best = c[0];
         int bv = 0;
@@ -309,7 +309,7 @@ __device__ __forceinline__ void combine(const typename SrF<T>::Acc (&P0)[DV],
           }
         if (S::kInt) gmax = gmax > best ? gmax : best;  // infinite rows fixed per group
         outs[l] = S::out(best);
-        args[l] = (uint8_t)bv;
+        if (args) args[l] = (uint8_t)bv;
       }
     }
   }
@@ -332,7 +332,7 @@ __device__ __forceinline__ void combine_nf(const uint32_t (&P0)[DV], const uint3
 #pragma unroll
     for (int v = 1; v < DV; v++) m = min(m, key[v]);
     outs[l] = (int32_t)(m >> SH);
-    args[l] = (uint8_t)(m & MASK);
+    if (args) args[l] = (uint8_t)(m & MASK);  // (null only for direct stores without argmins)
   };
   if constexpr (!H1) {
     uint32_t B[R2][DV];  // ((P0 + P2[b]) << SH) + v, shared by every a
@@ -385,7 +385,10 @@ __device__ __forceinline__ void combine_nf(const uint32_t (&P0)[DV], const uint3
 // CS >= 0 fixes the class structure at compile time (bit 3: class 0 present,
 // bits 0-2: classes 1-3 present), so only that combine and those loads are
 // emitted; CS = -1 reads it from the descriptor.
-template <typename T, int R, int R2, int DV, bool SP, bool NF, int NG, int GW, int CS = -1>
+// DS: direct stores -- consumers write rows and argmins straight to global
+// memory (no staging buffers, no storer work), which frees the staging
+// buffers' shared memory for more ring stages
+template <typename T, int R, int R2, int DV, bool SP, bool NF, int NG, int GW, int CS = -1, bool DS = false>
 // (registers: 2 groups of GW = 4 warps + producer + storer put 3 warps on one
 // SM sub-partition: 168 per thread)
 __global__ void __launch_bounds__((NG * GW + 1 + NG) * 32, 1)
@@ -486,6 +489,7 @@ __global__ void __launch_bounds__((NG * GW + 1 + NG) * 32, 1)
   const int PL = f.PL, es = (int)sizeof(T);
   const int nob = f.nout;
 
+  if (DS && warp == NG * GW) return;  // direct stores: no storer work
   if (warp == NG * GW) {  // ---- storer warp: TMA bulk stores of staged tiles ----
     // tiles in CTA order (tile i: group i mod NG, its buffer (i / NG) mod nob);
     // the buffer of tile i - 1 is released once tile i is committed and at
@@ -544,15 +548,15 @@ __global__ void __launch_bounds__((NG * GW + 1 + NG) * 32, 1)
   uint32_t ph = (uint32_t)((g / nst) & 1);
   for (int64_t t = t_begin + blockIdx.x + (int64_t)g * gridDim.x; t < t_end; t += (int64_t)NG * gridDim.x) {
     mbar_wait(&full[s], ph);
-    mbar_wait(&oempty[g][b], oph ^ 1u);  // staging buffer b: previous store has read it
+    if (!DS) mbar_wait(&oempty[g][b], oph ^ 1u);  // staging buffer b: previous store has read it
     const int32_t *sb = sbase + s * 32;
     const int64_t o0 = rowstart[s] - row_begin;
     // staging: element l of this tile lives at index l + sh (16-byte phase of
     // its global address), so the aligned interior is one TMA bulk store
     const int sh = (int)((((uintptr_t)(out + o0)) & 15) / es);
     const int sha = (int)(((uintptr_t)(arg + o0)) & 15);
-    T *outs = (T *)(obase + b * f.out_bytes) + sh;
-    uint8_t *args = abase + b * f.arg_bytes + sha;
+    T *outs = DS ? out + o0 : (T *)(obase + b * f.out_bytes) + sh;
+    uint8_t *args = DS ? (arg ? arg + o0 : nullptr) : abase + b * f.arg_bytes + sha;
     for (int q = ctid; q < Pmid; q += kGT) {
       Acc P0[DV], P1[R][DV], P2[R2][DV], P3[R][R2][DV];
       // class 0 (no group digit): P0[v]
@@ -677,7 +681,7 @@ __global__ void __launch_bounds__((NG * GW + 1 + NG) * 32, 1)
               const int l = loff(a, bb);
               if ((uint32_t)outq[l] >= kInf) {
                 outq[l] = (T)kInf;
-                argq[l] = 0;
+                if (argq) argq[l] = 0;
               }
             }
         }
@@ -685,11 +689,13 @@ __global__ void __launch_bounds__((NG * GW + 1 + NG) * 32, 1)
     }
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);  // input stage free
-    fence_proxy_async_smem();  // staged rows -> async proxy (the storer's bulk copy)
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) {
-      if (ctid == 0) ostart[g][b] = o0;
-      mbar_arrive(&ofull[g][b]);
+    if (!DS) {
+      fence_proxy_async_smem();  // staged rows -> async proxy (the storer's bulk copy)
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) {
+        if (ctid == 0) ostart[g][b] = o0;
+        mbar_arrive(&ofull[g][b]);
+      }
     }
     s += NG;
     if (s >= nst) {
@@ -706,10 +712,10 @@ __global__ void __launch_bounds__((NG * GW + 1 + NG) * 32, 1)
 // ---------------------------------------------------------------------------
 // dispatch table over (semiring, R, DV)
 
-template <typename T, int R, int R2, int DV, bool SP, bool NF, int NG, int GW, int CS = -1>
+template <typename T, int R, int R2, int DV, bool SP, bool NF, int NG, int GW, int CS = -1, bool DS = false>
 cudaError_t launch_one(const FastDesc *d, const InPtrs &in, void *out, uint8_t *arg, int64_t rb,
                        int64_t t0, int64_t t1, int grid, int block, int smem, cudaStream_t s) {
-  auto kern = bk_fast_kernel<T, R, R2, DV, SP, NF, NG, GW, CS>;
+  auto kern = bk_fast_kernel<T, R, R2, DV, SP, NF, NG, GW, CS, DS>;
   // the shared-memory opt-in is per device: one bit per device ordinal
   static std::atomic<uint64_t> attr_set{0};
   int dev = 0;
@@ -739,26 +745,41 @@ cudaError_t launch_333_cs(const FastDesc *d, const InPtrs &in, void *out, uint8_
                           int64_t t1, int grid, int block, int smem, cudaStream_t s) {
   return launch_one<int32_t, 3, 3, 3, false, true, 2, 4, CS>(d, in, out, arg, rb, t0, t1, grid, block, smem, s);
 }
+template <int CS>
+cudaError_t launch_333_cs_ds(const FastDesc *d, const InPtrs &in, void *out, uint8_t *arg, int64_t rb, int64_t t0,
+                             int64_t t1, int grid, int block, int smem, cudaStream_t s) {
+  return launch_one<int32_t, 3, 3, 3, false, true, 2, 4, CS, true>(d, in, out, arg, rb, t0, t1, grid, block, smem,
+                                                                    s);
+}
 using Launch333 = cudaError_t (*)(const FastDesc *, const InPtrs &, void *, uint8_t *, int64_t, int64_t, int64_t,
                                   int, int, int, cudaStream_t);
 constexpr Launch333 kLaunch333[16] = {
     launch_333_cs<0>, launch_333_cs<1>, launch_333_cs<2>,  launch_333_cs<3>,  launch_333_cs<4>,  launch_333_cs<5>,
     launch_333_cs<6>, launch_333_cs<7>, launch_333_cs<8>,  launch_333_cs<9>,  launch_333_cs<10>, launch_333_cs<11>,
     launch_333_cs<12>, launch_333_cs<13>, launch_333_cs<14>, launch_333_cs<15>};
+constexpr Launch333 kLaunch333ds[16] = {
+    launch_333_cs_ds<0>,  launch_333_cs_ds<1>,  launch_333_cs_ds<2>,  launch_333_cs_ds<3>,
+    launch_333_cs_ds<4>,  launch_333_cs_ds<5>,  launch_333_cs_ds<6>,  launch_333_cs_ds<7>,
+    launch_333_cs_ds<8>,  launch_333_cs_ds<9>,  launch_333_cs_ds<10>, launch_333_cs_ds<11>,
+    launch_333_cs_ds<12>, launch_333_cs_ds<13>, launch_333_cs_ds<14>, launch_333_cs_ds<15>};
 
 template <typename T, bool SP, bool NF>
 cudaError_t dispatch(int R, int R2, int DV, int NGr, const FastDesc *d, const InPtrs &in, void *out,
                      uint8_t *arg, int64_t rb, int64_t t0, int64_t t1, int grid, int block,
-                     int smem, cudaStream_t s, int cs = -1) {
+                     int smem, cudaStream_t s, int cs = -1, bool ds = false) {
   if constexpr (sizeof(T) == 4 && NF && !SP) {
     static const bool cs_off = std::getenv("GBE_FAST_NO_CS") != nullptr;  // A/B knob
-    if (R == 3 && R2 == 3 && DV == 3 && cs >= 0 && !cs_off)
+    if (ds && R == 3 && R2 == 3 && DV == 3 && cs >= 0)
+      return kLaunch333ds[cs](d, in, out, arg, rb, t0, t1, grid, block, smem, s);
+    if (!ds && R == 3 && R2 == 3 && DV == 3 && cs >= 0 && !cs_off)
       return kLaunch333[cs](d, in, out, arg, rb, t0, t1, grid, block, smem, s);
   }
 #define GBE_CASE(r, r2, dv)                                                                                  \
   if (R == r && R2 == r2 && DV == dv) {                                                                      \
     constexpr int ng = ng_of((int)sizeof(T), r, r2, dv), gw = gw_of((int)sizeof(T), r, r2, dv);             \
     if (NGr != ng) return cudaErrorInvalidValue;                                                             \
+    if (ds) return launch_one<T, r, r2, dv, SP, NF, ng, gw, -1, true>(d, in, out, arg, rb, t0, t1, grid, block, \
+                                                                      smem, s);                              \
     return launch_one<T, r, r2, dv, SP, NF, ng, gw>(d, in, out, arg, rb, t0, t1, grid, block, smem, s);      \
   }
   GBE_CASE(2, 2, 2) GBE_CASE(2, 2, 3) GBE_CASE(2, 2, 4) GBE_CASE(2, 2, 5) GBE_CASE(3, 3, 2) GBE_CASE(3, 3, 3)
@@ -871,7 +892,7 @@ void build_qperm(FastDesc &F, int es, int R, int R2, int Pmid, int64_t rows) {
 }  // namespace
 
 bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int num_sms,
-               FastDesc &F, BkfLaunch &L, bool noinf) {
+               FastDesc &F, BkfLaunch &L, bool noinf, bool ds) {
   const int m = h.nsep, k = h.ninputs, DV = h.d;
   const int es = h.semiring == GBE_MINSUM_I32 ? 4 : 8;
   if (m < 2 || k < 1 || k > 32 || DV < 2 || DV > 5) return false;
@@ -953,14 +974,31 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
       }
       return w;
     };
+    // GBE_FAST_BANKTOL (tuning knob): also accept pairs whose load cost is
+    // within that fraction of the best when their stores conflict less
+    static const double banktol = [] {
+      const char *e = std::getenv("GBE_FAST_BANKTOL");
+      return e ? std::atof(e) : 0.0;
+    }();
+    double minc = 1e30;
     for (int a = m - nl; a < m && !single_only; a++)
       for (int b = a + 1; b < m; b++) {
         int R = h.radix[a];
         if (h.radix[b] != R || !supported(R, R, DV, es)) continue;
         double c = 0;
         for (int j = 0; j < k; j++) c += 1.0 / ((has(j, a) ? 1 : R) * (has(j, b) ? 1 : R));
-        const int w = (c < bestc + 1e-12) ? store_ways(a, b) : 0;
-        if (c < bestc - 1e-12 || (c < bestc + 1e-12 && (w < bestw || (w == bestw && b > g2)))) {
+        minc = std::min(minc, c);
+      }
+    const double cap = minc * (1.0 + banktol) + 1e-12;
+    for (int a = m - nl; a < m && !single_only; a++)
+      for (int b = a + 1; b < m; b++) {
+        int R = h.radix[a];
+        if (h.radix[b] != R || !supported(R, R, DV, es)) continue;
+        double c = 0;
+        for (int j = 0; j < k; j++) c += 1.0 / ((has(j, a) ? 1 : R) * (has(j, b) ? 1 : R));
+        if (c > cap) continue;
+        const int w = store_ways(a, b);
+        if (w < bestw || (w == bestw && (c < bestc - 1e-12 || (c < bestc + 1e-12 && b > g2)))) {
           bestc = c;
           g1 = a;
           g2 = b;
@@ -1085,7 +1123,7 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
       const char *e = std::getenv("GBE_FAST_NOUT");
       return e ? std::max(1, std::min(kOutBufsMax, std::atoi(e))) : kOutBufsMax;
     }();
-    int nob = kNob;
+    int nob = ds ? 0 : kNob;  // direct stores: no staging buffers
     while (nob > std::min(2, kNob) && obuf * nob + tabs + (size_t)min_st * off > kSmemMax) nob--;
     f.nout = nob;
     size_t fixed = obuf * nob + tabs;
@@ -1119,6 +1157,7 @@ bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int
     L.g1 = g1;
     L.g2 = g2;
     L.nf = noinf && es == 4 && h.semiring == GBE_MINSUM_I32;
+    L.ds = ds;
     L.block = (NG * GW + 1 + NG) * 32;
     L.t_begin = row_begin / PL;
     L.t_end = row_end / PL;
@@ -1142,15 +1181,15 @@ cudaError_t bkf_launch(const FastDesc *dev_f, const BkfLaunch &L, const InPtrs &
                        uint8_t *arg, int64_t row_begin, cudaStream_t s) {
   if (L.sp)
     return dispatch<double, true, false>(L.R, L.R2, L.DV, L.NG, dev_f, in, out, arg, row_begin, L.t_begin,
-                                         L.t_end, L.grid, L.block, L.smem, s);
+                                         L.t_end, L.grid, L.block, L.smem, s, -1, L.ds);
   if (L.es == 8)
     return dispatch<double, false, false>(L.R, L.R2, L.DV, L.NG, dev_f, in, out, arg, row_begin, L.t_begin,
-                                          L.t_end, L.grid, L.block, L.smem, s);
+                                          L.t_end, L.grid, L.block, L.smem, s, -1, L.ds);
   if (L.nf)
     return dispatch<int32_t, false, true>(L.R, L.R2, L.DV, L.NG, dev_f, in, out, arg, row_begin, L.t_begin,
-                                          L.t_end, L.grid, L.block, L.smem, s, L.cs);
+                                          L.t_end, L.grid, L.block, L.smem, s, L.cs, L.ds);
   return dispatch<int32_t, false, false>(L.R, L.R2, L.DV, L.NG, dev_f, in, out, arg, row_begin, L.t_begin,
-                                         L.t_end, L.grid, L.block, L.smem, s);
+                                         L.t_end, L.grid, L.block, L.smem, s, -1, L.ds);
 }
 
 }  // namespace gbe

@@ -49,12 +49,13 @@ struct BkfLaunch {
   int NG = 1;       // consumer groups per CTA
   int g1 = -1, g2 = -1;  // group (register-blocking) digits
   int cs = -1;           // class structure (bit 3: class 0 present, bits 0-2: classes 1-3)
+  bool ds = false;       // direct stores: consumers write rows + argmins to global memory (no staging buffers)
   int grid = 1, block = 256, smem = 0;
   int64_t t_begin = 0, t_end = 0;
 };
 
 bool bkf_build(const gbe_bucket_desc &h, int64_t row_begin, int64_t row_end, int num_sms,
-               FastDesc &F, BkfLaunch &L, bool noinf = false);
+               FastDesc &F, BkfLaunch &L, bool noinf = false, bool ds = false);
 cudaError_t bkf_launch(const FastDesc *dev_f, const BkfLaunch &L, const InPtrs &in, void *out,
                        uint8_t *arg, int64_t row_begin, cudaStream_t s);
 

@@ -92,6 +92,12 @@ struct DevPlan {
   std::vector<gbe_bucket_desc> h_desc;
   std::vector<BkLaunchInfo> launch;
   std::vector<FastDesc> h_fast;
+  // direct-store descriptors of the tiled kernel (an autotuning candidate
+  // for the hot int32 shape: no staging buffers, more ring stages)
+  std::vector<FastDesc> h_fds;
+  std::vector<BkfLaunch> fl_ds;
+  std::vector<char> use_ds;
+  FastDesc *d_fds = nullptr;
   std::vector<BkfLaunch> fl;
   std::vector<char> use_fast;
   std::vector<StreamDesc> h_stream;  // streaming kernel (bk_stream.cu) descriptors
@@ -130,6 +136,7 @@ struct DevPlan {
     bool pf;      // streaming: L2 prefetch of the next tile's slices
     bool stage;   // streaming: staged mode
     bool half;    // streaming: the half-tile descriptor
+    bool ds = false;  // tiled: direct stores
   };
   std::vector<std::vector<Cand>> cands;  // [task]: candidate 0 = the default choice
   std::vector<std::vector<float>> t_cand;
@@ -266,6 +273,7 @@ struct DevPlan {
     for (auto e : tune_ev) cudaEventDestroy(e);
     for (auto e : c_ev) if (e) cudaEventDestroy(e);
     cudaFree(d_fast);
+    cudaFree(d_fds);
     cudaFree(d_stream);
     cudaFree(d_stage);
     cudaFree(d_half);
@@ -726,6 +734,9 @@ static DevPlan *dev_plan(gbe_plan *gp) {
   D->h_desc.resize(P.tasks.size());
   D->launch.resize(P.tasks.size());
   D->h_fast.resize(P.tasks.size());
+  D->h_fds.resize(P.tasks.size());
+  D->fl_ds.resize(P.tasks.size());
+  D->use_ds.assign(P.tasks.size(), 0);
   D->fl.resize(P.tasks.size());
   D->use_fast.assign(P.tasks.size(), 0);
   D->h_stream.resize(P.tasks.size());
@@ -797,6 +808,13 @@ static DevPlan *dev_plan(gbe_plan *gp) {
       if (fast_ok && !D->use_fast[ti]) cs.push_back({1, false, false, false});
       if (pf_alt) cs.push_back({2, !pf, false, false});
       if (stage_ok && !D->use_stage[ti]) cs.push_back({2, false, true, false});
+      // direct-store tiled descriptor (hot int32 shape; GBE_FAST_DS=0: off)
+      static const bool ds_off = [] {
+        const char *e = std::getenv("GBE_FAST_DS");
+        return e && std::atoi(e) == 0;
+      }();
+      if (fast_ok && !ds_off && bkf_build(h, t.shard.lo, t.shard.hi, D->num_sms, D->h_fds[ti], D->fl_ds[ti], noinf, true))
+        cs.push_back({1, false, false, false, true});
       // half-tile streaming descriptor (when it really has shorter tiles)
       static const bool half_off = [] {
         const char *e = std::getenv("GBE_STREAM_HALF");
@@ -880,6 +898,9 @@ static DevPlan *dev_plan(gbe_plan *gp) {
   CK(cudaMalloc(&D->d_stage, sizeof(StreamDesc) * std::max<size_t>(P.tasks.size(), 1)));
   if (!P.tasks.empty())
     CK(cudaMemcpy(D->d_stage, D->h_stage.data(), sizeof(StreamDesc) * P.tasks.size(), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&D->d_fds, sizeof(FastDesc) * std::max<size_t>(P.tasks.size(), 1)));
+  if (!P.tasks.empty())
+    CK(cudaMemcpy(D->d_fds, D->h_fds.data(), sizeof(FastDesc) * P.tasks.size(), cudaMemcpyHostToDevice));
   CK(cudaMalloc(&D->d_fast, sizeof(FastDesc) * std::max<size_t>(P.tasks.size(), 1)));
   if (!P.tasks.empty())
     CK(cudaMemcpy(D->d_fast, D->h_fast.data(), sizeof(FastDesc) * P.tasks.size(), cudaMemcpyHostToDevice));
@@ -1132,6 +1153,7 @@ static void run_util(RunImpl &R) {
         D->use_stream[ti] = c.variant == 2;
         D->use_stage[ti] = c.stage;
         D->use_half[ti] = c.half;
+        D->use_ds[ti] = c.ds;
         (c.half ? D->slh[ti] : D->sl[ti]).pf = c.pf;
       }
   }
@@ -1335,7 +1357,8 @@ static void run_util(RunImpl &R) {
       } else if (tuning && !D->cands[ti].empty()) {
         CK(cudaEventRecord(D->tune_ev[2 * ti], st));
         if (D->use_fast[ti])
-          CK(bkf_launch(D->d_fast + ti, D->fl[ti], ins[ti], out, argp, sh.lo, st));
+          CK(D->use_ds[ti] ? bkf_launch(D->d_fds + ti, D->fl_ds[ti], ins[ti], out, argp, sh.lo, st)
+                           : bkf_launch(D->d_fast + ti, D->fl[ti], ins[ti], out, argp, sh.lo, st));
         else
           CK(D->stream_launch(ti, ins[ti], out, argp, sh.lo, sh.hi, st));
         CK(cudaEventRecord(D->tune_ev[2 * ti + 1], st));
@@ -1343,7 +1366,8 @@ static void run_util(RunImpl &R) {
         CK(bk_count_launch(D->h_desc[ti], D->d_desc + ti, ins[ti], cins[ti], out,
                            (double *)(R.base + R.A->off_cnt[ti]), argp, sh.lo, sh.hi, P.ex.count == 2, st));
       else if (D->use_fast[ti])
-        CK(bkf_launch(D->d_fast + ti, D->fl[ti], ins[ti], out, argp, sh.lo, st));
+        CK(D->use_ds[ti] ? bkf_launch(D->d_fds + ti, D->fl_ds[ti], ins[ti], out, argp, sh.lo, st)
+                         : bkf_launch(D->d_fast + ti, D->fl[ti], ins[ti], out, argp, sh.lo, st));
       else if (D->use_stream[ti])
         CK(D->stream_launch(ti, ins[ti], out, argp, sh.lo, sh.hi, st));
       else
@@ -1463,6 +1487,7 @@ static void run_util(RunImpl &R) {
         D->use_stream[ti] = cs[best].variant == 2;
         D->use_stage[ti] = cs[best].stage;
         D->use_half[ti] = cs[best].half;
+        D->use_ds[ti] = cs[best].ds;
         (cs[best].half ? D->slh[ti] : D->sl[ti]).pf = cs[best].pf;
         D->launch[ti].variant = cs[best].variant;
       }
@@ -1649,8 +1674,9 @@ static std::string stats_json(const RunImpl &R) {
       << ",\"staged\":" << (R.D->use_stream[ti] && R.D->use_stage[ti] ? "true" : "false")
       << ",\"half_tiles\":" << (R.D->use_stream[ti] && R.D->use_half[ti] ? "true" : "false");
     if (R.D->use_fast[ti]) {
-      const FastHot &fh = R.D->h_fast[ti].hot;
+      const FastHot &fh = (R.D->use_ds[ti] ? R.D->h_fds[ti] : R.D->h_fast[ti]).hot;
       o << ",\"tile_rows\":" << fh.PL << ",\"stages\":" << fh.nstages << ",\"staging_bufs\":" << fh.nout
+        << ",\"direct_stores\":" << (R.D->use_ds[ti] ? "true" : "false")
         << ",\"groups\":" << R.D->fl[ti].NG << ",\"classes\":[" << fh.cls_off[1] - fh.cls_off[0] << ","
         << fh.cls_off[2] - fh.cls_off[1] << "," << fh.cls_off[3] - fh.cls_off[2] << "," << fh.cls_off[4] - fh.cls_off[3]
         << "],\"g\":[" << R.D->fl[ti].g1 << "," << R.D->fl[ti].g2 << "],\"slen\":[";

@@ -1,0 +1,8 @@
+set -u
+mkdir -p gpurun_out
+O=gpurun_out/sweep_r03n.txt; : > $O
+run() { local wl=$1; shift; env "$@" timeout 300 python scripts/sweep_one.py $wl "$*" >> $O 2>&1 || echo "$wl [$*] FAILED" >> $O; }
+run c4 X=0; run c4 GBE_FAST_DS=0; SWEEP_IB=16 run c3 X=0; SWEEP_IB=16 run c3 GBE_FAST_DS=0; run c4d4 X=0
+cat $O
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_ringwrap.py tests/test_gpu_merge.py -q -x > gpurun_out/pytest_r03n.log 2>&1; tail -3 gpurun_out/pytest_r03n.log
+timeout 900 python -m pytest tests/test_gpu_configs.py -q -x -k "c4_full" > gpurun_out/pytest_r03n2.log 2>&1; tail -3 gpurun_out/pytest_r03n2.log

@@ -22,4 +22,4 @@ for i in range(14):
 ks, tasks = best
 top = sorted(tasks, key=lambda t: -t["ms"])[:10]
 print(f"{wl} [{tag}] sum {ks:.2f} ms | " + " ".join(
-    f"x{t['var']}={t['ms']:.3f}{('S' if t.get('staged') else 's') if t['variant'] == 2 else ''}{'/' + str(t.get('tile_rows')) if t.get('tile_rows') else ''}" for t in top), flush=True)
+    f"x{t['var']}={t['ms']:.3f}{('S' if t.get('staged') else 's') if t['variant'] == 2 else ''}{'/' + str(t.get('tile_rows')) if t.get('tile_rows') else ''}{'D' + str(t['stages']) if t.get('direct_stores') else ''}" for t in top), flush=True)
