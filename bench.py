@@ -261,7 +261,7 @@ def main():
             r = step(pl)
             warm += 1
             post = 0 if r[2].get("autotune_solve") else post + 1
-            if warm >= max(args.warmup, 3) + 12:
+            if warm >= max(args.warmup, 3) + 24:
                 break
         warmups.append(warm)
         gdist.barrier(pg)

@@ -23,7 +23,10 @@
 //    warps) and per thread group (a shared-memory offset table built once per
 //    CTA): no per-row div/mod.
 //  * Output rows and argmins are staged in shared memory (2-3 buffers per
-//    group) and written by TMA bulk stores issued by the storer warp.
+//    group) and written by TMA bulk stores issued by the storer warp; or,
+//    in the direct-store mode (DS, a per-bucket autotuning candidate), the
+//    consumers write them straight to global memory and the staging
+//    buffers' shared memory becomes ring stages.
 //  * Tile order: the output digits missing from the largest input vary
 //    fastest, so tiles that re-read the same input slice run back to back and
 //    hit L2 instead of HBM.

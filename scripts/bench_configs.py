@@ -38,7 +38,7 @@ def measure(name, inst, order, ib, exact_value_only=False, oracle_threads=(), **
             return pl.solve_mbe(stats=stats, assignment=not exact_value_only)
         return pl.solve_be(stats=stats, assignment=not exact_value_only)
 
-    for _ in range(12):  # warm-up: lazy module loading, the autotuning solves
+    for _ in range(18):  # warm-up: lazy module loading, the autotuning solves
         solve(plan_t)
     r = solve(plan_t, stats=True)
     st = r[-1]
@@ -48,7 +48,7 @@ def measure(name, inst, order, ib, exact_value_only=False, oracle_threads=(), **
     big = [t for t in tasks if t["cells"] >= 1e8]
     del plan_t
     plan = G.Plan(P, order, ib, **opts)
-    for _ in range(12):  # autotuning solves, graph capture
+    for _ in range(18):  # autotuning solves, graph capture
         solve(plan)
     walls = []
     for _ in range(5):

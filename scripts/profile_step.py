@@ -17,7 +17,7 @@ ap.add_argument("--workload", default="c4")
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--which-fast", action="store_true")
 ap.add_argument("--var", type=int, default=-1)
-ap.add_argument("--warm", type=int, default=10)
+ap.add_argument("--warm", type=int, default=24)
 ap.add_argument("--no-autotune", action="store_true")  # default variants (ncu -s indices then count from the start)
 a = ap.parse_args()
 inst = {"c4": configs.c4, "c2": configs.c2, "c5": configs.c5, "c5sp": configs.c5, "c4d4": configs.c4d4}[a.workload]()

@@ -13,9 +13,9 @@ order = configs.c3_order() if wl == "c3" else P.order()[0]
 ib = int(os.environ.get("SWEEP_IB", "-1"))
 plan = G.Plan(P, order, ib, resident_inputs=True, timing=True)
 best = None
-for i in range(14):
+for i in range(20):
     run, root = plan.dpop_util(); run.value(); st = run.stats(); run.close()
-    if i >= 11:
+    if i >= 16:
         ks = sum(t["ms"] for t in st["tasks"])
         if best is None or ks < best[0]:
             best = (ks, st["tasks"])
